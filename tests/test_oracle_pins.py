@@ -1,0 +1,400 @@
+"""Pins for the fp64 oracle against what the paper and the mathematics fix.
+
+None of these retype the oracle's formulas: each compares against an independent
+fact -- a closed form, a printed example (tests/golden, with citations), a moment
+system, an analytic Green's function, a convergence order, the adjoint identity the
+paper states, or the Taylor expansion of the objective.
+"""
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ----------------------------------------------------------------------------- weights
+def closed_form_weights(r):
+    """w_k = 2 (-1)^{k+1} (r!)^2 / (k^2 (r-k)! (r+k)!), w_0 = -2 sum w_k (exact)."""
+    w = [Fraction(0)] * (r + 1)
+    for k in range(1, r + 1):
+        w[k] = Fraction(2 * (-1) ** (k + 1) * math.factorial(r) ** 2,
+                        k * k * math.factorial(r - k) * math.factorial(r + k))
+    w[0] = -2 * sum(w[1:])
+    return w
+
+
+@pytest.mark.parametrize("so", [2, 4, 6, 8, 10, 12, 14, 16])
+def test_fd_weights_closed_form(so):
+    r = so // 2
+    exact = closed_form_weights(r)
+    got = oracle.fd_weights(so)
+    ref = np.array([float(x) for x in exact])
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("so", [2, 4, 6, 8, 10, 12, 14, 16])
+def test_fd_weights_moments(so):
+    """Taylor moment system: sum_j w_j j^m = 2 [m == 2], m = 0..so+1
+    (even m only are nontrivial; odd moments vanish by symmetry)."""
+    r = so // 2
+    w = oracle.fd_weights(so)
+    full = np.concatenate([w[:0:-1], w])           # offsets -r..r
+    offs = np.arange(-r, r + 1, dtype=np.float64)
+    for mom in range(0, so + 2):
+        val = np.sum(full * offs ** mom)
+        target = 2.0 if mom == 2 else 0.0
+        assert abs(val - target) <= 1e-9 * max(1.0, float(np.sum(np.abs(full * offs ** mom))))
+    # the first moment beyond the order must NOT vanish (order is exactly so)
+    assert abs(np.sum(full * offs ** (so + 2))) > 1e-6
+
+
+def test_fd_weights_spec_golden():
+    with open(os.path.join(GOLD, "fd_weights_spec.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            so, rest = line.split(":")
+            so = int(so)
+            ref = np.array([float(Fraction(x)) for x in rest.split()])
+            w = oracle.fd_weights(so)
+            full = np.concatenate([w[:0:-1], w])
+            np.testing.assert_allclose(full, ref, rtol=0, atol=1e-14)
+
+
+def test_fd_weights_symmetry_sum_zero():
+    for so in range(2, 17, 2):
+        w = oracle.fd_weights(so)
+        full = np.concatenate([w[:0:-1], w])
+        assert abs(full.sum()) < 1e-12
+        np.testing.assert_array_equal(full, full[::-1])
+
+
+# ------------------------------------------------------------------------- laplacian MMS
+@pytest.mark.parametrize("so", [2, 4, 6, 8, 10, 12, 14, 16])
+def test_laplacian_mms_order(so):
+    """Operator convergence on f = sin(x) sin(0.8y) sin(0.6z), Lap f = -2 f, at points
+    farther than r from the (zero-halo) boundary; observed order >= 0.95 so."""
+    r = so // 2
+    errs = []
+    hs = []
+    for ppw in (8, 12) if so >= 6 else (8, 16):
+        h = 2 * math.pi / ppw
+        n = 2 * r + 7
+        g = (np.arange(n) - n // 2) * h + 0.3
+        X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+        f = np.sin(X) * np.sin(0.8 * Y) * np.sin(0.6 * Z)
+        L = oracle.laplacian(f, h, so)
+        sl = (slice(r, n - r),) * 3
+        errs.append(np.max(np.abs(L[sl] - (-2.0) * f[sl])))
+        hs.append(h)
+    order = math.log(errs[0] / errs[1]) / math.log(hs[0] / hs[1])
+    assert order >= 0.95 * so, (order, errs)
+
+
+def test_laplacian_2d_matches_second_difference():
+    """so=2, 2D: L_h u = (u_{i+1,j}+u_{i-1,j}+u_{i,j+1}+u_{i,j-1}-4u)/h^2 with zero halo."""
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal((7, 9))
+    up = np.pad(u, 1)
+    ref = (up[2:, 1:-1] + up[:-2, 1:-1] + up[1:-1, 2:] + up[1:-1, :-2] - 4 * u) / 4.0
+    np.testing.assert_allclose(oracle.laplacian(u, 2.0, 2), ref, rtol=0, atol=1e-13)
+
+
+# ----------------------------------------------------------------------- interpolation
+def test_interp_weights_spec_golden():
+    with open(os.path.join(GOLD, "interp_weights_spec.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            a, b = line.split(":")
+            xi = [float(x) for x in a.split()]
+            ref = np.array([float(x) for x in b.split()])
+            h = 10.0
+            coord = np.array([(3 + xi[0]) * h, (5 + xi[1]) * h])
+            idx, W = oracle.point_stencil((9, 11), h, coord)
+            np.testing.assert_allclose(W, ref, atol=1e-15)
+            # corner order (00, 01, 10, 11): last axis fastest
+            np.testing.assert_array_equal(idx, [3 * 11 + 5, 3 * 11 + 6, 4 * 11 + 5, 4 * 11 + 6])
+
+
+def test_interp_clamp_and_out_of_domain():
+    idx, W = oracle.point_stencil((5, 6), 1.0, np.array([4.0, 5.0]))   # last node
+    assert W[-1] == 1.0 and idx[-1] == 4 * 6 + 5 and np.all(W[:-1] == 0)
+    for bad in ([-1e-9, 1.0], [4.0 + 1e-9, 1.0], [1.0, 5.5]):
+        with pytest.raises(oracle.OracleError):
+            oracle.point_stencil((5, 6), 1.0, np.array(bad))
+
+
+def test_interp_partition_and_linear_reproduction():
+    rng = np.random.default_rng(11)
+    for nd in (2, 3):
+        shape = (6, 7, 8)[:nd]
+        h = 2.5
+        pts = rng.uniform(0, 1, (40, nd)) * (np.array(shape) - 1) * h
+        ones = np.ones(shape)
+        np.testing.assert_allclose(oracle.interpolate(pts, ones, h), 1.0, atol=1e-14)
+        grids = np.meshgrid(*[np.arange(s) * h for s in shape], indexing="ij")
+        a = rng.standard_normal(nd)
+        f = 0.7 + sum(a[i] * grids[i] for i in range(nd))
+        ref = 0.7 + pts @ a
+        np.testing.assert_allclose(oracle.interpolate(pts, f, h), ref, atol=1e-12)
+
+
+def test_interp_inject_adjoint_bruteforce():
+    """<P g, r> = <g, P^T r> for 50 random configurations,
+    plus the dense matrices of P and P^T are exact transposes (brute force)."""
+    rng = np.random.default_rng(0)
+    for trial in range(50):
+        nd = 2 + trial % 2
+        shape = tuple(rng.integers(3, 7, nd))
+        h = float(rng.uniform(0.5, 3.0))
+        npnt = int(rng.integers(1, 6))
+        pts = rng.uniform(0, 1, (npnt, nd)) * (np.array(shape) - 1) * h
+        g = rng.standard_normal(shape)
+        rr = rng.standard_normal(npnt)
+        lhs = np.dot(oracle.interpolate(pts, g, h), rr)
+        rhs = np.sum(g * oracle.inject(pts, rr, np.zeros(shape), h))
+        assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+        if trial < 6:
+            N = int(np.prod(shape))
+            P = np.stack([oracle.interpolate(pts, np.eye(N)[j].reshape(shape), h)
+                          for j in range(N)], axis=1)
+            PT = np.stack([oracle.inject(pts, np.eye(npnt)[i], np.zeros(shape), h).ravel()
+                           for i in range(npnt)], axis=1)
+            np.testing.assert_allclose(P.T, PT, atol=1e-15)
+
+
+# ------------------------------------------------------------------------- propagation
+def _dot_test(ndim, shape, so, nbl, seed=0, nt=120):
+    prob = synth.random_problem(ndim, shape, so, nt, seed=seed, nbl=nbl, nsrc=2, nrec=7,
+                                random_wavelet=True)
+    rng = np.random.default_rng(seed + 100)
+    x = rng.standard_normal((nt, 2))
+    y = rng.standard_normal((nt, 7))
+    Fx = oracle.forward(prob, wavelet=x)["rec"]
+    FTy = oracle.adjoint(prob, res=y)["srca"]
+    a, b = np.sum(Fx * y), np.sum(x * FTy)
+    return abs(a - b) / abs(a)
+
+
+@pytest.mark.parametrize("ndim,shape,so,nbl", [
+    (2, (41, 37), 2, 8), (2, (41, 37), 4, 8), (2, (33, 30), 16, 6), (3, (30, 28, 26), 8, 6)])
+def test_adjoint_dot_product_fp64(ndim, shape, so, nbl):
+    """<F x, y> = <x, F^T y> to < 1e-10 in fp64 (north_star),
+    with damping on, random x (wavelets) and random y (records) (reading C19)."""
+    assert _dot_test(ndim, shape, so, nbl) < 1e-10
+
+
+def test_zero_source_zero_field():
+    prob = synth.random_problem(2, (30, 31), 4, 50, seed=2, nbl=5)
+    out = oracle.forward(prob, wavelet=np.zeros((50, 2)))
+    assert np.all(out["rec"] == 0) and np.all(out["u_state"] == 0)
+
+
+def test_constant_preserved_in_interior():
+    """eta = 0, no source, u^{-1} = u^0 = c: L_h c = 0 away from the zero halo, so the
+    field stays c at points farther than r*steps from the boundary (invariant)."""
+    so, nt = 4, 6
+    prob = synth.random_problem(3, (30, 30, 30), so, nt, seed=5, nbl=0, damp=False)
+    st = np.full((2, 30, 30, 30), 1.7)
+    out = oracle.forward(prob, wavelet=np.zeros((nt, 2)), u_state=st)
+    k = (so // 2) * nt
+    core = out["u_state"][1][k:-k, k:-k, k:-k]
+    np.testing.assert_allclose(core, 1.7, rtol=0, atol=1e-12)
+
+
+# ------------------------------------------------------------- analytic Green's functions
+def green2d(t, r, v, h, f0):
+    """u(r,t) = (h^2 / 2pi) int_0^{acosh(vt/r)} w(t - (r/v) cosh th) dth for vt > r:
+    the 2D Green's function of u_tt - v^2 Lap u = v^2 h^2 w(t) delta(x) (the discrete
+    injection src*dt^2/m at one node, is a point source of strength h^2 w)."""
+    from scipy.integrate import quad
+    t0 = 1.0 / f0
+
+    def w(tt):
+        a = (math.pi * f0 * (tt - t0)) ** 2
+        return (1 - 2 * a) * math.exp(-a)
+
+    out = np.zeros_like(t)
+    for i, ti in enumerate(t):
+        if v * ti <= r:
+            continue
+        th = math.acosh(v * ti / r)
+        val, _ = quad(lambda s: w(ti - (r / v) * math.cosh(s)), 0.0, th, limit=200)
+        out[i] = h * h / (2 * math.pi) * val
+    return out
+
+
+def _green2d_run(h, so, courant, half, T, offsets, f0=10.0, v=1500.0):
+    n = int(round(2 * half / h)) + 1
+    dt = courant * h / v
+    nt = int(round(T / dt)) + 1
+    c = (n - 1) // 2 * h
+    m = np.full((n, n), 1.0 / v ** 2, dtype=np.float64)
+    src = np.array([[c, c]])
+    rec = np.array([[c + o, c] for o in offsets])
+    wav = synth.ricker(nt, dt, f0).astype(np.float64)[:, None]
+    # float64 Ricker for the analytic comparison (synth returns fp32; recompute in fp64)
+    t = np.arange(nt) * dt
+    a = (math.pi * f0 * (t - 1.0 / f0)) ** 2
+    wav = ((1 - 2 * a) * np.exp(-a))[:, None]
+    out = oracle.forward(m=m, damp=None, shape=(n, n), h=h, space_order=so, nt=nt, dt=dt,
+                         src_coords=src, wavelet=wav, rec_coords=rec)
+    refs = [green2d(t, o, v, h, f0) for o in offsets]
+    errs = [np.linalg.norm(out["rec"][:, i] - refs[i]) / np.linalg.norm(refs[i])
+            for i in range(len(offsets))]
+    return errs
+
+
+def test_green_function_2d():
+    """Source normalisation and time alignment (readings C3/C4/C10): so4, h = 10 m,
+    Courant 0.4, 10 Hz; relative L2 <= 3e-2 at 200 and 400 m offset (no reflections)."""
+    errs = _green2d_run(10.0, 4, 0.4, 2300.0, 1.0, [200.0, 400.0])
+    assert max(errs) <= 3e-2, errs
+
+
+def test_temporal_order_2d():
+    """Second order in time: errors vs the analytic solution at Courant 0.4/0.2/0.1
+    (so8, h=10) fall by ~4x per halving (3.6-4.4)."""
+    e = [_green2d_run(10.0, 8, c, 900.0, 0.55, [300.0])[0] for c in (0.4, 0.2, 0.1)]
+    r1, r2 = e[0] / e[1], e[1] / e[2]
+    assert 3.6 <= r1 <= 4.4 and 3.6 <= r2 <= 4.4, e
+
+
+@pytest.mark.slow
+def test_spatial_order_2d_analytic():
+    """Spatial order on the analytic solution (north_star): dt fixed at Courant 0.05
+    of the finest h; h = 20/10/5 m: ratios >= 0.85 * 2^so for so = 2, 4."""
+    for so in (2, 4):
+        errs = []
+        for h in (20.0, 10.0, 5.0):
+            courant = 0.05 * h / 5.0
+            errs.append(_green2d_run(h, so, courant, 900.0, 0.55, [300.0])[0])
+        ratios = [errs[0] / errs[1], errs[1] / errs[2]]
+        assert min(ratios) >= 0.85 * 2 ** so, (so, errs)
+
+
+def test_green_function_3d():
+    """3D: u = h^3 w(t - r/v) / (4 pi r); so8, h=10, 10 Hz, Courant 0.4, 101^3,
+    T = 0.42 s; relative L2 <= 3e-2 at 150 m and 141 m (diagonal); peaks within 1%."""
+    n, h, v, f0 = 101, 10.0, 1500.0, 10.0
+    dt = 0.4 * h / v
+    nt = int(round(0.42 / dt)) + 1
+    c = 50 * h
+    m = np.full((n, n, n), 1.0 / v ** 2)
+    t = np.arange(nt) * dt
+    a = (math.pi * f0 * (t - 1.0 / f0)) ** 2
+    wav = ((1 - 2 * a) * np.exp(-a))[:, None]
+    rec = np.array([[c + 150.0, c, c], [c + 100.0, c + 100.0, c]])
+    out = oracle.forward(m=m, damp=None, shape=(n, n, n), h=h, space_order=8, nt=nt, dt=dt,
+                         src_coords=np.array([[c, c, c]]), wavelet=wav, rec_coords=rec)
+    for i, rr in enumerate([150.0, math.hypot(100.0, 100.0)]):
+        ta = t - rr / v
+        aa = (math.pi * f0 * (ta - 1.0 / f0)) ** 2
+        ref = h ** 3 * (1 - 2 * aa) * np.exp(-aa) / (4 * math.pi * rr)
+        num = out["rec"][:, i]
+        err = np.linalg.norm(num - ref) / np.linalg.norm(ref)
+        assert err <= 3e-2, (rr, err)
+        assert abs(num.max() - ref.max()) <= 1e-2 * ref.max()
+        # first arrival (Ricker peak) at r/v + t0 within 2 dt
+        assert abs(t[np.argmax(num)] - (rr / v + 1.0 / f0)) <= 2 * dt
+
+
+# --------------------------------------------------------------------------- gradient
+def _taylor_problem():
+    nx, nz, nbl, h = 46, 40, 8, 10.0
+    z = np.arange(nz) * h
+    v0 = np.where(z < 200.0, 1500.0, 2000.0)[None, :].repeat(nx, 0)
+    X, Z = np.meshgrid(np.arange(nx) * h, z, indexing="ij")
+    vt = v0 + 300.0 * np.exp(-((X - 230.0) ** 2 + (Z - 260.0) ** 2) / (2 * 60.0 ** 2))
+    vmax = vt.max()
+    sig = synth.damping_profile((nx, nz), nbl, h, vmax)
+    m0 = 1.0 / v0 ** 2
+    mt = 1.0 / vt ** 2
+    dt = 0.4 * h / vmax
+    nt = 300
+    src = np.array([[230.0, (nbl + 1) * h]])
+    rec = np.stack([np.linspace((nbl + 1) * h, (nx - nbl - 2) * h, 28),
+                    np.full(28, (nbl + 1) * h)], axis=1)
+    t = np.arange(nt) * dt
+    a = (math.pi * 15.0 * (t - 1 / 15.0)) ** 2
+    wav = ((1 - 2 * a) * np.exp(-a))[:, None]
+    base = dict(shape=(nx, nz), h=h, space_order=4, nt=nt, dt=dt, src_coords=src,
+                wavelet=wav, rec_coords=rec)
+    # damping eta = m0 * sigma is held fixed while m varies (reading C13)
+    eta = m0 * sig
+    return base, m0, mt, eta
+
+
+def test_taylor_gradient_fp64():
+    """J(m0 + e dm) - J(m0) = O(e) and - e <g, dm> leaves O(e^2): ratios of successive
+    residuals as e halves are ~2 and ~4 ([1.9, 2.1] and [3.6, 4.4]) (north_star)."""
+    base, m0, mt, eta = _taylor_problem()
+    d_obs = oracle.forward(m=mt, damp=eta, **base)["rec"]
+
+    def J(m):
+        r = oracle.forward(m=m, damp=eta, **base)["rec"] - d_obs
+        return 0.5 * np.sum(r * r)
+
+    fw = oracle.forward(m=m0, damp=eta, save_every=1, **base)
+    res = fw["rec"] - d_obs
+    ad = oracle.adjoint(m=m0, damp=eta, res=res, save_every=1, snaps=fw["snaps"],
+                        **{k: v for k, v in base.items() if k != "wavelet"})
+    g = ad["grad"]
+    dm = mt - m0
+    J0 = 0.5 * np.sum(res * res)
+    gd = np.sum(g * dm)
+    r1, r2 = [], []
+    for e in (0.1, 0.05, 0.025, 0.0125):
+        Je = J(m0 + e * dm)
+        r1.append(abs(Je - J0))
+        r2.append(abs(Je - J0 - e * gd))
+    q1 = [r1[i] / r1[i + 1] for i in range(3)]
+    q2 = [r2[i] / r2[i + 1] for i in range(3)]
+    assert all(1.9 <= q <= 2.1 for q in q1), q1
+    assert all(3.6 <= q <= 4.4 for q in q2), q2
+
+
+def test_gradient_subsampled_consistent():
+    """k-subsampled correlation (reading C14) approximates the full one: cosine > 0.999."""
+    base, m0, mt, eta = _taylor_problem()
+    d_obs = oracle.forward(m=mt, damp=eta, **base)["rec"]
+    gs = []
+    for k in (1, 4):
+        fw = oracle.forward(m=m0, damp=eta, save_every=k, **base)
+        ad = oracle.adjoint(m=m0, damp=eta, res=fw["rec"] - d_obs, save_every=k,
+                            snaps=fw["snaps"],
+                            **{kk: v for kk, v in base.items() if kk != "wavelet"})
+        gs.append(ad["grad"].ravel())
+    cos = np.dot(gs[0], gs[1]) / np.linalg.norm(gs[0]) / np.linalg.norm(gs[1])
+    assert cos > 0.999
+
+
+def test_damping_term_closed_form():
+    """Uniform m and eta, zero Laplacian in the interior: the leapfrog of
+    m u_tt + eta u_t = 0 (centred u_t, reading C1) has the closed-form solution
+    u^n = A + B lam^n, lam = (m - eta dt/2)/(m + eta dt/2), from u^{-1} = 0, u^0 = 1.
+    Pins the sign and placement of every damping coefficient."""
+    n, so, nt = 24, 4, 4
+    mval, eta_val, dt, h = 1.0 / 2000.0 ** 2, 30.0 / 2000.0 ** 2, 2e-3, 10.0
+    m = np.full((n, n, n), mval)
+    eta = np.full((n, n, n), eta_val)
+    st = np.zeros((2, n, n, n))
+    st[1] = 1.0
+    out = oracle.forward(m=m, damp=eta, shape=(n, n, n), h=h, space_order=so, nt=nt, dt=dt,
+                         src_coords=None, wavelet=None, rec_coords=None, u_state=st)
+    a = eta_val * dt / 2
+    lam = (mval - a) / (mval + a)
+    B = 1.0 / (1.0 - 1.0 / lam)
+    A = 1.0 - B
+    k = (so // 2) * nt
+    core = out["u_state"][1][k:-k, k:-k, k:-k]
+    np.testing.assert_allclose(core, A + B * lam ** (nt - 1), rtol=1e-13)
+    prev = out["u_state"][0][k:-k, k:-k, k:-k]
+    np.testing.assert_allclose(prev, A + B * lam ** (nt - 2), rtol=1e-13)
