@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""bench.py -- GPts/s of the acoustic FD forward on BASELINE configs[1] (3D 256^3
+physical + 40-pt absorbing layer = 336^3 computational grid, space order 8, nt=1000,
+two-layer model, 15 Hz Ricker at the surface centre, 256x256 surface receivers).
+
+One "step" = one complete forward propagation (nt-1 = 999 leapfrog updates of every
+grid point, each with source injection and receiver interpolation) through the C-ABI
+(sf_forward) from a zero initial state.  value = N_points * (nt-1) * steps * n_gpus /
+max-over-ranks device time  [GPts/s = 1e9 grid-point updates per second].
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): weak scaling -- the grid is slab-decomposed along x
+with 336 planes per rank (global 336N x 336 x 336) and r=4 halo planes exchanged every
+step with NCCL send/recv.  --impl reference runs the fp64 CPU oracle (the only
+"reference" this paper-only build has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GPts/s (grid-point updates/s) at 1/2/4/8 B200, % of HBM roofline"
+UNIT = "GPts/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the stencil kernel from the committed ncu --set full
+    capture summary (profiles/stencil_ncu_summary.json), or None."""
+    path = os.path.join(ROOT, "profiles", "stencil_ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"clocks_{os.getpid()}.csv")
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                c = [x.strip() for x in line.split(",")]
+                if len(c) < 9:
+                    continue
+                try:
+                    sm.append(float(c[1]))
+                    smax = float(c[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, c[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- workload
+def build_problem(nt_override=None, rank=0, nranks=1):
+    import synth
+    p = synth.make_config(1, nt=nt_override)
+    if nranks == 1:
+        return p, p.m, p.damp, p.shape
+    # weak scaling: global grid (336 N) x 336 x 336 = the configs[1] model tiled along x
+    # (its physical part is x-invariant); the absorbing layer stays at the global x edges.
+    r = p.space_order // 2
+    n0 = p.shape[0]
+    gshape = (n0 * nranks,) + p.shape[1:]
+    import synth as S
+    vmax = 2500.0
+    sig = S.damping_profile(gshape, p.nbl, p.h, vmax)   # only a 1D x-profile part differs
+    x0 = rank * n0
+    lo, hi = x0 - r, x0 + n0 + r
+    idx = np.clip(np.arange(lo, hi), 0, gshape[0] - 1)
+    m_col = p.m[0]  # every x-plane of the padded configs[1] model is identical
+    m_loc = np.ascontiguousarray(np.broadcast_to(m_col, (hi - lo,) + p.shape[1:]), dtype=np.float32)
+    eta_loc = (m_loc.astype(np.float64) * sig[idx]).astype(np.float32)
+    src = p.src_coords.copy()
+    src[:, 0] = gshape[0] * p.h / 2.0
+    rec = p.rec_coords.copy()
+    rec[:, 0] = rec[:, 0] + (nranks - 1) * n0 * p.h / 2.0
+    p.src_coords, p.rec_coords = src, rec
+    return p, m_loc, eta_loc, gshape
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1707_03776_b200 as sf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [sf.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = sf.nccl_comm_init(uid[0], world, rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    p, m_loc, eta_loc, gshape = build_problem(args.nt, rank, world)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+    m_d, eta_d = dev(m_loc), dev(eta_loc)
+    prop = sf.Propagator(m_d, eta_d, shape=gshape, h=p.h, space_order=p.space_order, nt=p.nt,
+                         dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords,
+                         comm=comm, rank=rank, nranks=world)
+    wav = dev(p.wavelet)
+    u = prop.zeros_state()
+    rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
+    npts_local = int(np.prod(prop.local_shape)) if world == 1 else prop.n0_loc * int(np.prod(gshape[1:]))
+    tuning = prop.tuning()
+    log(f"[bench] rank {rank}/{world} grid {gshape} local {prop.local_shape} nt {p.nt} tuning {tuning}")
+
+    def step():
+        u.zero_()
+        prop.forward(wav, u=u, rec=rec)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    prop.set_profiling(True)
+    prop.profile(reset=True)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    prop.set_profiling(False)
+    ms = e0.elapsed_time(e1)
+    prof = prop.profile(reset=True)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    updates = npts_local * world * (p.nt - 1) * args.steps
+    value = updates / (ms_max * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (stencil step): algorithmic bytes per launch
+    bpp = 20 if eta_loc is not None else 16      # u^n, u^{n-1}, out, c3(+beta) fp32
+    launch_ms = prof["stencil_ms"] / max(prof["stencil_launches"], 1)
+    alg_bytes = bpp * npts_local
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    traffic, _ = ncu_traffic()
+
+    result = None
+    if rank == 0:
+        # end to end through the public C-ABI with HOST buffers (pinned), N=1 form
+        e2e = None
+        if world == 1 and not args.no_e2e:
+            e2e = run_e2e(p, args)
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(p, args.cpu_seconds)
+        result = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded configs[1] model: two layers, 40-pt quadratic damping layer, "
+                    "15 Hz Ricker; no dataset in the paper)",
+            "config": {"workload": "configs[1]: 3D acoustic forward 256^3 phys + nbl 40 -> "
+                                   f"{'x'.join(map(str, gshape))} comp, so8, nt={p.nt}, "
+                                   f"{p.rec_coords.shape[0]} receivers, 1 source",
+                       "grid": list(gshape), "space_order": p.space_order, "nt": p.nt,
+                       "points_per_rank": npts_local, "parallelism": f"slab{world}" if world > 1 else "1gpu",
+                       "l2": "inputs larger than L2 (each 336^3 fp32 field = 152 MB > 126 MB L2; "
+                             "4 fields streamed per update)",
+                       "kernel_tuning": tuning},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_source": peak_src,
+                         "kernel": "k_tma3d (stencil step, fwd)" if tuning["variant"] == 2 else "k_generic3d",
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "bytes_per_point": bpp, "avg_launch_ms": round(launch_ms, 5),
+                         "stencil_share_of_step": round(prof["stencil_ms"] / max(ms, 1e-9), 4)},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(prof["launches"]),
+            "clocks": clocks,
+        }
+    if world > 1:
+        dist.barrier()
+        sf.nccl_comm_destroy(comm) if comm else None
+        dist.destroy_process_group()
+    return result
+
+
+def run_e2e(p, args):
+    import torch
+
+    import paper_1707_03776_b200 as sf
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).pin_memory()
+    m_h, d_h, w_h = pin(p.m), pin(p.damp), pin(p.wavelet)
+    rec_h = torch.empty((p.nt, p.rec_coords.shape[0]), dtype=torch.float32).pin_memory()
+    call = lambda: sf.forward_host(m_h.numpy(), d_h.numpy(), h=p.h, space_order=p.space_order,
+                                   nt=p.nt, dt=p.dt, src_coords=p.src_coords,
+                                   wavelet=w_h.numpy(), rec_coords=p.rec_coords,
+                                   rec_out=rec_h.numpy())
+    call()  # warm-up (allocates the library's device cache)
+    torch.cuda.synchronize()
+    n = max(1, min(args.steps, 3))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(n):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = max(e0.elapsed_time(e1), wall * 1e3)
+    N = int(np.prod(p.shape))
+    return {"value": round(N * (p.nt - 1) * n / (ms * 1e-3) / 1e9, 3), "unit": UNIT,
+            "h2d_bytes_per_step": int(m_h.numel() * 4 + d_h.numel() * 4 + w_h.numel() * 4),
+            "d2h_bytes_per_step": int(rec_h.numel() * 4), "steps": n,
+            "includes": "H2D m/eta/wavelet, handle setup (coefficient hoist, tables, CFL), "
+                        "forward, D2H record"}
+
+
+def cpu_baseline(p, seconds):
+    """The oracle as it stands (fp64, OpenMP over all host cores) on a bounded sample:
+    the same grid and model, first `k` time steps, k sized to ~`seconds` of CPU work."""
+    import oracle
+    oracle.build()
+    N = int(np.prod(p.shape))
+    probe = 3
+    t0 = time.perf_counter()
+    oracle.forward(p, nt=probe, wavelet=p.wavelet[:probe])
+    tp = time.perf_counter() - t0
+    k = int(max(probe, min(p.nt, (probe - 1) * seconds / max(tp, 1e-3) + 1)))
+    t0 = time.perf_counter()
+    oracle.forward(p, nt=k, wavelet=p.wavelet[:k])
+    t = time.perf_counter() - t0
+    return {"value": round(N * (k - 1) / t / 1e9, 5), "unit": UNIT, "cores": oracle.num_threads(),
+            "kind": "oracle", "seconds": round(t, 2),
+            "sample": f"configs[1] full 336^3 grid, first {k} of {p.nt} time samples "
+                      f"({k - 1} updates), fp64 C oracle"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and rank != 0:
+        return None
+    import oracle
+    import synth
+    oracle.build()
+    p = synth.make_config(1, nt=args.nt)
+    N = int(np.prod(p.shape))
+    k = args.ref_steps_nt
+    for _ in range(args.warmup and 1):
+        oracle.forward(p, nt=2, wavelet=p.wavelet[:2])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.forward(p, nt=k, wavelet=p.wavelet[:k])
+    t = time.perf_counter() - t0
+    v = N * (k - 1) * args.steps / t / 1e9
+    cpu = {"value": round(v, 5), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"configs[1] full 336^3 grid, {k} time samples per step"}
+    return {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t / args.steps * 1e3, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"configs[1] 336^3 so8, bounded sample of {k} of {p.nt} time samples"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(v, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nt", type=int, default=None, help="override nt (default: configs[1] 1000)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-steps-nt", type=int, default=6,
+                    help="--impl reference: time samples per timed step of the oracle")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        res = run_reference(args)
+    else:
+        res = run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

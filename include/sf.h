@@ -1,0 +1,184 @@
+/*
+ * sf.h -- C-ABI of the B200-native acoustic finite-difference propagator (libsf.so).
+ *
+ * The hot path of the seismic example of Lange et al., "Optimised finite difference
+ * computation from symbolic equations" (Devito, SciPy 2017; PAPER.md = the paper's
+ * text, cited P:line):
+ *
+ *   forward:  m u_tt - Lap u + eta u_t = q
+ *            u.forward = solve(m*u.dt2 - u.laplace + eta*u.dt, u.forward)
+ *            src.inject(field=u, expr=src*dt**2/m)
+ *            rec.interpolate(expr=u)
+ *   adjoint:  same stencil run backwards in time (time_axis=Backward),
+ *            eta sign flipped, receivers injected, sources interpolated.
+ *   gradient (BASELINE north_star, not in the paper): g += v * u_tt correlation of
+ *            the adjoint wavefield with saved / subsampled forward wavefields.
+ *
+ * Discretisation (DESIGN.md §3 readings C1-C20):
+ *   A = m + eta dt/2, beta = (m - eta dt/2)/A, c3 = dt^2/A,
+ *   out = cur + beta (cur - old) + c3 * L_h cur,  L_h = centred order-`space_order`
+ *   Laplacian with a zero ghost halo (C6); forward (cur, old) = (u^n, u^{n-1}) -> u^{n+1},
+ *   adjoint (cur, old) = (v^n, v^{n+1}) -> v^{n-1}.  Injection after the stencil into the
+ *   new level with scale dt^2/m (C3, C9); records sample the level just completed (C4).
+ *   Gradient: g -= k * u^n * (v^{n+1} - 2 v^n + v^{n-1}) / dt^2 for n % k == 0 (C13, C14).
+ *
+ * Conventions for every call:
+ *   - Grid arrays: device-resident, caller-owned, contiguous fp32, row-major
+ *     [n0][n1][n2] = [x][y][z] (2D: [x][z]), last axis fastest, exactly N points.
+ *   - Sparse time series: device fp32, time-major [nt][npoint] (C12).
+ *   - Coordinates: HOST fp64 [npoint][ndim], metres from computational index 0;
+ *     a point outside [0, (n-1) h] on any axis is SF_ERR_OUT_OF_DOMAIN (never clipped).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); every call is
+ *     ordered on it and returns without synchronising unless stated.
+ *   - Ownership: the library never frees caller memory.  A handle owns its setup
+ *     tables and its coefficient arrays (beta, c3: 1-2 x N floats), freed by sf_destroy.
+ *   - Errors: every call validates before launching anything and returns an
+ *     sf_status; nothing is thrown across the ABI.  sf_last_error() gives a message
+ *     (thread-local).  A handle is not thread-safe.
+ */
+#ifndef SF_H
+#define SF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SF_API __attribute__((visibility("default")))
+#else
+#define SF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SF_OK = 0,
+    SF_ERR_INVALID_ARG = 1,   /* NULL required pointer, nt < 2, dt <= 0, h <= 0, min m <= 0 */
+    SF_ERR_SHAPE = 2,         /* an extent < 2, or a slab with fewer than r local planes     */
+    SF_ERR_ORDER = 3,         /* space_order odd, < 2 or > 16                                */
+    SF_ERR_CFL = 4,           /* dt * vmax / h > 2 / sqrt(ndim * sum|w|)                      */
+    SF_ERR_OUT_OF_DOMAIN = 5, /* sparse point outside the grid                               */
+    SF_ERR_WORKSPACE = 6,     /* workspace too small                                         */
+    SF_ERR_CUDA = 7,          /* CUDA runtime / driver error                                 */
+    SF_ERR_NCCL = 8           /* NCCL error                                                  */
+} sf_status;
+
+typedef struct {
+    int ndim;                 /* 2 or 3                                                      */
+    int64_t shape[3];         /* computational grid (GLOBAL grid when distributed)            */
+    double h;                 /* isotropic spacing [m]                                       */
+    int space_order;          /* even, 2..16 (r = space_order/2 halo)                         */
+    int nt;                   /* samples t_n = n dt, n = 0..nt-1 (nt-1 updates)                */
+    double dt;                /* [s]                                                          */
+    const float *m;           /* device [N] square slowness s^2/m^2, > 0 (local slab when     */
+                              /* distributed: [n0_loc + 2r][n1][n2], halo planes unused)      */
+    const float *damp;        /* device [N] eta >= 0, or NULL (== 0 everywhere)                */
+    int nsrc;                 /* number of sources (forward injection, adjoint interpolation) */
+    const double *src_coords; /* host [nsrc][ndim]                                            */
+    int nrec;                 /* number of receivers                                          */
+    const double *rec_coords; /* host [nrec][ndim]                                            */
+} sf_desc;
+
+typedef struct sf_handle sf_handle;
+
+/* Centred 2nd-derivative FD weights of order space_order:
+ * w[0] = centre, w[k] = weight at offsets +-k, k = 1..r, in units of 1/h^2. */
+SF_API sf_status sf_fd_weights(int space_order, double *w /* host [r+1] */);
+
+/* Validate (shape, order, CFL, domain), build interpolation / injection tables and the
+ * hoisted coefficient arrays beta and c3 on the device.  Synchronises the device once. */
+SF_API sf_status sf_create(const sf_desc *d, sf_handle **out);
+SF_API void sf_destroy(sf_handle *h);
+
+/* Forward propagation.
+ *   wavelet [nt][nsrc]   source signatures (may be NULL iff nsrc == 0)
+ *   rec     [nt][nrec]   OUT: rec[n] = P u^n (rec[0] = P u^0); may be NULL iff nrec == 0
+ *   u       [2][N]       IN (u^{-1}, u^0) (zeros for a fresh run), OUT (u^{nt-2}, u^{nt-1})
+ *   snaps   [nt_snap][N] or NULL: OUT u^n for n % save_every == 0, slot n/save_every,
+ *                        nt_snap = (nt-1)/save_every + 1 (slot 0 = u^0)
+ *   save_every           >= 1 when snaps != NULL                                      */
+SF_API sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, float *u, float *snaps,
+                     int save_every, void *stream);
+
+/* Adjoint propagation.
+ *   res  [nt][nrec]   injected at the receivers (scale dt^2/m)
+ *   srca [nt][nsrc]   OUT: srca[n] = P_s v^n (srca[nt-1] = P_s v^{nt-1}); may be NULL iff nsrc == 0
+ *   v    [2][N]       IN (v^{nt}, v^{nt-1}) (zeros), OUT (v^1, v^0)
+ *   snaps, save_every as written by sf_forward; with grad != NULL the correlation
+ *   grad -= k u^n (v^{n+1} - 2 v^n + v^{n-1}) / dt^2 (n % k == 0, n >= 1) is ACCUMULATED
+ *   into grad [N] (fused into the stencil kernel).  snaps/grad NULL: no gradient.     */
+SF_API sf_status sf_adjoint(sf_handle *h, const float *res, float *srca, float *v, const float *snaps,
+                     int save_every, float *grad, void *stream);
+
+/* res = d_syn - d_obs ([nt][nrec]) and *J = 1/2 sum res^2 accumulated in fp64 in a fixed
+ * order (deterministic).  J is a HOST pointer; the call synchronises `stream`.        */
+SF_API sf_status sf_residual(sf_handle *h, const float *d_syn, const float *d_obs, float *res,
+                      double *J, void *stream);
+
+/* Full FWI gradient at the handle's m: forward with snapshots every save_every steps,
+ * residual against d_obs, adjoint with fused correlation.  grad [N] is OVERWRITTEN;
+ * *J (host) = 1/2 ||d_syn - d_obs||^2.  ws: device workspace of
+ * sf_gradient_workspace_bytes() bytes (caller-owned). Synchronises `stream` (for J). */
+SF_API size_t sf_gradient_workspace_bytes(const sf_handle *h, int save_every);
+SF_API sf_status sf_gradient(sf_handle *h, const float *wavelet, const float *d_obs, float *grad,
+                      double *J, void *ws, size_t ws_bytes, int save_every, void *stream);
+
+/* Flat end-to-end form with HOST buffers (desc->m / desc->damp are HOST pointers here):
+ * uploads m, damp and the wavelet, creates a handle, runs sf_forward from a zero state,
+ * downloads rec [nt][nrec] and (optionally) u_final [2][N] = (u^{nt-2}, u^{nt-1}).
+ * Uses a library-owned device cache reused across calls with the same sizes.
+ * Synchronises `stream`. */
+SF_API sf_status sf_forward_host(const sf_desc *host_desc, const float *wavelet_host, float *rec_host,
+                          float *u_final_host, void *stream);
+
+/* Profiling: when on, the library records CUDA events around every stencil launch on
+ * the launch stream; sf_get_profile synchronises and returns the summed stencil-kernel
+ * time, the number of stencil launches and of all kernel launches since the last reset. */
+SF_API sf_status sf_set_profiling(sf_handle *h, int on);
+SF_API sf_status sf_get_profile(sf_handle *h, double *stencil_ms, long long *stencil_launches,
+                         long long *all_launches, int reset);
+
+/* Tuning: kernel variant (0 auto, 1 generic thread-per-point, 2 TMA 2.5D streaming),
+ * warps per CTA along y (0 auto, 8 or 16) and x-chunks per column (0 auto). */
+SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int by, int chunks);
+/* Which variant / by / chunks the next launch will use (after auto selection). */
+SF_API sf_status sf_get_tuning(const sf_handle *h, int *variant, int *by, int *chunks);
+
+/* ---- multi-GPU (slab decomposition along axis 0; one process per GPU, NCCL) ---- */
+
+/* Host-only: the slab owned by `rank`: planes [*x0, *x0 + *n0_loc) of the global axis 0.
+ * Needs no GPU.  SF_ERR_SHAPE if a rank would own fewer than r planes.            */
+SF_API sf_status sf_slab_plan(int64_t n0, int space_order, int rank, int nranks, int64_t *x0,
+                       int64_t *n0_loc);
+/* Owner rank of a sparse point for injection corners / records (reading C18): the rank
+ * owning plane floor-clamped base index along axis 0.  Host-only.                  */
+SF_API sf_status sf_sparse_owner(int64_t n0, int space_order, int nranks, double h, double coord0,
+                          int *owner);
+
+/* NCCL bootstrap: rank 0 calls sf_nccl_unique_id, broadcasts the 128 bytes (e.g. over
+ * torch.distributed), every rank calls sf_nccl_comm_init.  The comm is caller-owned. */
+SF_API sf_status sf_nccl_unique_id(char id_out[128]);
+SF_API sf_status sf_nccl_comm_init(const char id[128], int nranks, int rank, void **comm_out);
+SF_API sf_status sf_nccl_comm_destroy(void *comm);
+
+/* Slab handle: `global` holds the GLOBAL shape and sparse geometry; global->m/damp
+ * point to the LOCAL slab arrays [n0_loc + 2r][n1][n2] (halo planes unused).  All
+ * wavefield arrays passed to sf_forward/sf_adjoint are then local [n0_loc + 2r][n1][n2]
+ * (u: [2][...]); records/srca are full [nt][npoint] arrays in which each rank writes the
+ * rows of the points it owns (others are zeroed) -- sum them over ranks.  The halo of
+ * r planes is exchanged every step with ncclSend/ncclRecv over NVLink. */
+SF_API sf_status sf_create_slab(const sf_desc *global, void *nccl_comm, int rank, int nranks,
+                         sf_handle **out);
+/* In-place fp32 sum of grad [Nloc] and fp64 sum of *J (host) over the communicator
+ * (multi-shot FWI, one shot per GPU).  Synchronises `stream`. */
+SF_API sf_status sf_allreduce_gradient(sf_handle *h, void *nccl_comm, float *grad, size_t count,
+                                double *J, void *stream);
+
+SF_API const char *sf_last_error(void);
+SF_API int sf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SF_H */

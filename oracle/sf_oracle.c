@@ -101,31 +101,26 @@ static int64_t npts(int ndim, const int64_t *n)
     return N;
 }
 
-/* zero-halo read of u at integer index i (ndim entries) */
-static inline double at(const double *u, int ndim, const int64_t *n, const int64_t *i)
-{
-    int64_t off = 0;
-    for (int a = 0; a < ndim; ++a) {
-        if (i[a] < 0 || i[a] >= n[a]) return 0.0;
-        off = off * n[a] + i[a];
-    }
-    return u[off];
-}
-
-/* L_h u at the point with multi-index p (reading C6: zero ghost halo). */
-static double lap_point(const double *u, int ndim, const int64_t *n, const int64_t *p,
-                        const double *w, int r, double h)
+/* L_h u at the point with multi-index p and flat offset off (reading C6: zero ghost halo):
+ * sum over axes a and offsets k = -r..r of w_|k| u(p + k e_a), divided by h^2. */
+static double lap_point(const double *u, int ndim, const int64_t *n, const int64_t *stride,
+                        const int64_t *p, int64_t off, const double *w, int r, double h)
 {
     double acc = 0.0;
-    int64_t q[3];
     for (int a = 0; a < ndim; ++a) {
         for (int k = -r; k <= r; ++k) {
-            for (int b = 0; b < ndim; ++b) q[b] = p[b];
-            q[a] = p[a] + k;
-            acc += w[k < 0 ? -k : k] * at(u, ndim, n, q);
+            const int64_t q = p[a] + k;
+            const double val = (q < 0 || q >= n[a]) ? 0.0 : u[off + k * stride[a]];
+            acc += w[k < 0 ? -k : k] * val;
         }
     }
     return acc / (h * h);
+}
+
+static void strides_of(int ndim, const int64_t *n, int64_t *stride)
+{
+    stride[ndim - 1] = 1;
+    for (int a = ndim - 2; a >= 0; --a) stride[a] = stride[a + 1] * n[a + 1];
 }
 
 static void unravel(int ndim, const int64_t *n, int64_t off, int64_t *p)
@@ -142,12 +137,13 @@ int or_laplacian(int ndim, const int64_t *n, double h, int so, const double *u, 
     double w[OR_MAXR + 1];
     if (or_fd_weights(so, w)) return 1;
     int r = so / 2;
-    int64_t N = npts(ndim, n);
+    int64_t N = npts(ndim, n), stride[3];
+    strides_of(ndim, n, stride);
 #pragma omp parallel for schedule(static)
     for (int64_t off = 0; off < N; ++off) {
         int64_t p[3];
         unravel(ndim, n, off, p);
-        out[off] = lap_point(u, ndim, n, p, w, r, h);
+        out[off] = lap_point(u, ndim, n, stride, p, off, w, r, h);
     }
     return 0;
 }
@@ -221,16 +217,23 @@ static void leapfrog(int ndim, const int64_t *n, double h, const double *w, int 
                      const double *m, const double *damp, const double *cur, const double *prv,
                      double *nxt)
 {
-    int64_t N = npts(ndim, n);
+    int64_t stride[3];
+    strides_of(ndim, n, stride);
+    const int64_t rows = npts(ndim, n) / n[ndim - 1];  /* all axes but the last */
+    const int64_t nl = n[ndim - 1];
 #pragma omp parallel for schedule(static)
-    for (int64_t off = 0; off < N; ++off) {
+    for (int64_t row = 0; row < rows; ++row) {
         int64_t p[3];
-        unravel(ndim, n, off, p);
-        double L = lap_point(cur, ndim, n, p, w, r, h);
-        double eta = damp ? damp[off] : 0.0;
-        double mm = m[off];
-        nxt[off] = (2.0 * mm * cur[off] - (mm - 0.5 * eta * dt) * prv[off] + dt * dt * L)
-                   / (mm + 0.5 * eta * dt);
+        unravel(ndim, n, row * nl, p);
+        for (int64_t i = 0; i < nl; ++i) {
+            const int64_t off = row * nl + i;
+            p[ndim - 1] = i;
+            double L = lap_point(cur, ndim, n, stride, p, off, w, r, h);
+            double eta = damp ? damp[off] : 0.0;
+            double mm = m[off];
+            nxt[off] = (2.0 * mm * cur[off] - (mm - 0.5 * eta * dt) * prv[off] + dt * dt * L)
+                       / (mm + 0.5 * eta * dt);
+        }
     }
 }
 

@@ -1,0 +1,16 @@
+"""paper_1707_03776_b200 -- B200-native acoustic finite-difference propagator.
+
+The data-parallel hot path of the seismic example of Lange et al., "Optimised finite
+difference computation from symbolic equations" (Devito, SciPy 2017): the explicit
+leapfrog update of m u_tt - Lap u + eta u_t = q at space orders 2-16 with source
+injection and receiver interpolation, its adjoint, and the FWI gradient correlation
+-- hand-written CUDA for sm_100a behind the C-ABI of include/sf.h (libsf.so), with
+NCCL slab halos / gradient all-reduce for multiple GPUs.
+
+This package never imports ``oracle`` (the fp64 CPU reference used by the tests).
+"""
+from ._lib import EXPORTS, LIB_PATH, SfError, build, lib  # noqa: F401
+from .api import (Propagator, allreduce_gradient, fd_weights, forward_host,  # noqa: F401
+                  nccl_comm_destroy, nccl_comm_init, nccl_unique_id, slab_plan, sparse_owner)
+
+__version__ = "0.1.0"

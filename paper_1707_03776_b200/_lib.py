@@ -1,0 +1,103 @@
+"""ctypes loader for the in-tree ``libsf.so`` (the C-ABI of include/sf.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA
+kernels.  There is no fallback -- if the shared library is missing or fails to
+load, importing the package's compute API raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsf.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+STATUS = {0: "SF_OK", 1: "SF_ERR_INVALID_ARG", 2: "SF_ERR_SHAPE", 3: "SF_ERR_ORDER",
+          4: "SF_ERR_CFL", 5: "SF_ERR_OUT_OF_DOMAIN", 6: "SF_ERR_WORKSPACE", 7: "SF_ERR_CUDA",
+          8: "SF_ERR_NCCL"}
+
+# every symbol include/sf.h declares
+EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint", "sf_residual",
+           "sf_gradient_workspace_bytes", "sf_gradient", "sf_forward_host", "sf_set_profiling",
+           "sf_get_profile", "sf_set_tuning", "sf_get_tuning", "sf_slab_plan", "sf_sparse_owner",
+           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_create_slab",
+           "sf_allreduce_gradient", "sf_last_error", "sf_version"]
+
+
+class SfError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+        super().__init__(f"{self.status}: {msg}")
+
+
+class SfDesc(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int), ("shape", ctypes.c_int64 * 3), ("h", ctypes.c_double),
+                ("space_order", ctypes.c_int), ("nt", ctypes.c_int), ("dt", ctypes.c_double),
+                ("m", ctypes.c_void_p), ("damp", ctypes.c_void_p), ("nsrc", ctypes.c_int),
+                ("src_coords", ctypes.c_void_p), ("nrec", ctypes.c_int),
+                ("rec_coords", ctypes.c_void_p)]
+
+
+def build(force: bool = False, jobs: int = 8) -> str:
+    """Compile libsf.so in-tree with nvcc for sm_100a (make -C csrc)."""
+    args = ["make", "-C", CSRC, f"-j{jobs}"]
+    if force:
+        subprocess.check_call(["make", "-C", CSRC, "clean"])
+    subprocess.check_call(args)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built (run __graft_entry__.build() or make -C {CSRC}); "
+                              "the CUDA extension is required -- there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I, D, Z = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+        I64 = ctypes.c_int64
+        sig = {
+            "sf_fd_weights": [I, P],
+            "sf_create": [P, P],
+            "sf_forward": [P, P, P, P, P, I, P],
+            "sf_adjoint": [P, P, P, P, P, I, P, P],
+            "sf_residual": [P, P, P, P, P, P],
+            "sf_gradient": [P, P, P, P, P, P, Z, I, P],
+            "sf_forward_host": [P, P, P, P, P],
+            "sf_set_profiling": [P, I],
+            "sf_get_profile": [P, P, P, P, I],
+            "sf_set_tuning": [P, I, I, I],
+            "sf_get_tuning": [P, P, P, P],
+            "sf_slab_plan": [I64, I, I, I, P, P],
+            "sf_sparse_owner": [I64, I, I, D, D, P],
+            "sf_nccl_unique_id": [P],
+            "sf_nccl_comm_init": [P, I, I, P],
+            "sf_nccl_comm_destroy": [P],
+            "sf_create_slab": [P, P, I, I, P],
+            "sf_allreduce_gradient": [P, P, P, Z, P, P],
+        }
+        for name, at in sig.items():
+            f = getattr(L, name)
+            f.argtypes = at
+            f.restype = ctypes.c_int
+        L.sf_destroy.argtypes = [P]
+        L.sf_destroy.restype = None
+        L.sf_gradient_workspace_bytes.argtypes = [P, I]
+        L.sf_gradient_workspace_bytes.restype = Z
+        L.sf_last_error.argtypes = []
+        L.sf_last_error.restype = ctypes.c_char_p
+        L.sf_version.argtypes = []
+        L.sf_version.restype = I
+        _lib = L
+    return _lib
+
+
+def check(code: int):
+    if code != 0:
+        raise SfError(code, lib().sf_last_error().decode(errors="replace"))

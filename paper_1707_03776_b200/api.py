@@ -1,0 +1,278 @@
+"""Thin Python binding of libsf.so (same names as the C-ABI; marshalling only).
+
+torch is used for device memory and streams; every computation happens in the
+library's CUDA kernels.  Arrays:
+  * grid arrays: torch.float32 CUDA tensors, contiguous, shape = grid shape
+    ([x][y][z], 2D [x][z]); wavefield state u/v: shape (2, *grid);
+  * sparse series: (nt, npoint) float32 CUDA tensors (time-major, reading C12);
+  * coordinates: host arrays (npoint, ndim), metres from computational index 0.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+import torch
+
+from ._lib import SfDesc, SfError, check, lib
+
+__all__ = ["Propagator", "fd_weights", "forward_host", "slab_plan", "sparse_owner", "SfError",
+           "nccl_unique_id", "nccl_comm_init", "nccl_comm_destroy", "allreduce_gradient"]
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str, shape=None):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise TypeError(f"{name}: expected a contiguous float32 CUDA tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+    return t
+
+
+def fd_weights(space_order: int) -> np.ndarray:
+    w = np.zeros(space_order // 2 + 1)
+    check(lib().sf_fd_weights(space_order, w.ctypes.data_as(ctypes.c_void_p)))
+    return w
+
+
+def slab_plan(n0: int, space_order: int, rank: int, nranks: int):
+    x0, nl = ctypes.c_int64(), ctypes.c_int64()
+    check(lib().sf_slab_plan(n0, space_order, rank, nranks, ctypes.byref(x0), ctypes.byref(nl)))
+    return x0.value, nl.value
+
+
+def sparse_owner(n0: int, space_order: int, nranks: int, h: float, coord0: float) -> int:
+    o = ctypes.c_int()
+    check(lib().sf_sparse_owner(n0, space_order, nranks, h, coord0, ctypes.byref(o)))
+    return o.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib().sf_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_init(uid: bytes, nranks: int, rank: int) -> int:
+    c = ctypes.c_void_p()
+    check(lib().sf_nccl_comm_init(ctypes.create_string_buffer(uid, 128), nranks, rank, ctypes.byref(c)))
+    return c.value
+
+
+def nccl_comm_destroy(comm: int):
+    check(lib().sf_nccl_comm_destroy(ctypes.c_void_p(comm)))
+
+
+class Propagator:
+    """One acoustic problem bound to a device handle (sf_create / sf_create_slab).
+
+    ``shape`` is the (global) computational grid.  In slab mode (``comm`` given,
+    nranks > 1) ``m``/``damp`` are the rank's local arrays with r halo planes on
+    axis 0 ([n0_loc + 2r][n1][n2]) and every wavefield array is local likewise.
+    """
+
+    def __init__(self, m: torch.Tensor, damp: Optional[torch.Tensor], *, shape, h: float,
+                 space_order: int, nt: int, dt: float, src_coords=None, rec_coords=None,
+                 comm: Optional[int] = None, rank: int = 0, nranks: int = 1):
+        self.shape = tuple(int(s) for s in shape)
+        self.ndim = len(self.shape)
+        self.h, self.space_order, self.nt, self.dt = float(h), int(space_order), int(nt), float(dt)
+        self.r = self.space_order // 2
+        self.nranks, self.rank = int(nranks), int(rank)
+        if self.nranks > 1:
+            self.x0, self.n0_loc = slab_plan(self.shape[0], self.space_order, rank, nranks)
+            self.local_shape = (self.n0_loc + 2 * self.r,) + self.shape[1:]
+        else:
+            self.x0, self.n0_loc = 0, self.shape[0]
+            self.local_shape = self.shape
+        _dev(m, "m", self.local_shape)
+        if damp is not None:
+            _dev(damp, "damp", self.local_shape)
+        self._src = np.zeros((0, self.ndim)) if src_coords is None else \
+            np.ascontiguousarray(np.asarray(src_coords, dtype=np.float64).reshape(-1, self.ndim))
+        self._rec = np.zeros((0, self.ndim)) if rec_coords is None else \
+            np.ascontiguousarray(np.asarray(rec_coords, dtype=np.float64).reshape(-1, self.ndim))
+        self.nsrc, self.nrec = self._src.shape[0], self._rec.shape[0]
+        d = SfDesc()
+        d.ndim = self.ndim
+        for a in range(3):
+            d.shape[a] = self.shape[a] if a < self.ndim else 1
+        d.h, d.space_order, d.nt, d.dt = self.h, self.space_order, self.nt, self.dt
+        d.m = m.data_ptr()
+        d.damp = damp.data_ptr() if damp is not None else None
+        d.nsrc = self.nsrc
+        d.src_coords = self._src.ctypes.data if self.nsrc else None
+        d.nrec = self.nrec
+        d.rec_coords = self._rec.ctypes.data if self.nrec else None
+        self._desc = d
+        hnd = ctypes.c_void_p()
+        torch.cuda.synchronize()
+        if comm is not None or self.nranks > 1:
+            check(lib().sf_create_slab(ctypes.byref(d), ctypes.c_void_p(comm), rank, nranks,
+                                       ctypes.byref(hnd)))
+        else:
+            check(lib().sf_create(ctypes.byref(d), ctypes.byref(hnd)))
+        self._h = hnd
+        self.device = m.device
+
+    # -------------------------------------------------------------- lifetime
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().sf_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- helpers
+    def nsnap(self, save_every: int) -> int:
+        return (self.nt - 1) // save_every + 1
+
+    def zeros_state(self):
+        return torch.zeros((2,) + self.local_shape, device=self.device, dtype=torch.float32)
+
+    def set_tuning(self, variant: int = 0, by: int = 0, chunks: int = 0):
+        check(lib().sf_set_tuning(self._h, variant, by, chunks))
+
+    def tuning(self):
+        v, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(lib().sf_get_tuning(self._h, ctypes.byref(v), ctypes.byref(b), ctypes.byref(c)))
+        return {"variant": v.value, "by": b.value, "chunks": c.value}
+
+    def set_profiling(self, on: bool = True):
+        check(lib().sf_set_profiling(self._h, 1 if on else 0))
+
+    def profile(self, reset: bool = True):
+        ms, ns, na = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_longlong()
+        check(lib().sf_get_profile(self._h, ctypes.byref(ms), ctypes.byref(ns), ctypes.byref(na),
+                                   1 if reset else 0))
+        return {"stencil_ms": ms.value, "stencil_launches": ns.value, "launches": na.value}
+
+    # -------------------------------------------------------------- the path
+    def forward(self, wavelet: Optional[torch.Tensor], *, u: Optional[torch.Tensor] = None,
+                rec: Optional[torch.Tensor] = None, save_every: int = 0,
+                snaps: Optional[torch.Tensor] = None, stream=None):
+        """sf_forward.  Returns (rec [nt][nrec], u (u^{nt-2}, u^{nt-1}), snaps)."""
+        if self.nsrc:
+            _dev(wavelet, "wavelet", (self.nt, self.nsrc))
+        u = self.zeros_state() if u is None else _dev(u, "u", (2,) + self.local_shape)
+        if self.nrec:
+            rec = torch.empty((self.nt, self.nrec), device=self.device) if rec is None else \
+                _dev(rec, "rec", (self.nt, self.nrec))
+        else:
+            rec = None
+        if save_every > 0 and snaps is None:
+            snaps = torch.empty((self.nsnap(save_every),) + self.local_shape, device=self.device)
+        if snaps is not None:
+            _dev(snaps, "snaps", (self.nsnap(save_every),) + self.local_shape)
+        check(lib().sf_forward(self._h, _ptr(wavelet) if self.nsrc else None, _ptr(rec), _ptr(u),
+                               _ptr(snaps), int(save_every), _stream(stream)))
+        return rec, u, snaps
+
+    def adjoint(self, res: Optional[torch.Tensor], *, v: Optional[torch.Tensor] = None,
+                srca: Optional[torch.Tensor] = None, snaps: Optional[torch.Tensor] = None,
+                save_every: int = 0, grad: Optional[torch.Tensor] = None, stream=None):
+        """sf_adjoint.  Returns (srca [nt][nsrc], v (v^1, v^0), grad)."""
+        if self.nrec:
+            _dev(res, "res", (self.nt, self.nrec))
+        v = self.zeros_state() if v is None else _dev(v, "v", (2,) + self.local_shape)
+        if self.nsrc:
+            srca = torch.empty((self.nt, self.nsrc), device=self.device) if srca is None else \
+                _dev(srca, "srca", (self.nt, self.nsrc))
+        else:
+            srca = None
+        if snaps is not None:
+            _dev(snaps, "snaps", (self.nsnap(save_every),) + self.local_shape)
+            if grad is None:
+                grad = torch.zeros(self.local_shape, device=self.device)
+        if grad is not None:
+            _dev(grad, "grad", self.local_shape)
+        check(lib().sf_adjoint(self._h, _ptr(res) if self.nrec else None, _ptr(srca), _ptr(v),
+                               _ptr(snaps), int(save_every), _ptr(grad), _stream(stream)))
+        return srca, v, grad
+
+    def residual(self, d_syn: torch.Tensor, d_obs: torch.Tensor, res: Optional[torch.Tensor] = None,
+                 stream=None):
+        _dev(d_syn, "d_syn", (self.nt, self.nrec))
+        _dev(d_obs, "d_obs", (self.nt, self.nrec))
+        res = torch.empty_like(d_syn) if res is None else _dev(res, "res", (self.nt, self.nrec))
+        J = ctypes.c_double()
+        check(lib().sf_residual(self._h, _ptr(d_syn), _ptr(d_obs), _ptr(res), ctypes.byref(J),
+                                _stream(stream)))
+        return res, J.value
+
+    def gradient_workspace_bytes(self, save_every: int) -> int:
+        return int(lib().sf_gradient_workspace_bytes(self._h, int(save_every)))
+
+    def gradient(self, wavelet: torch.Tensor, d_obs: torch.Tensor, *, save_every: int = 1,
+                 grad: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None, stream=None):
+        """sf_gradient: returns (grad [local grid], J)."""
+        _dev(d_obs, "d_obs", (self.nt, self.nrec))
+        if self.nsrc:
+            _dev(wavelet, "wavelet", (self.nt, self.nsrc))
+        nbytes = self.gradient_workspace_bytes(save_every)
+        if ws is None or ws.numel() * ws.element_size() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        grad = torch.empty(self.local_shape, device=self.device) if grad is None else \
+            _dev(grad, "grad", self.local_shape)
+        J = ctypes.c_double()
+        check(lib().sf_gradient(self._h, _ptr(wavelet) if self.nsrc else None, _ptr(d_obs), _ptr(grad),
+                                ctypes.byref(J), ctypes.c_void_p(ws.data_ptr()), nbytes,
+                                int(save_every), _stream(stream)))
+        return grad, J.value
+
+    def allreduce_gradient(self, comm: int, grad: torch.Tensor, J: Optional[float] = None, stream=None):
+        return allreduce_gradient(comm, grad, J, handle=self, stream=stream)
+
+
+def allreduce_gradient(comm: int, grad: torch.Tensor, J: Optional[float] = None, handle=None,
+                       stream=None):
+    """sf_allreduce_gradient: in-place sum of grad (and J) over the NCCL communicator."""
+    _dev(grad, "grad")
+    Jc = ctypes.c_double(0.0 if J is None else J)
+    check(lib().sf_allreduce_gradient(handle._h if handle is not None else None, ctypes.c_void_p(comm),
+                                      _ptr(grad), grad.numel(),
+                                      ctypes.byref(Jc) if J is not None else None, _stream(stream)))
+    return grad, (Jc.value if J is not None else None)
+
+
+def forward_host(m: np.ndarray, damp: Optional[np.ndarray], *, h: float, space_order: int, nt: int,
+                 dt: float, src_coords, wavelet: np.ndarray, rec_coords, rec_out: Optional[np.ndarray] = None,
+                 u_out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
+    """sf_forward_host: end-to-end forward with HOST (numpy / pinned) buffers."""
+    shape = m.shape
+    nd = len(shape)
+    src = np.ascontiguousarray(np.asarray(src_coords, np.float64).reshape(-1, nd))
+    rec = np.ascontiguousarray(np.asarray(rec_coords, np.float64).reshape(-1, nd))
+    d = SfDesc()
+    d.ndim = nd
+    for a in range(3):
+        d.shape[a] = shape[a] if a < nd else 1
+    d.h, d.space_order, d.nt, d.dt = h, space_order, nt, dt
+    assert m.dtype == np.float32 and m.flags.c_contiguous
+    d.m = m.ctypes.data
+    if damp is not None:
+        assert damp.dtype == np.float32 and damp.flags.c_contiguous
+        d.damp = damp.ctypes.data
+    d.nsrc, d.src_coords = src.shape[0], src.ctypes.data if src.shape[0] else None
+    d.nrec, d.rec_coords = rec.shape[0], rec.ctypes.data if rec.shape[0] else None
+    wav = np.ascontiguousarray(wavelet, dtype=np.float32)
+    if rec_out is None:
+        rec_out = np.empty((nt, rec.shape[0]), np.float32)
+    check(lib().sf_forward_host(ctypes.byref(d), wav.ctypes.data_as(ctypes.c_void_p),
+                                rec_out.ctypes.data_as(ctypes.c_void_p),
+                                None if u_out is None else u_out.ctypes.data_as(ctypes.c_void_p),
+                                _stream(stream)))
+    return rec_out

@@ -1,0 +1,176 @@
+// comm.cu -- multi-GPU plumbing over NCCL (NVLink 5 / NVSwitch): slab halo exchange
+// and the multi-shot gradient all-reduce (a8).
+//
+// NCCL is resolved at run time with dlopen("libnccl.so.2") so that libsf.so loads on
+// hosts without NCCL and reuses the NCCL that torch already loaded (torch wheel,
+// 2.28.x) -- only one NCCL per process.  Header: the torch wheel's nccl.h.
+//
+// Halo exchange of the newest time level, after its stencil + injection (reading C18):
+//   send owned planes [r, 2r)              -> left neighbour's right halo [n0_loc + r, n0_loc + 2r)
+//   send owned planes [n0_loc, n0_loc + r) -> right neighbour's left halo [0, r)
+// Each face is one contiguous r * n1 * n2 block (x is the outermost axis): no packing.
+// Global edges keep their zero halo (Dirichlet ghost, reading C6).
+#include <dlfcn.h>
+
+#include <mutex>
+
+#include <nccl.h>
+
+#include "sf_internal.h"
+
+namespace {
+struct NcclApi {
+    void *lib = nullptr;
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    bool ok = false;
+};
+
+NcclApi &api()
+{
+    static NcclApi a;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *n : names) {
+            a.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (a.lib) break;
+        }
+        if (!a.lib) return;
+#define SF_SYM(f) a.f = reinterpret_cast<decltype(a.f)>(dlsym(a.lib, "nccl" #f))
+        SF_SYM(GetUniqueId);
+        SF_SYM(CommInitRank);
+        SF_SYM(CommDestroy);
+        SF_SYM(Send);
+        SF_SYM(Recv);
+        SF_SYM(GroupStart);
+        SF_SYM(GroupEnd);
+        SF_SYM(AllReduce);
+        SF_SYM(GetErrorString);
+#undef SF_SYM
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv &&
+               a.GroupStart && a.GroupEnd && a.AllReduce && a.GetErrorString;
+    });
+    return a;
+}
+
+sf_status nccl_err(const char *what, ncclResult_t r)
+{
+    return sf_set_error(SF_ERR_NCCL, "%s: %s", what, api().GetErrorString ? api().GetErrorString(r) : "?");
+}
+}  // namespace
+
+#define SF_NCCL_TRY(call)                                   \
+    do {                                                    \
+        ncclResult_t r_ = (call);                           \
+        if (r_ != ncclSuccess) return nccl_err(#call, r_);  \
+    } while (0)
+
+static sf_status need_nccl()
+{
+    if (!api().ok) return sf_set_error(SF_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    return SF_OK;
+}
+
+extern "C" sf_status sf_nccl_unique_id(char id_out[128])
+{
+    sf_status s = need_nccl();
+    if (s) return s;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    SF_NCCL_TRY(api().GetUniqueId(&id));
+    memcpy(id_out, &id, 128);
+    return SF_OK;
+}
+
+extern "C" sf_status sf_nccl_comm_init(const char id[128], int nranks, int rank, void **comm_out)
+{
+    sf_status s = need_nccl();
+    if (s) return s;
+    if (!comm_out) return sf_set_error(SF_ERR_INVALID_ARG, "comm_out is NULL");
+    ncclUniqueId uid;
+    memcpy(&uid, id, 128);
+    ncclComm_t c = nullptr;
+    SF_NCCL_TRY(api().CommInitRank(&c, nranks, uid, rank));
+    *comm_out = c;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_nccl_comm_destroy(void *comm)
+{
+    sf_status s = need_nccl();
+    if (s) return s;
+    if (comm) SF_NCCL_TRY(api().CommDestroy(static_cast<ncclComm_t>(comm)));
+    return SF_OK;
+}
+
+sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st)
+{
+    sf_status s = need_nccl();
+    if (s) return s;
+    const int r = h->r;
+    const int64_t plane = h->N / h->nb[0];
+    const size_t cnt = (size_t)r * (size_t)plane;
+    const int64_t nl = h->n0_loc;
+    ncclComm_t c = static_cast<ncclComm_t>(h->comm);
+    SF_NCCL_TRY(api().GroupStart());
+    if (h->rank > 0) {
+        SF_NCCL_TRY(api().Send(buf + (int64_t)r * plane, cnt, ncclFloat, h->rank - 1, c, st));
+        SF_NCCL_TRY(api().Recv(buf, cnt, ncclFloat, h->rank - 1, c, st));
+    }
+    if (h->rank < h->nranks - 1) {
+        SF_NCCL_TRY(api().Send(buf + nl * plane, cnt, ncclFloat, h->rank + 1, c, st));
+        SF_NCCL_TRY(api().Recv(buf + (nl + r) * plane, cnt, ncclFloat, h->rank + 1, c, st));
+    }
+    SF_NCCL_TRY(api().GroupEnd());
+    h->n_all++;
+    return SF_OK;
+}
+
+sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st)
+{
+    sf_status s = need_nccl();
+    if (s) return s;
+    SF_NCCL_TRY(api().AllReduce(buf, buf, count, ncclFloat, ncclSum, static_cast<ncclComm_t>(comm), st));
+    return SF_OK;
+}
+
+sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st)
+{
+    sf_status s = need_nccl();
+    if (s) return s;
+    SF_NCCL_TRY(api().AllReduce(buf, buf, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm), st));
+    return SF_OK;
+}
+
+extern "C" sf_status sf_allreduce_gradient(sf_handle *h, void *comm, float *grad, size_t count,
+                                           double *J, void *stream)
+{
+    if (!comm || !grad) return sf_set_error(SF_ERR_INVALID_ARG, "NULL argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    sf_status s = sf_comm_allreduce_f32(comm, grad, count, st);
+    if (s) return s;
+    if (J) {
+        double *dJ = h ? h->dJ : nullptr;
+        bool own = false;
+        if (!dJ) {
+            SF_CUDA_TRY(cudaMalloc(&dJ, sizeof(double)));
+            own = true;
+        }
+        SF_CUDA_TRY(cudaMemcpyAsync(dJ, J, sizeof(double), cudaMemcpyHostToDevice, st));
+        if ((s = sf_comm_allreduce_f64(comm, dJ, 1, st))) return s;
+        SF_CUDA_TRY(cudaMemcpyAsync(J, dJ, sizeof(double), cudaMemcpyDeviceToHost, st));
+        SF_CUDA_TRY(cudaStreamSynchronize(st));
+        if (own) cudaFree(dJ);
+    } else {
+        SF_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return SF_OK;
+}

@@ -1,0 +1,49 @@
+// launch.cuh -- per-radius launchers for the stencil-step kernels (one translation unit
+// per radius r = space_order/2, compiled in parallel; see inst_body.cuh).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "stencil_common.cuh"
+
+enum SfVariant { SF_VAR_AUTO = 0, SF_VAR_GENERIC = 1, SF_VAR_TMA = 2 };
+
+struct SfTmaMaps {
+    CUtensorMap cur, old, c3, beta, snap, grad;
+};
+
+struct SfLaunch {
+    int ndim;
+    int variant;      // SF_VAR_GENERIC or SF_VAR_TMA (resolved)
+    int by;           // TMA: warps (y rows) per CTA, 8 or 16
+    int chunks;       // TMA: x-chunks per (y, z) tile column
+    int damp;         // beta array present
+    int mode;         // SfMode
+    int snap_slot;    // GRAD: snapshot slot for the 4D snapshot tensor map
+    const SfTmaMaps *maps;
+};
+
+// shared-memory bytes of the TMA kernel for (r, by, damp, mode); 0 if unsupported
+int sf_tma_smem_bytes(int r, int by, int damp, int mode);
+
+#define SF_DECL_LAUNCH(R) \
+    cudaError_t sf_launch_step_r##R(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st);
+SF_DECL_LAUNCH(1)
+SF_DECL_LAUNCH(2)
+SF_DECL_LAUNCH(3)
+SF_DECL_LAUNCH(4)
+SF_DECL_LAUNCH(5)
+SF_DECL_LAUNCH(6)
+SF_DECL_LAUNCH(7)
+SF_DECL_LAUNCH(8)
+#undef SF_DECL_LAUNCH
+
+#define SF_DECL_SMEM(R) int sf_tma_smem_r##R(int by, int damp, int mode);
+SF_DECL_SMEM(1)
+SF_DECL_SMEM(2)
+SF_DECL_SMEM(3)
+SF_DECL_SMEM(4)
+SF_DECL_SMEM(5)
+SF_DECL_SMEM(6)
+SF_DECL_SMEM(7)
+SF_DECL_SMEM(8)
+#undef SF_DECL_SMEM

@@ -1,0 +1,889 @@
+// sf_api.cu -- host side of libsf.so: the C-ABI of include/sf.h.
+//
+// Validation, host FD weights, sparse tables, coefficient hoisting, the time-loop
+// drivers (forward, adjoint, gradient), the residual/objective and the end-to-end
+// host-buffer form.  Every step of the path runs in this library's CUDA kernels
+// (stencil_*.cuh, sparse.cuh); there is no CPU fallback: without a CUDA device every
+// compute call fails with SF_ERR_CUDA.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "sf_internal.h"
+#include "sparse.cuh"
+
+#define SF_VERSION 1
+
+static thread_local char g_err[1024] = "";
+
+sf_status sf_set_error(sf_status s, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+extern "C" const char *sf_last_error(void) { return g_err; }
+extern "C" int sf_version(void) { return SF_VERSION; }
+
+// ------------------------------------------------------------------ FD weights (host)
+// Closed form of the centred 2nd-derivative weights of order 2r:
+//   w_k = 2 (-1)^{k+1} (r!)^2 / (k^2 (r-k)! (r+k)!),  w_0 = -2 sum_{k>=1} w_k.
+// (All factorials up to 16! are exact in fp64.)
+static double fact(int n)
+{
+    double f = 1.0;
+    for (int i = 2; i <= n; ++i) f *= (double)i;
+    return f;
+}
+
+extern "C" sf_status sf_fd_weights(int space_order, double *w)
+{
+    if (!w) return sf_set_error(SF_ERR_INVALID_ARG, "sf_fd_weights: w is NULL");
+    if (space_order < 2 || space_order > 2 * SF_MAXR || (space_order & 1))
+        return sf_set_error(SF_ERR_ORDER, "space_order %d not in {2,4,...,16}", space_order);
+    const int r = space_order / 2;
+    double s = 0.0;
+    for (int k = 1; k <= r; ++k) {
+        const double sgn = (k & 1) ? 1.0 : -1.0;
+        w[k] = 2.0 * sgn * fact(r) * fact(r) / ((double)k * k * fact(r - k) * fact(r + k));
+        s += w[k];
+    }
+    w[0] = -2.0 * s;
+    return SF_OK;
+}
+
+// ------------------------------------------------------------------ tensor maps (TMA)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// fp32 tensor [dims[rank-1]]...[dims[0]] (dims[0] fastest), dense strides, box `box`.
+static sf_status make_map(CUtensorMap *m, const void *base, int rank, const int64_t *dims,
+                          const uint32_t *box)
+{
+    auto enc = tmap_encoder();
+    if (!enc) return sf_set_error(SF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5];
+    uint64_t stride = 4;
+    for (int i = 0; i < rank; ++i) {
+        gd[i] = (cuuint64_t)dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i > 0) gs[i - 1] = stride;
+        stride *= (uint64_t)dims[i];
+    }
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void *>(base),
+                     gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return sf_set_error(SF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SF_OK;
+}
+
+// ------------------------------------------------------------------ launch plumbing
+static inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static cudaError_t launch_step_r(int r, const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
+{
+    switch (r) {
+    case 1: return sf_launch_step_r1(L, a, st);
+    case 2: return sf_launch_step_r2(L, a, st);
+    case 3: return sf_launch_step_r3(L, a, st);
+    case 4: return sf_launch_step_r4(L, a, st);
+    case 5: return sf_launch_step_r5(L, a, st);
+    case 6: return sf_launch_step_r6(L, a, st);
+    case 7: return sf_launch_step_r7(L, a, st);
+    default: return sf_launch_step_r8(L, a, st);
+    }
+}
+
+int sf_tma_smem_bytes(int r, int by, int damp, int mode)
+{
+    switch (r) {
+    case 1: return sf_tma_smem_r1(by, damp, mode);
+    case 2: return sf_tma_smem_r2(by, damp, mode);
+    case 3: return sf_tma_smem_r3(by, damp, mode);
+    case 4: return sf_tma_smem_r4(by, damp, mode);
+    case 5: return sf_tma_smem_r5(by, damp, mode);
+    case 6: return sf_tma_smem_r6(by, damp, mode);
+    case 7: return sf_tma_smem_r7(by, damp, mode);
+    default: return sf_tma_smem_r8(by, damp, mode);
+    }
+}
+
+static bool tma_ok(const sf_handle *h)
+{
+    return h->ndim == 3 && (h->nb[2] % 4) == 0 && h->nb[2] >= 4 && h->nb[1] >= 1 &&
+           h->N < (int64_t(1) << 40) && h->nb[0] < (int64_t(1) << 31);
+}
+
+static int resolve_variant(const sf_handle *h)
+{
+    if (h->variant == SF_VAR_GENERIC) return SF_VAR_GENERIC;
+    if (tma_ok(h)) return SF_VAR_TMA;
+    return SF_VAR_GENERIC;
+}
+
+static int resolve_by(const sf_handle *h)
+{
+    if (h->by == 8) return 8;
+    if (h->by == 16 && h->r <= 4) return 16;
+    return h->r <= 4 ? 16 : 8;
+}
+
+// x-chunks per tile column: balance whole waves of one CTA per SM against the 2r
+// warm-up planes each chunk re-reads (SURVEY H2 parallelism model).
+static int resolve_chunks(const sf_handle *h, int by)
+{
+    if (h->chunks > 0) return h->chunks;
+    const int64_t planes = h->xb - h->xa;
+    const int64_t tiles = ((h->nb[2] + 127) / 128) * ((h->nb[1] + by - 1) / by);
+    int sms = 148;
+    {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+            sms = v;
+    }
+    const int per_sm = by == 8 ? 2 : 1;
+    const int64_t slots = (int64_t)sms * per_sm;
+    double best = 1e300;
+    int bestc = 1;
+    const int64_t cmax = std::max<int64_t>(1, planes / std::max(2 * h->r, 8));
+    for (int64_t c = 1; c <= cmax && c <= 4096; ++c) {
+        const int64_t chunk = (planes + c - 1) / c;
+        const int64_t nch = (planes + chunk - 1) / chunk;
+        const int64_t ctas = tiles * nch;
+        const int64_t waves = (ctas + slots - 1) / slots;
+        const double t = (double)waves * ((double)chunk + 1.0 * h->r);
+        if (t < best - 1e-9) {
+            best = t;
+            bestc = (int)c;
+        }
+    }
+    return bestc;
+}
+
+// prof events
+static cudaEvent_t next_event(sf_handle *h)
+{
+    if (h->ev_used == h->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        h->ev_pool.push_back(e);
+    }
+    return h->ev_pool[h->ev_used++];
+}
+
+struct StepBufs {
+    const float *cur;
+    float *out;
+    float *snap_out;       // SAVE
+    const float *snaps;    // GRAD: snapshot array base
+    int snap_slot;
+    int64_t nsnap;
+    float *grad;
+    float gscale;
+};
+
+static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStream_t st)
+{
+    SfStepArgs a{};
+    a.cur = b.cur;
+    a.out = b.out;
+    a.c3 = h->c3;
+    a.beta = h->beta;
+    a.snap_out = b.snap_out;
+    a.snap_in = b.snaps ? b.snaps + (int64_t)b.snap_slot * h->N : nullptr;
+    a.grad = b.grad;
+    a.gscale = b.gscale;
+    if (h->ndim == 3) {
+        a.n0b = h->nb[0];
+        a.n1 = h->nb[1];
+        a.n2 = h->nb[2];
+    } else {
+        a.n0b = h->nb[0];
+        a.n1 = 1;
+        a.n2 = h->nb[1];
+    }
+    a.xa = h->xa;
+    a.xb = h->xb;
+    a.w = h->w;
+
+    SfLaunch L{};
+    L.ndim = h->ndim;
+    L.variant = resolve_variant(h);
+    L.by = resolve_by(h);
+    L.chunks = resolve_chunks(h, L.by);
+    L.damp = h->beta != nullptr;
+    L.mode = mode;
+    L.snap_slot = b.snap_slot;
+    SfTmaMaps maps;
+    memset(&maps, 0, sizeof maps);
+    if (L.variant == SF_VAR_TMA) {
+        const int HZ = ((h->r + 3) / 4) * 4;
+        const int64_t d3[3] = {h->nb[2], h->nb[1], h->nb[0]};
+        const uint32_t bcur[3] = {(uint32_t)(128 + 2 * HZ), (uint32_t)(L.by + 2 * h->r), 1};
+        const uint32_t bpl[3] = {128, (uint32_t)L.by, 1};
+        sf_status s;
+        if ((s = make_map(&maps.cur, b.cur, 3, d3, bcur))) return s;
+        if ((s = make_map(&maps.old, b.out, 3, d3, bpl))) return s;
+        if ((s = make_map(&maps.c3, h->c3, 3, d3, bpl))) return s;
+        if (h->beta && (s = make_map(&maps.beta, h->beta, 3, d3, bpl))) return s;
+        if (mode == SF_MODE_GRAD) {
+            const int64_t d4[4] = {h->nb[2], h->nb[1], h->nb[0], b.nsnap};
+            const uint32_t b4[4] = {128, (uint32_t)L.by, 1, 1};
+            if ((s = make_map(&maps.snap, b.snaps, 4, d4, b4))) return s;
+            if ((s = make_map(&maps.grad, b.grad, 3, d3, bpl))) return s;
+        }
+    }
+    L.maps = &maps;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->prof) {
+        e0 = next_event(h);
+        e1 = next_event(h);
+        cudaEventRecord(e0, st);
+    }
+    cudaError_t e = launch_step_r(h->r, L, a, st);
+    if (h->prof) cudaEventRecord(e1, st);
+    if (e != cudaSuccess) return sf_set_error(SF_ERR_CUDA, "stencil launch: %s", cudaGetErrorString(e));
+    h->n_stencil++;
+    h->n_all++;
+    return SF_OK;
+}
+
+static sf_status launch_interp(sf_handle *h, const SfSparse &sp, const float *u, float *out,
+                               cudaStream_t st)
+{
+    if (sp.np == 0 || !out) return SF_OK;
+    k_interp<<<(sp.np + 127) / 128, 128, 0, st>>>(u, sp.i_idx, sp.i_w, sp.i_owned, sp.np, sp.nc, out);
+    h->n_all++;
+    SF_CUDA_TRY(cudaGetLastError());
+    return SF_OK;
+}
+
+static sf_status launch_inject(sf_handle *h, const SfSparse &sp, float *u, const float *vals,
+                               float *snap_patch, const float *grad_snap, float *grad, float gscale,
+                               cudaStream_t st)
+{
+    if (sp.ntgt == 0 || !vals) return SF_OK;
+    k_inject<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.j_rowptr, sp.j_pt, sp.j_coef,
+                                                     sp.ntgt, vals, snap_patch, grad_snap, grad, gscale);
+    h->n_all++;
+    SF_CUDA_TRY(cudaGetLastError());
+    return SF_OK;
+}
+
+// ------------------------------------------------------------------ sparse tables
+static void free_sparse(SfSparse &s)
+{
+    cudaFree(s.i_idx);
+    cudaFree(s.i_w);
+    cudaFree(s.i_owned);
+    cudaFree(s.j_tgt);
+    cudaFree(s.j_rowptr);
+    cudaFree(s.j_pt);
+    cudaFree(s.j_coef);
+    s = SfSparse{};
+}
+
+template <class T>
+static sf_status upload(T **dst, const std::vector<T> &v)
+{
+    if (v.empty()) return SF_OK;
+    SF_CUDA_TRY(cudaMalloc((void **)dst, v.size() * sizeof(T)));
+    SF_CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return SF_OK;
+}
+
+// Reading C11: pos = x/h; base = min(floor(pos), n-2); xi = pos - base; weights =
+// product of (1 - xi) / xi; corners ordered last-axis fastest; outside [0, n-1] is an
+// error.  Slab mode (C18): axis-0 corners are mapped to the local buffer; a record row
+// is owned by the rank owning the base plane; injection corners by the rank owning
+// the corner's plane.
+static sf_status build_sparse(sf_handle *h, int np, const double *coords, const float *m_dev,
+                              SfSparse &out, const char *what)
+{
+    out = SfSparse{};
+    if (np <= 0) return SF_OK;
+    if (!coords) return sf_set_error(SF_ERR_INVALID_ARG, "%s coordinates are NULL", what);
+    const int nd = h->ndim;
+    const int nc = 1 << nd;
+    std::vector<int64_t> iidx((size_t)np * nc);
+    std::vector<float> iw((size_t)np * nc);
+    std::vector<int> owned(np, 1);
+    struct Ent {
+        int64_t tgt;
+        int pt;
+        int c;
+        double w;
+    };
+    std::vector<Ent> ents;
+    ents.reserve((size_t)np * nc);
+    for (int p = 0; p < np; ++p) {
+        int64_t base[3];
+        double xi[3];
+        for (int a = 0; a < nd; ++a) {
+            const double x = coords[(size_t)p * nd + a];
+            const double pos = x / h->h;
+            const int64_t n = h->gshape[a];
+            if (!(pos >= 0.0) || pos > (double)(n - 1))
+                return sf_set_error(SF_ERR_OUT_OF_DOMAIN,
+                                    "%s %d coordinate %d = %g m outside [0, %g] m", what, p, a, x,
+                                    (double)(n - 1) * h->h);
+            int64_t b = (int64_t)std::floor(pos);
+            if (b > n - 2) b = n - 2;
+            base[a] = b;
+            xi[a] = pos - (double)b;
+        }
+        if (h->nranks > 1) owned[p] = (base[0] >= h->x0 && base[0] < h->x0 + h->n0_loc) ? 1 : 0;
+        for (int c = 0; c < nc; ++c) {
+            double wt = 1.0;
+            int64_t off = 0;
+            int64_t gx = 0;
+            for (int a = 0; a < nd; ++a) {
+                const int bit = (c >> (nd - 1 - a)) & 1;
+                wt *= bit ? xi[a] : (1.0 - xi[a]);
+                int64_t ia = base[a] + bit;
+                if (a == 0) {
+                    gx = ia;
+                    ia = ia - h->x0 + (h->nranks > 1 ? h->r : 0);
+                }
+                off = off * h->nb[a] + ia;
+            }
+            // interpolation corner (zero weights kept in the table, skipped by the kernel;
+            // non-owned rows point at a valid in-buffer index only when owned)
+            const bool inbuf = (h->nranks == 1) || owned[p];
+            iidx[(size_t)p * nc + c] = inbuf ? off : 0;
+            iw[(size_t)p * nc + c] = inbuf ? (float)wt : 0.0f;
+            const bool own_corner =
+                (h->nranks == 1) || (gx >= h->x0 && gx < h->x0 + h->n0_loc);
+            if (wt != 0.0 && own_corner) ents.push_back({off, p, c, wt});
+        }
+    }
+    std::stable_sort(ents.begin(), ents.end(), [](const Ent &a, const Ent &b) {
+        return std::tie(a.tgt, a.pt, a.c) < std::tie(b.tgt, b.pt, b.c);
+    });
+    std::vector<int64_t> tgt;
+    std::vector<int> rowptr, pt;
+    std::vector<int64_t> etgt;
+    std::vector<double> ew;
+    for (size_t e = 0; e < ents.size(); ++e) {
+        if (e == 0 || ents[e].tgt != ents[e - 1].tgt) {
+            tgt.push_back(ents[e].tgt);
+            rowptr.push_back((int)e);
+        }
+        pt.push_back(ents[e].pt);
+        etgt.push_back(ents[e].tgt);
+        ew.push_back(ents[e].w);
+    }
+    rowptr.push_back((int)ents.size());
+    out.np = np;
+    out.nc = nc;
+    out.ntgt = (int)tgt.size();
+    out.nent = (int)ents.size();
+    sf_status s;
+    if ((s = upload(&out.i_idx, iidx))) return s;
+    if ((s = upload(&out.i_w, iw))) return s;
+    if (h->nranks > 1 && (s = upload(&out.i_owned, owned))) return s;
+    if (out.ntgt > 0) {
+        if ((s = upload(&out.j_tgt, tgt))) return s;
+        if ((s = upload(&out.j_rowptr, rowptr))) return s;
+        if ((s = upload(&out.j_pt, pt))) return s;
+        int64_t *d_etgt = nullptr;
+        double *d_ew = nullptr;
+        if ((s = upload(&d_etgt, etgt))) return s;
+        if ((s = upload(&d_ew, ew))) return s;
+        SF_CUDA_TRY(cudaMalloc(&out.j_coef, sizeof(float) * out.nent));
+        k_inject_coef<<<(out.nent + 255) / 256, 256>>>(m_dev, d_etgt, d_ew, out.nent, h->dt * h->dt,
+                                                       out.j_coef);
+        SF_CUDA_TRY(cudaGetLastError());
+        SF_CUDA_TRY(cudaDeviceSynchronize());
+        cudaFree(d_etgt);
+        cudaFree(d_ew);
+    }
+    return SF_OK;
+}
+
+// ------------------------------------------------------------------ create / destroy
+static sf_status validate_desc(const sf_desc *d)
+{
+    if (!d) return sf_set_error(SF_ERR_INVALID_ARG, "desc is NULL");
+    if (d->ndim != 2 && d->ndim != 3) return sf_set_error(SF_ERR_SHAPE, "ndim %d not 2 or 3", d->ndim);
+    for (int a = 0; a < d->ndim; ++a)
+        if (d->shape[a] < 2) return sf_set_error(SF_ERR_SHAPE, "shape[%d] = %lld < 2", a, (long long)d->shape[a]);
+    if (d->space_order < 2 || d->space_order > 16 || (d->space_order & 1))
+        return sf_set_error(SF_ERR_ORDER, "space_order %d not in {2,4,...,16}", d->space_order);
+    if (!d->m) return sf_set_error(SF_ERR_INVALID_ARG, "m is NULL");
+    if (d->nt < 2) return sf_set_error(SF_ERR_INVALID_ARG, "nt = %d < 2", d->nt);
+    if (!(d->dt > 0.0)) return sf_set_error(SF_ERR_INVALID_ARG, "dt = %g <= 0", d->dt);
+    if (!(d->h > 0.0)) return sf_set_error(SF_ERR_INVALID_ARG, "h = %g <= 0", d->h);
+    if (d->nsrc < 0 || d->nrec < 0) return sf_set_error(SF_ERR_INVALID_ARG, "negative point count");
+    return SF_OK;
+}
+
+extern "C" void sf_destroy(sf_handle *h)
+{
+    if (!h) return;
+    cudaFree(h->c3);
+    cudaFree(h->beta);
+    cudaFree(h->partial);
+    cudaFree(h->dJ);
+    free_sparse(h->src);
+    free_sparse(h->rec);
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
+    delete h;
+}
+
+static sf_status create_common(const sf_desc *d, sf_handle *h)
+{
+    const int r = d->space_order / 2;
+    h->so = d->space_order;
+    h->r = r;
+    h->nt = d->nt;
+    h->dt = d->dt;
+    h->h = d->h;
+    double w[SF_MAXR + 1];
+    sf_fd_weights(d->space_order, w);
+    for (int k = 0; k <= SF_MAXR; ++k) h->w.w[k] = k <= r ? (float)(w[k] / (d->h * d->h)) : 0.0f;
+    // coefficient hoisting (same bytes as streaming m and eta)
+    SF_CUDA_TRY(cudaMalloc(&h->c3, sizeof(float) * h->N));
+    h->damp = d->damp != nullptr;
+    if (h->damp) SF_CUDA_TRY(cudaMalloc(&h->beta, sizeof(float) * h->N));
+    k_hoist<<<1184, 256>>>(d->m, d->damp, h->N, d->dt, h->c3, h->beta);
+    SF_CUDA_TRY(cudaGetLastError());
+    // min m over the computed planes -> CFL (SF_ERR_CFL) and positivity (SF_ERR_INVALID_ARG)
+    unsigned int *dmin = nullptr;
+    int *dbad = nullptr;
+    SF_CUDA_TRY(cudaMalloc(&dmin, sizeof(unsigned int)));
+    SF_CUDA_TRY(cudaMalloc(&dbad, sizeof(int)));
+    const unsigned int init = 0x7f7fffffu;
+    SF_CUDA_TRY(cudaMemcpy(dmin, &init, sizeof init, cudaMemcpyHostToDevice));
+    SF_CUDA_TRY(cudaMemset(dbad, 0, sizeof(int)));
+    const int64_t plane = h->N / h->nb[0];
+    k_min_m<<<592, 256>>>(d->m + h->xa * plane, (h->xb - h->xa) * plane, dmin, dbad);
+    SF_CUDA_TRY(cudaGetLastError());
+    unsigned int minbits = 0;
+    int bad = 0;
+    SF_CUDA_TRY(cudaMemcpy(&minbits, dmin, sizeof minbits, cudaMemcpyDeviceToHost));
+    SF_CUDA_TRY(cudaMemcpy(&bad, dbad, sizeof bad, cudaMemcpyDeviceToHost));
+    cudaFree(dmin);
+    cudaFree(dbad);
+    if (bad) return sf_set_error(SF_ERR_INVALID_ARG, "m has a non-positive or non-finite value");
+    float mmin;
+    memcpy(&mmin, &minbits, sizeof mmin);
+    double sabs = 0.0;
+    for (int k = 0; k <= r; ++k) sabs += (k ? 2.0 : 1.0) * std::fabs(w[k]);
+    const double vmax = 1.0 / std::sqrt((double)mmin);
+    const double courant = d->dt * vmax / d->h;
+    const double lim = 2.0 / std::sqrt((double)d->ndim * sabs);
+    if (courant > lim)
+        return sf_set_error(SF_ERR_CFL, "Courant number %.4f exceeds the stability limit %.4f "
+                            "(so %d, %dD)", courant, lim, d->space_order, d->ndim);
+    sf_status s;
+    if ((s = build_sparse(h, d->nsrc, d->src_coords, d->m, h->src, "source"))) return s;
+    if ((s = build_sparse(h, d->nrec, d->rec_coords, d->m, h->rec, "receiver"))) return s;
+    SF_CUDA_TRY(cudaMalloc(&h->partial, sizeof(double) * 1024));
+    SF_CUDA_TRY(cudaMalloc(&h->dJ, sizeof(double)));
+    SF_CUDA_TRY(cudaDeviceSynchronize());
+    return SF_OK;
+}
+
+extern "C" sf_status sf_create(const sf_desc *d, sf_handle **out)
+{
+    if (!out) return sf_set_error(SF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    sf_status s = validate_desc(d);
+    if (s) return s;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return sf_set_error(SF_ERR_CUDA, "no CUDA device (libsf has no CPU fallback)");
+    sf_handle *h = new sf_handle();
+    h->ndim = d->ndim;
+    h->N = 1;
+    for (int a = 0; a < d->ndim; ++a) {
+        h->gshape[a] = d->shape[a];
+        h->nb[a] = d->shape[a];
+        h->N *= d->shape[a];
+    }
+    h->xa = 0;
+    h->xb = d->shape[0];
+    h->n0_loc = d->shape[0];
+    s = create_common(d, h);
+    if (s) {
+        sf_destroy(h);
+        return s;
+    }
+    *out = h;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_slab_plan(int64_t n0, int space_order, int rank, int nranks, int64_t *x0,
+                                  int64_t *n0_loc)
+{
+    if (!x0 || !n0_loc || nranks < 1 || rank < 0 || rank >= nranks)
+        return sf_set_error(SF_ERR_INVALID_ARG, "bad slab plan arguments");
+    if (space_order < 2 || space_order > 16 || (space_order & 1))
+        return sf_set_error(SF_ERR_ORDER, "space_order %d", space_order);
+    const int64_t base = n0 / nranks, rem = n0 % nranks;
+    *n0_loc = base + (rank < rem ? 1 : 0);
+    *x0 = rank * base + std::min<int64_t>(rank, rem);
+    if (*n0_loc < space_order / 2)
+        return sf_set_error(SF_ERR_SHAPE, "slab of %lld planes < r = %d", (long long)*n0_loc,
+                            space_order / 2);
+    return SF_OK;
+}
+
+extern "C" sf_status sf_sparse_owner(int64_t n0, int space_order, int nranks, double h,
+                                     double coord0, int *owner)
+{
+    if (!owner || !(h > 0) || nranks < 1) return sf_set_error(SF_ERR_INVALID_ARG, "bad arguments");
+    const double pos = coord0 / h;
+    if (!(pos >= 0.0) || pos > (double)(n0 - 1))
+        return sf_set_error(SF_ERR_OUT_OF_DOMAIN, "coordinate %g outside the grid", coord0);
+    int64_t b = (int64_t)std::floor(pos);
+    if (b > n0 - 2) b = n0 - 2;
+    for (int p = 0; p < nranks; ++p) {
+        int64_t x0, nl;
+        sf_status s = sf_slab_plan(n0, space_order, p, nranks, &x0, &nl);
+        if (s) return s;
+        if (b >= x0 && b < x0 + nl) {
+            *owner = p;
+            return SF_OK;
+        }
+    }
+    return sf_set_error(SF_ERR_OUT_OF_DOMAIN, "no owner");
+}
+
+extern "C" sf_status sf_create_slab(const sf_desc *d, void *comm, int rank, int nranks,
+                                    sf_handle **out)
+{
+    if (!out) return sf_set_error(SF_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    sf_status s = validate_desc(d);
+    if (s) return s;
+    if (nranks > 1 && !comm) return sf_set_error(SF_ERR_INVALID_ARG, "nccl comm is NULL");
+    int64_t x0, nl;
+    if ((s = sf_slab_plan(d->shape[0], d->space_order, rank, nranks, &x0, &nl))) return s;
+    sf_handle *h = new sf_handle();
+    h->ndim = d->ndim;
+    h->rank = rank;
+    h->nranks = nranks;
+    h->comm = comm;
+    h->x0 = x0;
+    h->n0_loc = nl;
+    const int r = d->space_order / 2;
+    for (int a = 0; a < d->ndim; ++a) {
+        h->gshape[a] = d->shape[a];
+        h->nb[a] = d->shape[a];
+    }
+    if (nranks > 1) {
+        h->nb[0] = nl + 2 * r;
+        h->xa = r;
+        h->xb = r + nl;
+    } else {
+        h->xa = 0;
+        h->xb = d->shape[0];
+    }
+    h->N = 1;
+    for (int a = 0; a < d->ndim; ++a) h->N *= h->nb[a];
+    s = create_common(d, h);
+    if (s) {
+        sf_destroy(h);
+        return s;
+    }
+    *out = h;
+    return SF_OK;
+}
+
+// ------------------------------------------------------------------ tuning / profiling
+extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int by, int chunks)
+{
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    if (variant < 0 || variant > 2 || (by != 0 && by != 8 && by != 16) || chunks < 0)
+        return sf_set_error(SF_ERR_INVALID_ARG, "bad tuning (%d, %d, %d)", variant, by, chunks);
+    if (variant == SF_VAR_TMA && !tma_ok(h))
+        return sf_set_error(SF_ERR_INVALID_ARG, "TMA variant needs 3D and n2 %% 4 == 0");
+    h->variant = variant;
+    h->by = by;
+    h->chunks = chunks;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_get_tuning(const sf_handle *h, int *variant, int *by, int *chunks)
+{
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    const int v = resolve_variant(h);
+    const int b = resolve_by(h);
+    if (variant) *variant = v;
+    if (by) *by = v == SF_VAR_TMA ? b : 0;
+    if (chunks) *chunks = v == SF_VAR_TMA ? resolve_chunks(h, b) : 0;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_set_profiling(sf_handle *h, int on)
+{
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    h->prof = on != 0;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_get_profile(sf_handle *h, double *ms, long long *nst, long long *nall, int reset)
+{
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
+        SF_CUDA_TRY(cudaEventSynchronize(h->ev_pool[i + 1]));
+        float t = 0.f;
+        SF_CUDA_TRY(cudaEventElapsedTime(&t, h->ev_pool[i], h->ev_pool[i + 1]));
+        tot += t;
+    }
+    if (ms) *ms = tot;
+    if (nst) *nst = h->n_stencil;
+    if (nall) *nall = h->n_all;
+    if (reset) {
+        h->ev_used = 0;
+        h->n_stencil = 0;
+        h->n_all = 0;
+    }
+    return SF_OK;
+}
+
+// ------------------------------------------------------------------ time loops
+static sf_status post_step_exchange(sf_handle *h, float *buf, cudaStream_t st)
+{
+    if (h->nranks <= 1) return SF_OK;
+    return sf_comm_halo_exchange(h, buf, st);
+}
+
+static sf_status swap_halves(sf_handle *h, float *a, float *b, cudaStream_t st)
+{
+    k_swap<<<1184, 256, 0, st>>>(a, b, h->N);
+    h->n_all++;
+    SF_CUDA_TRY(cudaGetLastError());
+    return SF_OK;
+}
+
+extern "C" sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, float *u,
+                                float *snaps, int save_every, void *stream)
+{
+    if (!h || !u) return sf_set_error(SF_ERR_INVALID_ARG, "handle or u is NULL");
+    if (h->src.np > 0 && !wavelet) return sf_set_error(SF_ERR_INVALID_ARG, "wavelet is NULL");
+    if (h->rec.np > 0 && !rec) return sf_set_error(SF_ERR_INVALID_ARG, "rec is NULL");
+    if (snaps && save_every < 1) return sf_set_error(SF_ERR_INVALID_ARG, "save_every < 1 with snaps");
+    cudaStream_t st = S(stream);
+    const int64_t N = h->N;
+    float *A = u, *B = u + N;  // A = u^{-1}, B = u^0
+    sf_status s;
+    if (h->nranks > 1) {  // make the halo of u^0 valid for the first stencil / record
+        if ((s = post_step_exchange(h, B, st))) return s;
+    }
+    if ((s = launch_interp(h, h->rec, B, rec, st))) return s;
+    if (snaps) SF_CUDA_TRY(cudaMemcpyAsync(snaps, B, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
+    for (int n = 0; n <= h->nt - 2; ++n) {
+        float *cur = (n % 2 == 0) ? B : A;
+        float *out = (n % 2 == 0) ? A : B;
+        const bool save = snaps && ((n + 1) % save_every == 0);
+        float *slot = save ? snaps + (int64_t)((n + 1) / save_every) * N : nullptr;
+        StepBufs b{cur, out, slot, nullptr, 0, 0, nullptr, 0.f};
+        if ((s = launch_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, st))) return s;
+        if ((s = launch_inject(h, h->src, out, wavelet ? wavelet + (int64_t)n * h->src.np : nullptr,
+                               slot, nullptr, nullptr, 0.f, st)))
+            return s;
+        if ((s = post_step_exchange(h, out, st))) return s;
+        if ((s = launch_interp(h, h->rec, out, rec ? rec + (int64_t)(n + 1) * h->rec.np : nullptr, st)))
+            return s;
+    }
+    // u^{nt-1} was written into A when nt is even: restore (u^{nt-2}, u^{nt-1}) order
+    if (h->nt % 2 == 0) return swap_halves(h, A, B, st);
+    return SF_OK;
+}
+
+extern "C" sf_status sf_adjoint(sf_handle *h, const float *res, float *srca, float *v,
+                                const float *snaps, int save_every, float *grad, void *stream)
+{
+    if (!h || !v) return sf_set_error(SF_ERR_INVALID_ARG, "handle or v is NULL");
+    if (h->rec.np > 0 && !res) return sf_set_error(SF_ERR_INVALID_ARG, "res is NULL");
+    if (h->src.np > 0 && !srca) return sf_set_error(SF_ERR_INVALID_ARG, "srca is NULL");
+    const bool dograd = grad != nullptr;
+    if (dograd && (!snaps || save_every < 1))
+        return sf_set_error(SF_ERR_INVALID_ARG, "gradient needs snaps and save_every >= 1");
+    cudaStream_t st = S(stream);
+    const int64_t N = h->N;
+    const int64_t nsnap = dograd ? (h->nt - 1) / save_every + 1 : 0;
+    const float gscale = dograd ? (float)((double)save_every / (h->dt * h->dt)) : 0.f;
+    float *A = v, *B = v + N;  // A = v^{nt}, B = v^{nt-1}
+    sf_status s;
+    if (h->nranks > 1) {
+        if ((s = post_step_exchange(h, B, st))) return s;
+    }
+    if ((s = launch_interp(h, h->src, B, srca ? srca + (int64_t)(h->nt - 1) * h->src.np : nullptr, st)))
+        return s;
+    for (int n = h->nt - 1, j = 0; n >= 1; --n, ++j) {
+        float *cur = (j % 2 == 0) ? B : A;
+        float *out = (j % 2 == 0) ? A : B;
+        const bool g = dograd && (n % save_every == 0);
+        StepBufs b{cur, out, nullptr, g ? snaps : nullptr, g ? n / save_every : 0, nsnap,
+                   g ? grad : nullptr, gscale};
+        if ((s = launch_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, st))) return s;
+        if ((s = launch_inject(h, h->rec, out, res ? res + (int64_t)n * h->rec.np : nullptr, nullptr,
+                               g ? snaps + (int64_t)(n / save_every) * N : nullptr,
+                               g ? grad : nullptr, gscale, st)))
+            return s;
+        if ((s = post_step_exchange(h, out, st))) return s;
+        if ((s = launch_interp(h, h->src, out, srca ? srca + (int64_t)(n - 1) * h->src.np : nullptr, st)))
+            return s;
+    }
+    if (h->nt % 2 == 0) return swap_halves(h, A, B, st);
+    return SF_OK;
+}
+
+extern "C" sf_status sf_residual(sf_handle *h, const float *d_syn, const float *d_obs, float *res,
+                                 double *J, void *stream)
+{
+    if (!h || !d_syn || !d_obs || !res) return sf_set_error(SF_ERR_INVALID_ARG, "NULL argument");
+    cudaStream_t st = S(stream);
+    const int64_t n = (int64_t)h->nt * h->rec.np;
+    const int nb = 1024;
+    k_residual<<<nb, 256, 0, st>>>(d_syn, d_obs, res, n, h->partial);
+    k_sum_partials<<<1, 32, 0, st>>>(h->partial, nb, h->dJ);
+    h->n_all += 2;
+    SF_CUDA_TRY(cudaGetLastError());
+    if (J) {
+        SF_CUDA_TRY(cudaMemcpyAsync(J, h->dJ, sizeof(double), cudaMemcpyDeviceToHost, st));
+        SF_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return SF_OK;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+extern "C" size_t sf_gradient_workspace_bytes(const sf_handle *h, int save_every)
+{
+    if (!h || save_every < 1) return 0;
+    const size_t N = (size_t)h->N;
+    const size_t nsnap = (size_t)((h->nt - 1) / save_every + 1);
+    return align256(sizeof(float) * N * nsnap) + 2 * align256(sizeof(float) * 2 * N) +
+           align256(sizeof(float) * (size_t)h->nt * std::max(h->rec.np, 1)) +
+           align256(sizeof(float) * (size_t)h->nt * std::max(h->src.np, 1));
+}
+
+extern "C" sf_status sf_gradient(sf_handle *h, const float *wavelet, const float *d_obs, float *grad,
+                                 double *J, void *ws, size_t ws_bytes, int save_every, void *stream)
+{
+    if (!h || !grad || !d_obs || !ws) return sf_set_error(SF_ERR_INVALID_ARG, "NULL argument");
+    if (save_every < 1) return sf_set_error(SF_ERR_INVALID_ARG, "save_every < 1");
+    if (ws_bytes < sf_gradient_workspace_bytes(h, save_every))
+        return sf_set_error(SF_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes,
+                            sf_gradient_workspace_bytes(h, save_every));
+    cudaStream_t st = S(stream);
+    const size_t N = (size_t)h->N;
+    const size_t nsnap = (size_t)((h->nt - 1) / save_every + 1);
+    char *p = static_cast<char *>(ws);
+    float *snaps = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * N * nsnap);
+    float *u = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * 2 * N);
+    float *v = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * 2 * N);
+    float *rec = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * (size_t)h->nt * std::max(h->rec.np, 1));
+    float *srca = reinterpret_cast<float *>(p);
+    SF_CUDA_TRY(cudaMemsetAsync(u, 0, sizeof(float) * 2 * N, st));
+    SF_CUDA_TRY(cudaMemsetAsync(v, 0, sizeof(float) * 2 * N, st));
+    SF_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * N, st));
+    sf_status s;
+    if ((s = sf_forward(h, wavelet, rec, u, snaps, save_every, st))) return s;
+    if (h->nranks > 1 && h->rec.np > 0) {  // every rank needs the full record (C18)
+        if ((s = sf_comm_allreduce_f32(h->comm, rec, (size_t)h->nt * h->rec.np, st))) return s;
+    }
+    if ((s = sf_residual(h, rec, d_obs, rec, J, st))) return s;
+    if ((s = sf_adjoint(h, rec, h->src.np > 0 ? srca : nullptr, v, snaps, save_every, grad, st))) return s;
+    return SF_OK;
+}
+
+// ------------------------------------------------------------------ end-to-end host form
+namespace {
+struct HostCache {
+    std::mutex mu;
+    float *m = nullptr, *damp = nullptr, *wav = nullptr, *rec = nullptr, *u = nullptr;
+    size_t nm = 0, nd = 0, nw = 0, nr = 0, nu = 0;
+};
+HostCache g_hc;
+
+sf_status ensure(float **p, size_t *cap, size_t n)
+{
+    if (n == 0) return SF_OK;
+    if (*cap >= n) return SF_OK;
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    SF_CUDA_TRY(cudaMalloc(p, n * sizeof(float)));
+    *cap = n;
+    return SF_OK;
+}
+}  // namespace
+
+extern "C" sf_status sf_forward_host(const sf_desc *hd, const float *wavelet_host, float *rec_host,
+                                     float *u_final_host, void *stream)
+{
+    sf_status s = validate_desc(hd);
+    if (s) return s;
+    cudaStream_t st = S(stream);
+    std::lock_guard<std::mutex> lk(g_hc.mu);
+    size_t N = 1;
+    for (int a = 0; a < hd->ndim; ++a) N *= (size_t)hd->shape[a];
+    const size_t nw = (size_t)hd->nt * hd->nsrc, nr = (size_t)hd->nt * hd->nrec;
+    if ((s = ensure(&g_hc.m, &g_hc.nm, N))) return s;
+    if (hd->damp && (s = ensure(&g_hc.damp, &g_hc.nd, N))) return s;
+    if ((s = ensure(&g_hc.wav, &g_hc.nw, nw))) return s;
+    if ((s = ensure(&g_hc.rec, &g_hc.nr, nr))) return s;
+    if ((s = ensure(&g_hc.u, &g_hc.nu, 2 * N))) return s;
+    SF_CUDA_TRY(cudaMemcpyAsync(g_hc.m, hd->m, N * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (hd->damp)
+        SF_CUDA_TRY(cudaMemcpyAsync(g_hc.damp, hd->damp, N * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (nw) SF_CUDA_TRY(cudaMemcpyAsync(g_hc.wav, wavelet_host, nw * sizeof(float), cudaMemcpyHostToDevice, st));
+    SF_CUDA_TRY(cudaMemsetAsync(g_hc.u, 0, 2 * N * sizeof(float), st));
+    SF_CUDA_TRY(cudaStreamSynchronize(st));  // sf_create runs on the legacy stream
+    sf_desc dd = *hd;
+    dd.m = g_hc.m;
+    dd.damp = hd->damp ? g_hc.damp : nullptr;
+    sf_handle *h = nullptr;
+    if ((s = sf_create(&dd, &h))) return s;
+    s = sf_forward(h, nw ? g_hc.wav : nullptr, nr ? g_hc.rec : nullptr, g_hc.u, nullptr, 0, st);
+    if (!s && nr && rec_host) {
+        cudaError_t e = cudaMemcpyAsync(rec_host, g_hc.rec, nr * sizeof(float), cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) s = sf_set_error(SF_ERR_CUDA, "rec download: %s", cudaGetErrorString(e));
+    }
+    if (!s && u_final_host) {
+        cudaError_t e = cudaMemcpyAsync(u_final_host, g_hc.u, 2 * N * sizeof(float), cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) s = sf_set_error(SF_ERR_CUDA, "u download: %s", cudaGetErrorString(e));
+    }
+    if (!s) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) s = sf_set_error(SF_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+    }
+    sf_destroy(h);
+    return s;
+}

@@ -1,0 +1,71 @@
+// sf_internal.h -- handle layout and helpers shared by the host translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sf.h"
+#include "launch.cuh"
+
+// Sparse point set on the device (one for sources, one for receivers).
+struct SfSparse {
+    int np = 0;          // points
+    int nc = 0;          // corners per point (2^ndim)
+    // interpolation (row p: nc corners, fixed order, last axis fastest)
+    int64_t *i_idx = nullptr;
+    float *i_w = nullptr;
+    int *i_owned = nullptr;  // slab mode: 1 if this rank writes the record row
+    // injection: CSR by target grid point
+    int ntgt = 0;
+    int nent = 0;
+    int64_t *j_tgt = nullptr;
+    int *j_rowptr = nullptr;
+    int *j_pt = nullptr;
+    float *j_coef = nullptr;  // W dt^2 / m[target]
+};
+
+struct sf_handle {
+    int ndim = 3;
+    int64_t gshape[3] = {1, 1, 1};  // global computational grid
+    int64_t nb[3] = {1, 1, 1};      // local buffer extents (axis 0 includes slab halos)
+    int64_t N = 0;                  // points in the local buffer
+    int64_t xa = 0, xb = 0;         // computed planes of the buffer
+    double h = 0, dt = 0;
+    int so = 0, r = 0, nt = 0;
+    SfWeights w{};
+    float *c3 = nullptr;
+    float *beta = nullptr;
+    bool damp = false;
+    SfSparse src, rec;
+    double *partial = nullptr;  // residual partial sums
+    double *dJ = nullptr;
+    // tuning
+    int variant = SF_VAR_AUTO, by = 0, chunks = 0;
+    // slab decomposition
+    int rank = 0, nranks = 1;
+    void *comm = nullptr;
+    int64_t x0 = 0, n0_loc = 0;
+    // profiling
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    long long n_stencil = 0, n_all = 0;
+};
+
+// error reporting (thread-local message)
+sf_status sf_set_error(sf_status s, const char *fmt, ...);
+#define SF_CUDA_TRY(call)                                                                  \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return sf_set_error(SF_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                __FILE__, __LINE__);                                       \
+    } while (0)
+
+// comm.cu
+sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st);
+sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st);
+sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st);

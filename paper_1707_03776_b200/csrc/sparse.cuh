@@ -1,0 +1,134 @@
+// sparse.cuh -- sparse-point kernels (injection, interpolation), residual/objective,
+// and the small setup kernels (coefficient hoisting, min reduction, state swap).
+//
+//   interpolate (reading C11):
+//       out[p] = sum_c W_{p,c} u[idx_{p,c}]        corners in fixed order, zero weights skipped
+//   inject (readings C3, C9):
+//       u[t] += delta_t,  delta_t = sum_{e in row t} coef_e * vals[pt_e],  coef_e = W_e dt^2/m[t]
+//     as a deterministic CSR gather by target grid point (no atomics: bitwise reproducible,
+//     SPEC.md:228 rationale).  Fused patches:
+//       save step:      snap[t] += delta_t              (snapshot taken before injection)
+//       gradient step:  grad[t] -= gscale * snap_n[t] * delta_t   (completes the in-kernel
+//                       correlation, which saw v^{n-1} before injection)
+//   residual (BASELINE configs[2]): res = d_syn - d_obs, J = 1/2 sum res^2 (fp64, fixed order)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__global__ void k_interp(const float *__restrict__ u, const int64_t *__restrict__ idx,
+                         const float *__restrict__ W, const int *__restrict__ owned, int np, int nc,
+                         float *__restrict__ out)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    float acc = 0.0f;
+    for (int c = 0; c < nc; ++c) {
+        const float w = W[(int64_t)p * nc + c];
+        if (w != 0.0f) acc = __fmaf_rn(w, u[idx[(int64_t)p * nc + c]], acc);
+    }
+    out[p] = owned ? (owned[p] ? acc : 0.0f) : acc;
+}
+
+__global__ void k_inject(float *__restrict__ u, const int64_t *__restrict__ tgt,
+                         const int *__restrict__ rowptr, const int *__restrict__ ent_pt,
+                         const float *__restrict__ ent_coef, int ntgt,
+                         const float *__restrict__ vals, float *__restrict__ snap_patch,
+                         const float *__restrict__ grad_snap, float *__restrict__ grad, float gscale)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntgt) return;
+    float d = 0.0f;
+    for (int e = rowptr[t]; e < rowptr[t + 1]; ++e) d = __fmaf_rn(ent_coef[e], vals[ent_pt[e]], d);
+    const int64_t g = tgt[t];
+    u[g] = __fadd_rn(u[g], d);
+    if (snap_patch) snap_patch[g] = __fadd_rn(snap_patch[g], d);
+    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(grad_snap[g], d), grad[g]);
+}
+
+// coef_e = W_e * dt^2 / m[t_e], computed in fp64, rounded once
+__global__ void k_inject_coef(const float *__restrict__ m, const int64_t *__restrict__ ent_tgt,
+                              const double *__restrict__ ent_w, int ne, double dt2,
+                              float *__restrict__ coef)
+{
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= ne) return;
+    coef[e] = (float)(ent_w[e] * dt2 / (double)m[ent_tgt[e]]);
+}
+
+// hoisted per-point coefficients: A = m + eta dt/2, beta = (m - eta dt/2)/A, c3 = dt^2/A (fp64)
+__global__ void k_hoist(const float *__restrict__ m, const float *__restrict__ damp, int64_t n,
+                        double dt, float *__restrict__ c3, float *__restrict__ beta)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double mm = m[i];
+        const double e = damp ? (double)damp[i] : 0.0;
+        const double A = mm + 0.5 * e * dt;
+        c3[i] = (float)(dt * dt / A);
+        if (beta) beta[i] = (float)((mm - 0.5 * e * dt) / A);
+    }
+}
+
+// min over a float array (positive floats order like their bit patterns; non-positive
+// values and NaN are reported through the flag)
+__global__ void k_min_m(const float *__restrict__ m, int64_t n, unsigned int *__restrict__ minbits,
+                        int *__restrict__ bad)
+{
+    unsigned int loc = 0x7f7fffffu;
+    int b = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = m[i];
+        if (!(v > 0.0f) || !(v < 3.0e38f)) b = 1;
+        else loc = min(loc, __float_as_uint(v));
+    }
+    for (int o = 16; o; o >>= 1) {
+        loc = min(loc, __shfl_xor_sync(0xffffffffu, loc, o));
+        b |= __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(minbits, loc);
+        if (b) atomicOr(bad, 1);
+    }
+}
+
+// res = a - b ; per-block fp64 partial sums of res^2 (fixed tree order)
+__global__ void k_residual(const float *__restrict__ a, const float *__restrict__ b,
+                           float *__restrict__ res, int64_t n, double *__restrict__ partial)
+{
+    __shared__ double sh[256];
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float r = __fsub_rn(a[i], b[i]);
+        res[i] = r;
+        acc += (double)r * (double)r;
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_sum_partials(const double *__restrict__ partial, int n, double *__restrict__ out)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += partial[i];
+        *out = 0.5 * s;
+    }
+}
+
+// elementwise swap of two arrays (restores the (u^{nt-2}, u^{nt-1}) output order)
+__global__ void k_swap(float *__restrict__ a, float *__restrict__ b, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float t = a[i];
+        a[i] = b[i];
+        b[i] = t;
+    }
+}

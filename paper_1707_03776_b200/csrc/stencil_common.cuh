@@ -1,0 +1,82 @@
+// stencil_common.cuh -- per-point arithmetic shared by every stencil kernel variant.
+//
+// One fixed evaluation order for every variant (generic thread-per-point, TMA 2.5D
+// streaming, slab boundary/interior launches), so that all variants -- and the
+// multi-GPU slab run vs the 1-GPU run -- produce identical bits (reading C18).
+//
+// Laplacian in the per-radius difference form (reading C15):
+//   P  = sum_{k=1..r} w_k * ( ((y_-k + y_+k) + (z_-k + z_+k)) - 4 u )   (3D; 2D: (z_-k + z_+k) - 2u)
+//   X  = sum_{k=1..r} w_k * ( (x_-k + x_+k) - 2 u )
+//   Lap = P + X,  w_k = fp32(w_k^exact / h^2)
+// so that a constant field is annihilated exactly (4u and 2u are exact) and the fp32
+// weights never need to sum to zero.  Update (the paper's solve(), with a
+// centred u.dt, reading C1), beta/c3 hoisted per point at setup:
+//   out = u + beta (u - old) + c3 * Lap
+// Gradient term formed in-register (reading C13/C14; north_star "g += v u_tt"):
+//   S = out - 2u + old (before injection) = (beta - 1)(u - old) + c3 * Lap
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define SF_MAXR 8
+
+struct SfWeights {
+    float w[SF_MAXR + 1];   // w[k], k = 1..r, already divided by h^2 (w[0] unused)
+};
+
+enum SfMode { SF_MODE_PLAIN = 0, SF_MODE_SAVE = 1, SF_MODE_GRAD = 2 };
+
+// in-plane term at radius k for 3D: ((ym + yp) + (zm + zp)) - 4u, as one fma
+__device__ __forceinline__ float sf_inplane3(float ym, float yp, float zm, float zp, float u)
+{
+    float s = __fadd_rn(__fadd_rn(ym, yp), __fadd_rn(zm, zp));
+    return __fmaf_rn(-4.0f, u, s);
+}
+
+// in-plane term at radius k for 2D (only z in-plane): (zm + zp) - 2u
+__device__ __forceinline__ float sf_inplane2(float zm, float zp, float u)
+{
+    return __fmaf_rn(-2.0f, u, __fadd_rn(zm, zp));
+}
+
+// x term at radius k: (xm + xp) - 2u
+__device__ __forceinline__ float sf_xterm(float xm, float xp, float u)
+{
+    return __fmaf_rn(-2.0f, u, __fadd_rn(xm, xp));
+}
+
+// out = u + beta (u - old) + c3 * lap
+__device__ __forceinline__ float sf_update(float u, float old, float beta, float c3, float lap)
+{
+    float d = __fsub_rn(u, old);
+    float o = __fmaf_rn(beta, d, u);
+    return __fmaf_rn(c3, lap, o);
+}
+
+// S = (beta - 1)(u - old) + c3 * lap
+__device__ __forceinline__ float sf_d2(float u, float old, float beta, float c3, float lap)
+{
+    float d = __fsub_rn(u, old);
+    return __fmaf_rn(__fsub_rn(beta, 1.0f), d, __fmul_rn(c3, lap));
+}
+
+// grad -= gscale * snap * S
+__device__ __forceinline__ float sf_grad(float g, float gscale, float snap, float S)
+{
+    return __fmaf_rn(-gscale, __fmul_rn(snap, S), g);
+}
+
+// Kernel parameter block shared by all stencil variants.
+struct SfStepArgs {
+    const float *cur;      // u^n (read, with neighbours)
+    float *out;            // old level on input (u^{n-1}), new level on output (in place)
+    const float *c3;       // hoisted dt^2 / A
+    const float *beta;     // hoisted (m - eta dt/2) / A, or NULL (== 1)
+    float *snap_out;       // SAVE: snapshot slot to write (== out values), else NULL
+    const float *snap_in;  // GRAD: u^n snapshot slot
+    float *grad;           // GRAD: gradient accumulator
+    float gscale;          // GRAD: k / dt^2
+    int64_t n0b, n1, n2;   // buffer extents (n0b includes slab halo planes)
+    int64_t xa, xb;        // planes [xa, xb) of the buffer to compute
+    SfWeights w;
+};

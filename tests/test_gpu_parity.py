@@ -1,0 +1,313 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle on the same seeded
+inputs.  Tolerance: relative L2 <= 1e-4 on records, final wavefields and gradients
+(BASELINE north_star); bitwise where the operation is exact (integer/index work,
+zero-in/zero-out, constant preservation, determinism, variant equivalence).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def sf():
+    import paper_1707_03776_b200 as m
+    return m
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def make_prop(p, m=None, **kw):
+    m = p.m if m is None else m
+    return sf().Propagator(dev(m), None if p.damp is None else dev(p.damp), shape=p.shape, h=p.h,
+                           space_order=p.space_order, nt=p.nt, dt=p.dt,
+                           src_coords=p.src_coords.astype(np.float64),
+                           rec_coords=p.rec_coords.astype(np.float64), **kw)
+
+
+def gpu_forward(p, variant=0, chunks=0, by=0, save_every=0, wavelet=None):
+    prop = make_prop(p)
+    prop.set_tuning(variant, by, chunks)
+    rec, u, snaps = prop.forward(dev(p.wavelet if wavelet is None else wavelet), save_every=save_every)
+    torch.cuda.synchronize()
+    out = (rec.cpu().numpy(), u.cpu().numpy(), None if snaps is None else snaps.cpu().numpy())
+    prop.close()
+    return out
+
+
+def oracle_forward(p, save_every=0, wavelet=None):
+    o = oracle.forward(p, save_every=save_every, wavelet=wavelet)
+    return o["rec"], o["u_state"], o["snaps"]
+
+
+# ------------------------------------------------------------------- forward parity
+@pytest.mark.parametrize("so", [2, 4, 6, 8, 10, 12, 14, 16])
+def test_forward_3d_all_orders_both_variants(so):
+    """3D, damping on, ragged tiles in every axis (n2 = 132: one full + one partial
+    128-column tile; n1 = 45; 37 planes split in 3 x-chunks)."""
+    p = synth.random_problem(3, (37, 45, 132), so, 60, seed=so, nbl=6, nsrc=2, nrec=9)
+    ro, uo, _ = oracle_forward(p)
+    results = {}
+    for variant, chunks in ((1, 0), (2, 1), (2, 3)):
+        rg, ug, _ = gpu_forward(p, variant=variant, chunks=chunks)
+        assert rel(rg, ro) <= TOL, (variant, chunks, rel(rg, ro))
+        assert rel(ug[1], uo[1]) <= TOL and rel(ug[0], uo[0]) <= TOL
+        results[(variant, chunks)] = (rg, ug)
+    # every variant evaluates the same per-point expression in the same order: identical bits
+    base = results[(1, 0)]
+    for k, v in results.items():
+        assert np.array_equal(v[0], base[0]) and np.array_equal(v[1], base[1]), k
+
+
+@pytest.mark.parametrize("by", [8, 16])
+def test_forward_3d_tma_block_heights(by):
+    p = synth.random_problem(3, (30, 50, 64), 8, 40, seed=7, nbl=5)
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p, variant=2, by=by, chunks=2)
+    assert rel(rg, ro) <= TOL and rel(ug[1], uo[1]) <= TOL
+
+
+def test_forward_3d_generic_when_n2_not_multiple_of_4():
+    p = synth.random_problem(3, (21, 23, 27), 4, 50, seed=3, nbl=4)
+    prop = make_prop(p)
+    assert prop.tuning()["variant"] == 1
+    prop.close()
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p)
+    assert rel(rg, ro) <= TOL and rel(ug[1], uo[1]) <= TOL
+
+
+@pytest.mark.parametrize("so", [2, 4, 8, 16])
+def test_forward_2d(so):
+    p = synth.random_problem(2, (61, 47), so, 150, seed=so + 1, nbl=8, nsrc=2, nrec=11)
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p)
+    assert rel(rg, ro) <= TOL and rel(ug[1], uo[1]) <= TOL and rel(ug[0], uo[0]) <= TOL
+
+
+def test_config0_full_size_vs_oracle_and_green():
+    """BASELINE configs[0] at its full size (141^2 comp grid, so4, nt=500)."""
+    p = synth.make_config(0)
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p)
+    assert rel(rg, ro) <= TOL
+    assert rel(ug[1], uo[1]) <= TOL
+
+
+def test_config1_reduced_vs_oracle():
+    """configs[1] structure (two layers, 40-pt layer scaled, surface receiver grid,
+    source off-node at the surface centre) at scale 1/4: 84^3, nt 250."""
+    p = synth.make_config(1, scale=0.25, nt=250)
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p)
+    assert rel(rg, ro) <= TOL and rel(ug[1], uo[1]) <= TOL
+
+
+def test_config1_full_grid_short_run_bench_launch():
+    """configs[1] at its FULL grid (336^3, so8, damping) in the launch configuration
+    bench.py times (auto tuning: TMA variant), short record (nt = 24) so the oracle
+    finishes; every receiver row and both final levels compared."""
+    p = synth.make_config(1, nt=24)
+    prop = make_prop(p)
+    assert prop.tuning()["variant"] == 2
+    prop.close()
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p)
+    assert rel(rg, ro) <= TOL
+    assert rel(ug[1], uo[1]) <= TOL and rel(ug[0], uo[0]) <= TOL
+
+
+def test_config3_shape_so16_no_damping_reduced():
+    """configs[3] structure (so16, no damping layer, layered model) at scale 1/8."""
+    p = synth.make_config(3, scale=0.125, nt=80)
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p)
+    assert rel(rg, ro) <= TOL and rel(ug[1], uo[1]) <= TOL
+
+
+# ------------------------------------------------------------------- snapshots / adjoint
+def test_forward_snapshots():
+    p = synth.random_problem(3, (26, 30, 64), 8, 41, seed=9, nbl=5)
+    ro, uo, so_ = oracle_forward(p, save_every=4)
+    rg, ug, sg = gpu_forward(p, save_every=4)
+    assert sg.shape == so_.shape
+    assert np.all(sg[0] == 0)
+    for k in range(1, sg.shape[0]):
+        assert rel(sg[k], so_[k]) <= TOL, k
+
+
+@pytest.mark.parametrize("ndim,shape,so", [(2, (51, 44), 4), (3, (28, 26, 64), 8), (3, (24, 22, 20), 6)])
+def test_adjoint_parity(ndim, shape, so):
+    p = synth.random_problem(ndim, shape, so, 70, seed=21, nbl=5, nsrc=2, nrec=8)
+    res = np.random.default_rng(1).standard_normal((p.nt, 8)).astype(np.float32)
+    ad = oracle.adjoint(p, res=res)
+    prop = make_prop(p)
+    srca, v, _ = prop.adjoint(dev(res))
+    torch.cuda.synchronize()
+    assert rel(srca.cpu().numpy(), ad["srca"]) <= TOL
+    assert rel(v.cpu().numpy()[1], ad["v_state"][1]) <= TOL
+
+
+@pytest.mark.parametrize("ndim,shape,so", [(2, (45, 41), 4), (3, (30, 28, 64), 8)])
+def test_dot_product_gpu_fp32(ndim, shape, so):
+    """<F x, y> = <x, F^T y> for the fp32 GPU operators: <= 1e-4."""
+    p = synth.random_problem(ndim, shape, so, 90, seed=4, nbl=6, nsrc=2, nrec=7, random_wavelet=True)
+    rng = np.random.default_rng(8)
+    y = rng.standard_normal((p.nt, 7)).astype(np.float32)
+    prop = make_prop(p)
+    rec, _, _ = prop.forward(dev(p.wavelet))
+    srca, _, _ = prop.adjoint(dev(y))
+    torch.cuda.synchronize()
+    a = float(np.sum(rec.cpu().numpy().astype(np.float64) * y))
+    b = float(np.sum(p.wavelet.astype(np.float64) * srca.cpu().numpy()))
+    assert abs(a - b) / abs(a) <= 1e-4
+
+
+# ------------------------------------------------------------------- gradient
+def _grad_problem(ndim=3):
+    if ndim == 3:
+        p = synth.make_config(2, scale=0.125, nt=120)   # 32^3 + 5-pt layer, 5 layers + anomaly
+    else:
+        p = synth.random_problem(2, (50, 44), 4, 150, seed=2, nbl=6, nsrc=1, nrec=12)
+        p.m_true = (p.m * 0.97).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    return p, d_obs
+
+
+@pytest.mark.parametrize("k", [1, 3, 4])
+def test_gradient_parity_3d(k):
+    p, d_obs = _grad_problem(3)
+    go = oracle.gradient(p, d_obs, save_every=k)
+    prop = make_prop(p)
+    g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=k)
+    torch.cuda.synchronize()
+    assert rel(g.cpu().numpy(), go["grad"]) <= TOL, rel(g.cpu().numpy(), go["grad"])
+    assert abs(J - go["J"]) <= 1e-4 * go["J"]
+
+
+def test_gradient_parity_2d_and_components():
+    p, d_obs = _grad_problem(2)
+    go = oracle.gradient(p, d_obs, save_every=2)
+    prop = make_prop(p)
+    # component calls: forward with snapshots, residual, adjoint with correlation
+    rec, _, snaps = prop.forward(dev(p.wavelet), save_every=2)
+    res, J = prop.residual(rec, dev(d_obs))
+    _, _, g = prop.adjoint(res, snaps=snaps, save_every=2)
+    torch.cuda.synchronize()
+    assert rel(res.cpu().numpy(), go["res"]) <= TOL
+    assert rel(g.cpu().numpy(), go["grad"]) <= TOL
+    g2, J2 = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
+    assert np.array_equal(g2.cpu().numpy(), g.cpu().numpy()) and J2 == J
+
+
+def test_residual_objective_fp64():
+    p = synth.random_problem(2, (20, 20), 4, 300, seed=1, nbl=0, nrec=50, damp=False)
+    prop = make_prop(p)
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((300, 50)).astype(np.float32)
+    b = rng.standard_normal((300, 50)).astype(np.float32)
+    res, J = prop.residual(dev(a), dev(b))
+    r = a.astype(np.float64) - b.astype(np.float64)
+    assert np.array_equal(res.cpu().numpy(), (a - b))
+    assert abs(J - 0.5 * np.sum(r * r)) <= 1e-12 * J
+
+
+# ------------------------------------------------------------------- invariants / edges
+def test_zero_in_zero_out_and_determinism():
+    p = synth.make_config(1, scale=0.25, nt=60)
+    rg, ug, _ = gpu_forward(p, wavelet=np.zeros_like(p.wavelet))
+    assert not rg.any() and not ug.any()
+    a = gpu_forward(p)
+    b = gpu_forward(p)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_constant_preserved_bitwise_interior():
+    """eta = 0, no source: a constant field is annihilated exactly by the difference-form
+    Laplacian (reading C15) -> bitwise constant away from the zero halo."""
+    n, so, nt = 40, 8, 5
+    p = synth.random_problem(3, (n, n, 64), so, nt, seed=3, nbl=0, damp=False)
+    prop = make_prop(p)
+    u0 = torch.full((2, n, n, 64), 0.7311, device="cuda")
+    _, u, _ = prop.forward(torch.zeros((nt, 2), device="cuda"), u=u0)
+    k = (so // 2) * nt
+    core = u.cpu().numpy()[1][k:-k, k:-k, k:-k]
+    assert np.all(core == np.float32(0.7311))
+
+
+def test_single_step_and_no_sparse_points():
+    p = synth.random_problem(3, (20, 21, 32), 4, 2, seed=5, nbl=0)
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p)
+    assert rel(rg, ro) <= TOL and rel(ug[1], uo[1]) <= TOL
+    # no sources, no receivers, nonzero initial state
+    st = np.random.default_rng(2).standard_normal((2, 20, 21, 32)).astype(np.float32)
+    o = oracle.forward(m=p.m, damp=p.damp, shape=p.shape, h=p.h, space_order=4, nt=9, dt=p.dt,
+                       src_coords=None, wavelet=None, rec_coords=None, u_state=st)
+    prop = sf().Propagator(dev(p.m), None if p.damp is None else dev(p.damp), shape=p.shape, h=p.h,
+                           space_order=4, nt=9, dt=p.dt)
+    _, u, _ = prop.forward(None, u=dev(st))
+    assert rel(u.cpu().numpy(), o["u_state"]) <= TOL
+
+
+def test_receivers_on_last_node_clamp():
+    p = synth.random_problem(3, (16, 18, 20), 4, 30, seed=6, nbl=0)
+    n = np.array(p.shape)
+    p.rec_coords = np.array([(n - 1) * p.h, [0.0, 0.0, 0.0], [(n[0] - 1) * p.h, 0.0, 3.5 * p.h]],
+                            dtype=np.float32)
+    ro, _, _ = oracle_forward(p)
+    rg, _, _ = gpu_forward(p)
+    assert rel(rg, ro) <= TOL
+
+
+def test_errors():
+    p = synth.random_problem(3, (16, 16, 16), 4, 10, seed=0, nbl=0)
+    S = sf()
+    with pytest.raises(S.SfError) as e:
+        S.Propagator(dev(p.m), None, shape=p.shape, h=p.h, space_order=4, nt=10, dt=p.dt,
+                     rec_coords=np.array([[0.0, 0.0, 15.01 * p.h]]))
+    assert e.value.status == "SF_ERR_OUT_OF_DOMAIN"
+    with pytest.raises(S.SfError) as e:
+        S.Propagator(dev(p.m), None, shape=p.shape, h=p.h, space_order=4, nt=10, dt=p.dt * 2.0)
+    assert e.value.status == "SF_ERR_CFL"
+    with pytest.raises(S.SfError) as e:
+        S.Propagator(dev(p.m), None, shape=p.shape, h=p.h, space_order=5, nt=10, dt=p.dt)
+    assert e.value.status == "SF_ERR_ORDER"
+    bad = p.m.copy()
+    bad[3, 3, 3] = -1.0
+    with pytest.raises(S.SfError) as e:
+        S.Propagator(dev(bad), None, shape=p.shape, h=p.h, space_order=4, nt=10, dt=p.dt)
+    assert e.value.status == "SF_ERR_INVALID_ARG"
+
+
+def test_forward_host_matches_device():
+    p = synth.make_config(1, scale=0.2, nt=50)
+    rg, ug, _ = gpu_forward(p)
+    u = np.empty((2,) + p.shape, np.float32)
+    rh = sf().forward_host(p.m, p.damp, h=p.h, space_order=p.space_order, nt=p.nt, dt=p.dt,
+                           src_coords=p.src_coords, wavelet=p.wavelet, rec_coords=p.rec_coords,
+                           u_out=u)
+    assert np.array_equal(rh, rg) and np.array_equal(u, ug)
+
+
+def test_profiling_counts():
+    p = synth.make_config(1, scale=0.2, nt=30)
+    prop = make_prop(p)
+    prop.set_profiling(True)
+    prop.forward(dev(p.wavelet))
+    prof = prop.profile()
+    assert prof["stencil_launches"] == p.nt - 1 and prof["stencil_ms"] > 0
+    assert prof["launches"] >= 3 * (p.nt - 1)
