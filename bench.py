@@ -236,7 +236,9 @@ def run_ours(args):
                          "kernel": "k_tma3d (stencil step, fwd)" if tuning["variant"] == 2 else "k_generic3d",
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "bytes_per_point": bpp, "avg_launch_ms": round(launch_ms, 5),
-                         "stencil_share_of_step": round(prof["stencil_ms"] / max(ms, 1e-9), 4)},
+                         "stencil_share_of_step": round(prof["stencil_ms"] / max(ms, 1e-9), 4),
+                         "per_update_us": {k: round(prof[f"{k}_ms"] * 1e3 / (args.steps * (p.nt - 1)), 2)
+                                           for k in ("stencil", "inject", "interp", "other")}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(prof["launches"]),

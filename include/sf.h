@@ -139,6 +139,11 @@ SF_API sf_status sf_set_profiling(sf_handle *h, int on);
 SF_API sf_status sf_get_profile(sf_handle *h, double *stencil_ms, long long *stencil_launches,
                          long long *all_launches, int reset);
 
+/* Per-kind launch times: ms_by_kind[4] / launches_by_kind[4] = {stencil, inject,
+ * interpolate, other (swap, residual)}; synchronises like sf_get_profile. */
+SF_API sf_status sf_get_profile_detail(sf_handle *h, double *ms_by_kind, long long *launches_by_kind,
+                                       int reset);
+
 /* Tuning: kernel variant (0 auto, 1 generic thread-per-point, 2 TMA 2.5D streaming),
  * warps per CTA along y (0 auto, 8 or 16) and x-chunks per column (0 auto). */
 SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int by, int chunks);

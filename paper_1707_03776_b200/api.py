@@ -155,10 +155,16 @@ class Propagator:
         check(lib().sf_set_profiling(self._h, 1 if on else 0))
 
     def profile(self, reset: bool = True):
-        ms, ns, na = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_longlong()
-        check(lib().sf_get_profile(self._h, ctypes.byref(ms), ctypes.byref(ns), ctypes.byref(na),
-                                   1 if reset else 0))
-        return {"stencil_ms": ms.value, "stencil_launches": ns.value, "launches": na.value}
+        """Summed in-stream kernel times (CUDA events) and launch counts since the last
+        reset, by kind: stencil / inject / interp / other."""
+        ms = (ctypes.c_double * 4)()
+        cnt = (ctypes.c_longlong * 4)()
+        check(lib().sf_get_profile_detail(self._h, ms, cnt, 1 if reset else 0))
+        kinds = ("stencil", "inject", "interp", "other")
+        out = {f"{k}_ms": ms[i] for i, k in enumerate(kinds)}
+        out.update({f"{k}_launches": cnt[i] for i, k in enumerate(kinds)})
+        out["launches"] = sum(cnt)
+        return out
 
     # -------------------------------------------------------------- the path
     def forward(self, wavelet: Optional[torch.Tensor], *, u: Optional[torch.Tensor] = None,

@@ -131,6 +131,7 @@ sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st)
     }
     SF_NCCL_TRY(api().GroupEnd());
     h->n_all++;
+    h->n_kind[3]++;
     return SF_OK;
 }
 

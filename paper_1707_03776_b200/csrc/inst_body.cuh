@@ -28,7 +28,7 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
     const int chunk = (int)((planes + nchunks - 1) / nchunks);
     const int nch = (int)((planes + chunk - 1) / chunk);
     dim3 grid((unsigned)((a.n2 + C::TZ - 1) / C::TZ), (unsigned)((a.n1 + BY - 1) / BY), (unsigned)nch);
-    dim3 block(32, BY);
+    dim3 block(32, BY + 1);  // BY consumer warps + 1 TMA producer warp
     kern<<<grid, block, C::SMEM, st>>>(L.maps->cur, L.maps->old, L.maps->c3, L.maps->beta,
                                        L.maps->snap, L.maps->grad, a, L.snap_slot, chunk);
     return cudaGetLastError();

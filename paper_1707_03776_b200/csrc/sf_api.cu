@@ -152,25 +152,23 @@ static int resolve_by(const sf_handle *h)
     return h->r <= 4 ? 16 : 8;
 }
 
-// x-chunks per tile column: balance whole waves of one CTA per SM against the 2r
-// warm-up planes each chunk re-reads (SURVEY H2 parallelism model).
+// x-chunks per tile column.  Measured on B200 (scripts/tune.py, profiles/): with the
+// TMA pipeline one partial wave of CTAs already saturates HBM, so when the (y, z)
+// tiles fit in one wave we take the largest chunk count that keeps a single wave
+// (fewest 2r warm-up planes); otherwise balance whole waves against the warm-up
+// planes each chunk re-reads (SURVEY H2 model).
 static int resolve_chunks(const sf_handle *h, int by)
 {
     if (h->chunks > 0) return h->chunks;
     const int64_t planes = h->xb - h->xa;
     const int64_t tiles = ((h->nb[2] + 127) / 128) * ((h->nb[1] + by - 1) / by);
-    int sms = 148;
-    {
-        int dev = 0, v = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
-            sms = v;
-    }
-    const int per_sm = by == 8 ? 2 : 1;
+    const int sms = h->sms;
+    const int per_sm = (by == 8 && h->r <= 4) ? 2 : 1;
     const int64_t slots = (int64_t)sms * per_sm;
+    const int64_t cmax = std::max<int64_t>(1, planes / std::max(2 * h->r, 8));
+    if (tiles <= slots) return (int)std::max<int64_t>(1, std::min<int64_t>(cmax, slots / tiles));
     double best = 1e300;
     int bestc = 1;
-    const int64_t cmax = std::max<int64_t>(1, planes / std::max(2 * h->r, 8));
     for (int64_t c = 1; c <= cmax && c <= 4096; ++c) {
         const int64_t chunk = (planes + c - 1) / c;
         const int64_t nch = (planes + chunk - 1) / chunk;
@@ -185,7 +183,9 @@ static int resolve_chunks(const sf_handle *h, int by)
     return bestc;
 }
 
-// prof events
+// ---- profiling: CUDA events around every launch, grouped by kind (stream-ordered)
+enum { PK_STENCIL = 0, PK_INJECT = 1, PK_INTERP = 2, PK_OTHER = 3, PK_N = 4 };
+
 static cudaEvent_t next_event(sf_handle *h)
 {
     if (h->ev_used == h->ev_pool.size()) {
@@ -196,6 +196,27 @@ static cudaEvent_t next_event(sf_handle *h)
     return h->ev_pool[h->ev_used++];
 }
 
+struct ProfScope {
+    sf_handle *h;
+    cudaStream_t st;
+    cudaEvent_t e1 = nullptr;
+    ProfScope(sf_handle *h_, int kind, cudaStream_t st_) : h(h_), st(st_)
+    {
+        h->n_all++;
+        h->n_kind[kind]++;
+        if (h->prof) {
+            cudaEvent_t e0 = next_event(h);
+            e1 = next_event(h);
+            h->ev_kind.push_back(kind);
+            cudaEventRecord(e0, st);
+        }
+    }
+    ~ProfScope()
+    {
+        if (e1) cudaEventRecord(e1, st);
+    }
+};
+
 struct StepBufs {
     const float *cur;
     float *out;
@@ -205,10 +226,71 @@ struct StepBufs {
     int64_t nsnap;
     float *grad;
     float gscale;
+    SfSparse *inj;         // point set injected after this step (or NULL)
+    const float *inj_vals; // its values for this step ([npoint])
 };
 
-static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStream_t st)
+template <class T>
+static sf_status upload(T **dst, const std::vector<T> &v)
 {
+    if (v.empty()) return SF_OK;
+    SF_CUDA_TRY(cudaMalloc((void **)dst, v.size() * sizeof(T)));
+    SF_CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return SF_OK;
+}
+
+// Per-(y, z)-tile lists of the injection targets for the TMA kernel's fused epilogue
+// (built once per point set and tile height; see SfStepArgs::inj_*).
+static sf_status ensure_inj_tiles(sf_handle *h, SfSparse &sp, int by)
+{
+    SfInjTiles &T = sp.tiles;
+    if (T.by == by) return SF_OK;
+    cudaFree(T.beg);
+    cudaFree(T.q);
+    cudaFree(T.pos);
+    cudaFree(T.t);
+    T = SfInjTiles{};
+    const int64_t n1 = h->nb[1], n2 = h->nb[2];
+    const int64_t ntz = (n2 + 127) / 128, nty = (n1 + by - 1) / by;
+    const int64_t ntiles = ntz * nty;
+    struct E {
+        int tile, q, pos, t;
+    };
+    std::vector<E> es;
+    es.reserve(sp.h_tgt.size());
+    for (size_t t = 0; t < sp.h_tgt.size(); ++t) {
+        const int64_t off = sp.h_tgt[t];
+        const int64_t x = off / (n1 * n2), y = (off / n2) % n1, z = off % n2;
+        const int tile = (int)((y / by) * ntz + z / 128);
+        const int pos = (int)((((y % by) * 32) + (z % 128) / 4) * 4 + (z % 4));
+        es.push_back({tile, (int)x, pos, (int)t});
+    }
+    std::sort(es.begin(), es.end(), [](const E &a, const E &b) {
+        return std::tie(a.tile, a.q, a.pos) < std::tie(b.tile, b.q, b.pos);
+    });
+    std::vector<int> beg(ntiles + 1, 0), q, pos, tt;
+    for (const E &e : es) beg[e.tile + 1]++;
+    for (int64_t i = 0; i < ntiles; ++i) beg[i + 1] += beg[i];
+    for (const E &e : es) {
+        q.push_back(e.q);
+        pos.push_back(e.pos);
+        tt.push_back(e.t);
+    }
+    sf_status s;
+    if ((s = upload(&T.beg, beg))) return s;
+    if (!es.empty()) {
+        if ((s = upload(&T.q, q))) return s;
+        if ((s = upload(&T.pos, pos))) return s;
+        if ((s = upload(&T.t, tt))) return s;
+    }
+    T.by = by;
+    return SF_OK;
+}
+
+static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStream_t st,
+                             bool *fused)
+{
+    *fused = false;
     SfStepArgs a{};
     a.cur = b.cur;
     a.out = b.out;
@@ -259,17 +341,25 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         }
     }
     L.maps = &maps;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->prof) {
-        e0 = next_event(h);
-        e1 = next_event(h);
-        cudaEventRecord(e0, st);
+    if (L.variant == SF_VAR_TMA && b.inj && b.inj->ntgt > 0 && b.inj_vals) {
+        sf_status s = ensure_inj_tiles(h, *b.inj, L.by);
+        if (s) return s;
+        a.inj_beg = b.inj->tiles.beg;
+        a.inj_q = b.inj->tiles.q;
+        a.inj_pos = b.inj->tiles.pos;
+        a.inj_t = b.inj->tiles.t;
+        a.inj_rowptr = b.inj->j_rowptr;
+        a.inj_pt = b.inj->j_pt;
+        a.inj_coef = b.inj->j_coef;
+        a.inj_vals = b.inj_vals;
+        *fused = true;
     }
-    cudaError_t e = launch_step_r(h->r, L, a, st);
-    if (h->prof) cudaEventRecord(e1, st);
+    cudaError_t e;
+    {
+        ProfScope ps(h, PK_STENCIL, st);
+        e = launch_step_r(h->r, L, a, st);
+    }
     if (e != cudaSuccess) return sf_set_error(SF_ERR_CUDA, "stencil launch: %s", cudaGetErrorString(e));
-    h->n_stencil++;
-    h->n_all++;
     return SF_OK;
 }
 
@@ -277,8 +367,8 @@ static sf_status launch_interp(sf_handle *h, const SfSparse &sp, const float *u,
                                cudaStream_t st)
 {
     if (sp.np == 0 || !out) return SF_OK;
+    ProfScope ps(h, PK_INTERP, st);
     k_interp<<<(sp.np + 127) / 128, 128, 0, st>>>(u, sp.i_idx, sp.i_w, sp.i_owned, sp.np, sp.nc, out);
-    h->n_all++;
     SF_CUDA_TRY(cudaGetLastError());
     return SF_OK;
 }
@@ -288,9 +378,9 @@ static sf_status launch_inject(sf_handle *h, const SfSparse &sp, float *u, const
                                cudaStream_t st)
 {
     if (sp.ntgt == 0 || !vals) return SF_OK;
+    ProfScope ps(h, PK_INJECT, st);
     k_inject<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.j_rowptr, sp.j_pt, sp.j_coef,
                                                      sp.ntgt, vals, snap_patch, grad_snap, grad, gscale);
-    h->n_all++;
     SF_CUDA_TRY(cudaGetLastError());
     return SF_OK;
 }
@@ -305,17 +395,13 @@ static void free_sparse(SfSparse &s)
     cudaFree(s.j_rowptr);
     cudaFree(s.j_pt);
     cudaFree(s.j_coef);
+    cudaFree(s.tiles.beg);
+    cudaFree(s.tiles.q);
+    cudaFree(s.tiles.pos);
+    cudaFree(s.tiles.t);
     s = SfSparse{};
 }
 
-template <class T>
-static sf_status upload(T **dst, const std::vector<T> &v)
-{
-    if (v.empty()) return SF_OK;
-    SF_CUDA_TRY(cudaMalloc((void **)dst, v.size() * sizeof(T)));
-    SF_CUDA_TRY(cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
-    return SF_OK;
-}
 
 // Reading C11: pos = x/h; base = min(floor(pos), n-2); xi = pos - base; weights =
 // product of (1 - xi) / xi; corners ordered last-axis fastest; outside [0, n-1] is an
@@ -401,6 +487,7 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
     rowptr.push_back((int)ents.size());
     out.np = np;
     out.nc = nc;
+    out.h_tgt = tgt;
     out.ntgt = (int)tgt.size();
     out.nent = (int)ents.size();
     sf_status s;
@@ -458,6 +545,12 @@ extern "C" void sf_destroy(sf_handle *h)
 
 static sf_status create_common(const sf_desc *d, sf_handle *h)
 {
+    {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+            h->sms = v;
+    }
     const int r = d->space_order / 2;
     h->so = d->space_order;
     h->r = r;
@@ -649,25 +742,47 @@ extern "C" sf_status sf_set_profiling(sf_handle *h, int on)
     return SF_OK;
 }
 
-extern "C" sf_status sf_get_profile(sf_handle *h, double *ms, long long *nst, long long *nall, int reset)
+static sf_status collect_profile(sf_handle *h, double *ms_kind, long long *n_kind, long long *nall,
+                                 int reset)
 {
-    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
-    double tot = 0.0;
+    double tot[PK_N] = {0, 0, 0, 0};
     for (size_t i = 0; i + 1 < h->ev_used; i += 2) {
         SF_CUDA_TRY(cudaEventSynchronize(h->ev_pool[i + 1]));
         float t = 0.f;
         SF_CUDA_TRY(cudaEventElapsedTime(&t, h->ev_pool[i], h->ev_pool[i + 1]));
-        tot += t;
+        tot[h->ev_kind[i / 2]] += t;
     }
-    if (ms) *ms = tot;
-    if (nst) *nst = h->n_stencil;
+    for (int k = 0; k < PK_N; ++k) {
+        if (ms_kind) ms_kind[k] = tot[k];
+        if (n_kind) n_kind[k] = h->n_kind[k];
+    }
     if (nall) *nall = h->n_all;
     if (reset) {
         h->ev_used = 0;
-        h->n_stencil = 0;
+        h->ev_kind.clear();
+        for (int k = 0; k < PK_N; ++k) h->n_kind[k] = 0;
         h->n_all = 0;
     }
     return SF_OK;
+}
+
+extern "C" sf_status sf_get_profile(sf_handle *h, double *ms, long long *nst, long long *nall, int reset)
+{
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    double mk[PK_N];
+    long long nk[PK_N];
+    sf_status s = collect_profile(h, mk, nk, nall, reset);
+    if (s) return s;
+    if (ms) *ms = mk[PK_STENCIL];
+    if (nst) *nst = nk[PK_STENCIL];
+    return SF_OK;
+}
+
+extern "C" sf_status sf_get_profile_detail(sf_handle *h, double *ms_by_kind, long long *launches_by_kind,
+                                           int reset)
+{
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    return collect_profile(h, ms_by_kind, launches_by_kind, nullptr, reset);
 }
 
 // ------------------------------------------------------------------ time loops
@@ -679,8 +794,8 @@ static sf_status post_step_exchange(sf_handle *h, float *buf, cudaStream_t st)
 
 static sf_status swap_halves(sf_handle *h, float *a, float *b, cudaStream_t st)
 {
+    ProfScope ps(h, PK_OTHER, st);
     k_swap<<<1184, 256, 0, st>>>(a, b, h->N);
-    h->n_all++;
     SF_CUDA_TRY(cudaGetLastError());
     return SF_OK;
 }
@@ -706,10 +821,11 @@ extern "C" sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, 
         float *out = (n % 2 == 0) ? A : B;
         const bool save = snaps && ((n + 1) % save_every == 0);
         float *slot = save ? snaps + (int64_t)((n + 1) / save_every) * N : nullptr;
-        StepBufs b{cur, out, slot, nullptr, 0, 0, nullptr, 0.f};
-        if ((s = launch_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, st))) return s;
-        if ((s = launch_inject(h, h->src, out, wavelet ? wavelet + (int64_t)n * h->src.np : nullptr,
-                               slot, nullptr, nullptr, 0.f, st)))
+        const float *wrow = wavelet ? wavelet + (int64_t)n * h->src.np : nullptr;
+        StepBufs b{cur, out, slot, nullptr, 0, 0, nullptr, 0.f, &h->src, wrow};
+        bool fused = false;
+        if ((s = launch_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, st, &fused))) return s;
+        if (!fused && (s = launch_inject(h, h->src, out, wrow, slot, nullptr, nullptr, 0.f, st)))
             return s;
         if ((s = post_step_exchange(h, out, st))) return s;
         if ((s = launch_interp(h, h->rec, out, rec ? rec + (int64_t)(n + 1) * h->rec.np : nullptr, st)))
@@ -744,12 +860,14 @@ extern "C" sf_status sf_adjoint(sf_handle *h, const float *res, float *srca, flo
         float *cur = (j % 2 == 0) ? B : A;
         float *out = (j % 2 == 0) ? A : B;
         const bool g = dograd && (n % save_every == 0);
+        const float *rrow = res ? res + (int64_t)n * h->rec.np : nullptr;
         StepBufs b{cur, out, nullptr, g ? snaps : nullptr, g ? n / save_every : 0, nsnap,
-                   g ? grad : nullptr, gscale};
-        if ((s = launch_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, st))) return s;
-        if ((s = launch_inject(h, h->rec, out, res ? res + (int64_t)n * h->rec.np : nullptr, nullptr,
-                               g ? snaps + (int64_t)(n / save_every) * N : nullptr,
-                               g ? grad : nullptr, gscale, st)))
+                   g ? grad : nullptr, gscale, &h->rec, rrow};
+        bool fused = false;
+        if ((s = launch_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, st, &fused))) return s;
+        if (!fused && (s = launch_inject(h, h->rec, out, rrow, nullptr,
+                                         g ? snaps + (int64_t)(n / save_every) * N : nullptr,
+                                         g ? grad : nullptr, gscale, st)))
             return s;
         if ((s = post_step_exchange(h, out, st))) return s;
         if ((s = launch_interp(h, h->src, out, srca ? srca + (int64_t)(n - 1) * h->src.np : nullptr, st)))
@@ -766,9 +884,14 @@ extern "C" sf_status sf_residual(sf_handle *h, const float *d_syn, const float *
     cudaStream_t st = S(stream);
     const int64_t n = (int64_t)h->nt * h->rec.np;
     const int nb = 1024;
-    k_residual<<<nb, 256, 0, st>>>(d_syn, d_obs, res, n, h->partial);
-    k_sum_partials<<<1, 32, 0, st>>>(h->partial, nb, h->dJ);
-    h->n_all += 2;
+    {
+        ProfScope ps(h, PK_OTHER, st);
+        k_residual<<<nb, 256, 0, st>>>(d_syn, d_obs, res, n, h->partial);
+    }
+    {
+        ProfScope ps(h, PK_OTHER, st);
+        k_sum_partials<<<1, 32, 0, st>>>(h->partial, nb, h->dJ);
+    }
     SF_CUDA_TRY(cudaGetLastError());
     if (J) {
         SF_CUDA_TRY(cudaMemcpyAsync(J, h->dJ, sizeof(double), cudaMemcpyDeviceToHost, st));

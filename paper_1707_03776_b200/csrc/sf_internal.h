@@ -10,6 +10,13 @@
 #include "../../include/sf.h"
 #include "launch.cuh"
 
+// Injection targets grouped by (y, z) tile of the TMA kernel (fused injection).
+struct SfInjTiles {
+    int by = 0;          // tile height the lists were built for (0 = not built)
+    int *beg = nullptr;  // [ntiles + 1]
+    int *q = nullptr, *pos = nullptr, *t = nullptr;
+};
+
 // Sparse point set on the device (one for sources, one for receivers).
 struct SfSparse {
     int np = 0;          // points
@@ -25,6 +32,8 @@ struct SfSparse {
     int *j_rowptr = nullptr;
     int *j_pt = nullptr;
     float *j_coef = nullptr;  // W dt^2 / m[target]
+    std::vector<int64_t> h_tgt;  // host copy of the target offsets
+    SfInjTiles tiles;
 };
 
 struct sf_handle {
@@ -51,8 +60,11 @@ struct sf_handle {
     // profiling
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
+    std::vector<int> ev_kind;       // kind of event pair i (stencil / inject / interp / other)
     size_t ev_used = 0;
-    long long n_stencil = 0, n_all = 0;
+    long long n_kind[4] = {0, 0, 0, 0};
+    long long n_all = 0;
+    int sms = 148;                  // multiprocessors of the device (set at create)
 };
 
 // error reporting (thread-local message)

@@ -66,6 +66,50 @@ __device__ __forceinline__ float sf_grad(float g, float gscale, float snap, floa
     return __fmaf_rn(-gscale, __fmul_rn(snap, S), g);
 }
 
+// ---- packed fp32x2 forms (sm_100a FADD2 / FFMA2 / FMUL2): two lanes of exactly the
+// scalar IEEE round-to-nearest operations above, so results are bitwise identical to
+// the scalar path while the FP issue count halves.
+typedef unsigned long long f2_t;
+
+__device__ __forceinline__ f2_t pk2(float lo, float hi)
+{
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk2(f2_t v, float &lo, float &hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b)
+{
+    f2_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b)
+{
+    f2_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c)
+{
+    f2_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+// ((ym + yp) + (zm + zp)) - 4u  (== sf_inplane3 per lane)
+__device__ __forceinline__ f2_t sf_inplane3_x2(f2_t ym, f2_t yp, f2_t zm, f2_t zp, f2_t u, f2_t m4)
+{
+    return fma2(m4, u, add2(add2(ym, yp), add2(zm, zp)));
+}
+// (xm + xp) - 2u  (== sf_xterm per lane)
+__device__ __forceinline__ f2_t sf_xterm_x2(f2_t xm, f2_t xp, f2_t u, f2_t m2)
+{
+    return fma2(m2, u, add2(xm, xp));
+}
+
 // Kernel parameter block shared by all stencil variants.
 struct SfStepArgs {
     const float *cur;      // u^n (read, with neighbours)
@@ -79,4 +123,10 @@ struct SfStepArgs {
     int64_t n0b, n1, n2;   // buffer extents (n0b includes slab halo planes)
     int64_t xa, xb;        // planes [xa, xb) of the buffer to compute
     SfWeights w;
+    // fused source injection (TMA kernel epilogue; NULL inj_beg = none).  Per (y, z)
+    // tile t = blockIdx.y * gridDim.x + blockIdx.x, entries [inj_beg[t], inj_beg[t+1])
+    // sorted by output plane: inj_q (buffer plane), inj_pos ((warp*32 + lane)*4 + j),
+    // inj_t (row of the injection CSR: rowptr / pt / coef, values vals[pt]).
+    const int *inj_beg, *inj_q, *inj_pos, *inj_t, *inj_rowptr, *inj_pt;
+    const float *inj_coef, *inj_vals;
 };

@@ -41,6 +41,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
                  : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     uint32_t done = 0;
@@ -98,91 +103,122 @@ struct Cfg {
     static constexpr int PL_BYTES = TZ * BY * 4;         // one plane without halo
     static constexpr int NPL = 2 + (DAMP ? 1 : 0) + (MODE == SF_MODE_GRAD ? 2 : 0);
     static constexpr int STAGE_BYTES = CUR_BYTES + NPL * PL_BYTES;
-    static constexpr int S_MAX = (220 * 1024) / STAGE_BYTES;
+    static constexpr int PRING = R + 1;                  // in-plane partials kept for R planes
+    static constexpr int PRING_BYTES = PRING * PL_BYTES;
+    static constexpr int S_MAX = (220 * 1024 - PRING_BYTES) / STAGE_BYTES;
     static constexpr int S = S_MAX >= 4 ? 4 : S_MAX;      // pipeline depth
-    static constexpr int SMEM = S * STAGE_BYTES + 128;    // + alignment slack
+    static constexpr int SMEM = S * STAGE_BYTES + PRING_BYTES + 128;  // + alignment slack
+    static constexpr int THREADS = 32 * (BY + 1);         // BY consumer warps + 1 TMA producer warp
     static_assert(S >= 2, "stage does not fit shared memory");
 };
 
+// One CTA = BY consumer warps (one y row each, 4 z per lane) + 1 producer warp whose
+// elected lane issues every TMA load.  Per stage: `full` (TMA transaction bytes) and
+// `empty` (one arrive per consumer warp) mbarriers.
 template <int R, int BY, bool DAMP, int MODE>
-__global__ void __launch_bounds__(32 * BY, 1)
+__global__ void __launch_bounds__(32 * (BY + 1), (BY == 8 && R <= 4) ? 2 : 1)
 k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_old,
         const __grid_constant__ CUtensorMap tm_c3, const __grid_constant__ CUtensorMap tm_beta,
         const __grid_constant__ CUtensorMap tm_snap, const __grid_constant__ CUtensorMap tm_grad,
         const SfStepArgs a, const int snap_slot, const int chunk)
 {
     using C = Cfg<R, BY, DAMP, MODE>;
-    constexpr int Q = C::Q, TZ = C::TZ, HZ = C::HZ, W = C::W, S = C::S;
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    __shared__ __align__(8) uint64_t full[S];
+    constexpr int Q = C::Q, TZ = C::TZ, HZ = C::HZ, W = C::W, S = C::S, PR = C::PRING;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // keep the address space visible to the compiler (LDS, not generic LD): align by
+    // offsetting the shared array itself
+    unsigned char *smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    float *pring = reinterpret_cast<float *>(smem + S * C::STAGE_BYTES);
+    __shared__ __align__(8) uint64_t full[S];   // TMA bytes landed in stage s
+    __shared__ __align__(8) uint64_t empty[S];  // every consumer warp finished reading stage s
 
-    const int lane = threadIdx.x, wy = threadIdx.y, tid = wy * 32 + lane;
+    const int lane = threadIdx.x, wy = threadIdx.y;
     const int z0 = blockIdx.x * TZ, y0 = blockIdx.y * BY;
     const int64_t qa = a.xa + (int64_t)blockIdx.z * chunk;
     const int64_t qb = min(qa + (int64_t)chunk, a.xb);
     if (qa >= qb) return;  // uniform over the CTA
     const int NP = (int)(qb - qa) + 2 * R;
 
-    if (tid == 0) {
-        prefetch_tmap(&tm_cur);
-        prefetch_tmap(&tm_old);
+    if (wy == 0 && lane == 0) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], BY);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
 
-    // producer: plane p = qa - R + i, output plane q = p - R
-    auto issue = [&](int i) {
-        const int st = i % S;
-        unsigned char *base = smem + st * C::STAGE_BYTES;
-        const int64_t p = qa - R + i;
-        const int64_t q = p - R;
-        const bool outp = (q >= qa);
-        uint32_t bytes = W * C::H * 4;  // full box, OOB part zero-filled
-        if (outp) bytes += C::NPL * C::PL_BYTES;
-        mbar_expect_tx(&full[st], bytes);
-        tma_load3(base, &tm_cur, z0 - HZ, y0 - R, (int)p, &full[st]);
-        if (outp) {
-            unsigned char *pl = base + C::CUR_BYTES;
-            tma_load3(pl, &tm_old, z0, y0, (int)q, &full[st]);
-            pl += C::PL_BYTES;
-            tma_load3(pl, &tm_c3, z0, y0, (int)q, &full[st]);
-            pl += C::PL_BYTES;
-            if (DAMP) {
-                tma_load3(pl, &tm_beta, z0, y0, (int)q, &full[st]);
-                pl += C::PL_BYTES;
-            }
-            if (MODE == SF_MODE_GRAD) {
-                tma_load4(pl, &tm_snap, z0, y0, (int)q, snap_slot, &full[st]);
-                pl += C::PL_BYTES;
-                tma_load3(pl, &tm_grad, z0, y0, (int)q, &full[st]);
+    if (wy == BY) {
+        // ------------------------------------------------ producer warp (TMA issue)
+        if (lane == 0) {
+            prefetch_tmap(&tm_cur);
+            prefetch_tmap(&tm_old);
+            prefetch_tmap(&tm_c3);
+            int st = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < NP; ++i) {
+                if (i >= S) mbar_wait(&empty[st], ph ^ 1u);
+                unsigned char *base = smem + st * C::STAGE_BYTES;
+                const int p = (int)(qa - R) + i;   // plane of u^n
+                const int q = p - R;               // output plane
+                const bool outp = (i >= 2 * R);
+                uint32_t bytes = W * C::H * 4;    // full box; out-of-bounds part zero-filled
+                if (outp) bytes += C::NPL * C::PL_BYTES;
+                mbar_expect_tx(&full[st], bytes);
+                tma_load3(base, &tm_cur, z0 - HZ, y0 - R, p, &full[st]);
+                if (outp) {
+                    unsigned char *pl = base + C::CUR_BYTES;
+                    tma_load3(pl, &tm_old, z0, y0, q, &full[st]);
+                    pl += C::PL_BYTES;
+                    tma_load3(pl, &tm_c3, z0, y0, q, &full[st]);
+                    pl += C::PL_BYTES;
+                    if (DAMP) {
+                        tma_load3(pl, &tm_beta, z0, y0, q, &full[st]);
+                        pl += C::PL_BYTES;
+                    }
+                    if (MODE == SF_MODE_GRAD) {
+                        tma_load4(pl, &tm_snap, z0, y0, q, snap_slot, &full[st]);
+                        pl += C::PL_BYTES;
+                        tma_load3(pl, &tm_grad, z0, y0, q, &full[st]);
+                    }
+                }
+                if (++st == S) {
+                    st = 0;
+                    ph ^= 1u;
+                }
             }
         }
-    };
-    if (tid == 0) {
-        for (int i = 0; i < S && i < NP; ++i) issue(i);
+        return;
     }
 
-    float V[Q][4];  // u at planes, slot = plane index mod Q (relative to qa - R)
-    float P[Q][4];  // in-plane partial Laplacian, same slots
+    // ---------------------------------------------------- consumer warps
+    float V[Q][4];  // u at planes, slot = iteration index mod Q
     const int rown = R + wy;
     const int zg = z0 + 4 * lane;
     const int yg = y0 + wy;
     const bool active = (zg < a.n2) && (yg < a.n1);
     const int64_t plane = a.n1 * a.n2;
     const int64_t rowoff = (int64_t)yg * a.n2 + zg;
+    const int po = wy * TZ + 4 * lane;   // this thread's float4 in a halo-free plane
+    float *myP = pring + po;            // private ring of in-plane partials (stride PL floats)
+    int st = 0, pw = 0;
+    uint32_t ph = 0;
+    // packed constants: weights {w_k, w_k}, -4, -2, -1, -gscale
+    f2_t Wk[R + 1];
+#pragma unroll
+    for (int k = 1; k <= R; ++k) Wk[k] = pk2(a.w.w[k], a.w.w[k]);
+    Wk[0] = 0ull;
+    const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f);
+    const f2_t NG = pk2(-a.gscale, -a.gscale);
 
     for (int base = 0; base < NP; base += Q) {
 #pragma unroll
         for (int s = 0; s < Q; ++s) {
             const int i = base + s;
             if (i < NP) {
-                const int st = i % S;
-                mbar_wait(&full[st], (uint32_t)((i / S) & 1));
+                mbar_wait(&full[st], ph);
                 const unsigned char *sb = smem + st * C::STAGE_BYTES;
                 const float *cs = reinterpret_cast<const float *>(sb);
                 // z row of this thread: columns [4 lane, 4 lane + 2 HZ + 4)
@@ -197,58 +233,92 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                 }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) V[s][j] = zr[HZ + j];
-                float pp[4] = {0.f, 0.f, 0.f, 0.f};
+                // in-plane partial P_p = sum_k w_k ((y-k + y+k) + (z-k + z+k) - 4u), as
+                // two fp32x2 lanes (points j, j+1)
+                f2_t pp2[2] = {0ull, 0ull};
 #pragma unroll
                 for (int k = 1; k <= R; ++k) {
-                    const float4 ym = *reinterpret_cast<const float4 *>(cs + (rown - k) * W + HZ + 4 * lane);
-                    const float4 yp = *reinterpret_cast<const float4 *>(cs + (rown + k) * W + HZ + 4 * lane);
-                    const float ymv[4] = {ym.x, ym.y, ym.z, ym.w};
-                    const float ypv[4] = {yp.x, yp.y, yp.z, yp.w};
+                    const float4 m4 = *reinterpret_cast<const float4 *>(cs + (rown - k) * W + HZ + 4 * lane);
+                    const float4 p4 = *reinterpret_cast<const float4 *>(cs + (rown + k) * W + HZ + 4 * lane);
+                    const f2_t ym2[2] = {pk2(m4.x, m4.y), pk2(m4.z, m4.w)};
+                    const f2_t yp2[2] = {pk2(p4.x, p4.y), pk2(p4.z, p4.w)};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        pp[j] = __fmaf_rn(a.w.w[k],
-                                          sf_inplane3(ymv[j], ypv[j], zr[HZ + j - k], zr[HZ + j + k],
-                                                      zr[HZ + j]),
-                                          pp[j]);
+                    for (int jp = 0; jp < 2; ++jp) {
+                        const int j = 2 * jp;
+                        const f2_t t = sf_inplane3_x2(ym2[jp], yp2[jp], pk2(zr[HZ + j - k], zr[HZ + j + 1 - k]),
+                                                      pk2(zr[HZ + j + k], zr[HZ + j + 1 + k]),
+                                                      pk2(zr[HZ + j], zr[HZ + j + 1]), M4);
+                        pp2[jp] = fma2(Wk[k], t, pp2[jp]);
+                    }
                 }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) P[s][j] = pp[j];
-
-                if (i >= 2 * R) {
-                    const int sq = (s - R + Q) % Q;  // compile-time after unrolling
-                    const int64_t q = qa + (i - 2 * R);
+                float pp[4];
+                upk2(pp2[0], pp[0], pp[1]);
+                upk2(pp2[1], pp[2], pp[3]);
+                const bool outp = (i >= 2 * R);
+                float ov[4], cv[4], bv[4] = {1.f, 1.f, 1.f, 1.f}, sv[4], gv[4], pq[4];
+                if (outp) {
                     const float *pl = reinterpret_cast<const float *>(sb + C::CUR_BYTES);
-                    const int po = wy * TZ + 4 * lane;
                     const float4 o4 = *reinterpret_cast<const float4 *>(pl + po);
                     const float4 c4 = *reinterpret_cast<const float4 *>(pl + TZ * BY + po);
-                    float4 b4 = make_float4(1.f, 1.f, 1.f, 1.f);
+                    ov[0] = o4.x; ov[1] = o4.y; ov[2] = o4.z; ov[3] = o4.w;
+                    cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
                     int nxt = 2;
                     if (DAMP) {
-                        b4 = *reinterpret_cast<const float4 *>(pl + 2 * TZ * BY + po);
+                        const float4 b4 = *reinterpret_cast<const float4 *>(pl + 2 * TZ * BY + po);
+                        bv[0] = b4.x; bv[1] = b4.y; bv[2] = b4.z; bv[3] = b4.w;
                         nxt = 3;
                     }
-                    const float ov[4] = {o4.x, o4.y, o4.z, o4.w};
-                    const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
-                    const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
-                    float res[4], gres[4];
-                    float sv[4] = {0.f, 0.f, 0.f, 0.f}, gv[4] = {0.f, 0.f, 0.f, 0.f};
                     if (MODE == SF_MODE_GRAD) {
                         const float4 s4 = *reinterpret_cast<const float4 *>(pl + nxt * TZ * BY + po);
                         const float4 g4 = *reinterpret_cast<const float4 *>(pl + (nxt + 1) * TZ * BY + po);
                         sv[0] = s4.x; sv[1] = s4.y; sv[2] = s4.z; sv[3] = s4.w;
                         gv[0] = g4.x; gv[1] = g4.y; gv[2] = g4.z; gv[3] = g4.w;
                     }
+                }
+                // this warp is done with the stage: release it to the producer
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+                if (++st == S) {
+                    st = 0;
+                    ph ^= 1u;
+                }
+                // P ring (thread-private slots): read P_{p-R} (slot pw+1), write P_p (slot pw)
+                int pr = pw + 1;
+                if (pr == PR) pr = 0;
+                if (outp) {
+                    const float4 t = *reinterpret_cast<const float4 *>(myP + pr * (TZ * BY));
+                    pq[0] = t.x; pq[1] = t.y; pq[2] = t.z; pq[3] = t.w;
+                }
+                *reinterpret_cast<float4 *>(myP + pw * (TZ * BY)) = make_float4(pp[0], pp[1], pp[2], pp[3]);
+                pw = pr;
+                // ---- finish output plane q = p - R from the register queue ----
+                if (outp) {
+                    const int sq = (s - R + Q) % Q;  // compile-time after unrolling
+                    const int64_t q = qa + (i - 2 * R);
+                    float res[4], gres[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float u = V[sq][j];
-                        float X = 0.f;
+                    for (int jp = 0; jp < 2; ++jp) {
+                        const int j = 2 * jp;
+                        const f2_t u = pk2(V[sq][j], V[sq][j + 1]);
+                        f2_t X = 0ull;
 #pragma unroll
-                        for (int k = 1; k <= R; ++k)
-                            X = __fmaf_rn(a.w.w[k], sf_xterm(V[(sq - k + Q) % Q][j], V[(sq + k) % Q][j], u), X);
-                        const float lap = __fadd_rn(P[sq][j], X);
-                        res[j] = sf_update(u, ov[j], bv[j], cv[j], lap);
-                        if (MODE == SF_MODE_GRAD)
-                            gres[j] = sf_grad(gv[j], a.gscale, sv[j], sf_d2(u, ov[j], bv[j], cv[j], lap));
+                        for (int k = 1; k <= R; ++k) {
+                            const int sm = (sq - k + Q) % Q, sp = (sq + k) % Q;
+                            X = fma2(Wk[k], sf_xterm_x2(pk2(V[sm][j], V[sm][j + 1]), pk2(V[sp][j], V[sp][j + 1]), u, M2),
+                                     X);
+                        }
+                        const f2_t lap = add2(pk2(pq[j], pq[j + 1]), X);
+                        // out = u + beta (u - old) + c3 lap   (== sf_update per lane)
+                        const f2_t d = fma2(M1, pk2(ov[j], ov[j + 1]), u);
+                        const f2_t b2 = pk2(bv[j], bv[j + 1]), c2 = pk2(cv[j], cv[j + 1]);
+                        const f2_t o = fma2(c2, lap, fma2(b2, d, u));
+                        upk2(o, res[j], res[j + 1]);
+                        if (MODE == SF_MODE_GRAD) {
+                            // S = (beta - 1) d + c3 lap ; g -= gscale * snap * S   (== sf_d2 / sf_grad)
+                            const f2_t S2 = fma2(add2(b2, M1), d, mul2(c2, lap));
+                            const f2_t g2 = fma2(NG, mul2(pk2(sv[j], sv[j + 1]), S2), pk2(gv[j], gv[j + 1]));
+                            upk2(g2, gres[j], gres[j + 1]);
+                        }
                     }
                     if (active) {
                         const int64_t off = q * plane + rowoff;
@@ -259,9 +329,32 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             stg4(a.grad + off, make_float4(gres[0], gres[1], gres[2], gres[3]));
                     }
                 }
-                __syncthreads();
-                if (tid == 0 && i + S < NP) issue(i + S);
             }
+        }
+    }
+
+    if (a.inj_beg) {
+        // fused injection of every source/receiver corner this CTA owns in
+        // [qa, qb): after all of this CTA's stores (named barrier over the consumer warps,
+        // CTA-scope ordering of global memory), out[t] += sum_e coef_e vals[pt_e] -- the
+        // fp32 operations of k_inject, bitwise -- plus the snapshot / gradient patches.
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * BY) : "memory");
+        const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+        const int ib = a.inj_beg[tile], iend = a.inj_beg[tile + 1];
+        for (int e = ib + wy * 32 + lane; e < iend; e += 32 * BY) {
+            const int q = a.inj_q[e];
+            if (q < qa || q >= qb) continue;
+            const int pos = a.inj_pos[e];
+            const int t = a.inj_t[e];
+            float d = 0.f;
+            for (int k = a.inj_rowptr[t]; k < a.inj_rowptr[t + 1]; ++k)
+                d = __fmaf_rn(a.inj_coef[k], a.inj_vals[a.inj_pt[k]], d);
+            const int64_t off = (int64_t)q * plane + (int64_t)(y0 + (pos >> 7)) * a.n2 + z0 + (pos & 127);
+            const float v = __fadd_rn(a.out[off], d);
+            a.out[off] = v;
+            if (MODE == SF_MODE_SAVE) a.snap_out[off] = v;
+            if (MODE == SF_MODE_GRAD)
+                a.grad[off] = __fmaf_rn(-a.gscale, __fmul_rn(a.snap_in[off], d), a.grad[off]);
         }
     }
 }
