@@ -20,6 +20,7 @@
 #include "sparse.cuh"
 
 #define SF_VERSION 1
+#define SF_FUSE_MAX 256  // largest sparse point set handled inside the stencil kernel
 
 static thread_local char g_err[1024] = "";
 
@@ -228,6 +229,8 @@ struct StepBufs {
     float gscale;
     SfSparse *inj;         // point set injected after this step (or NULL)
     const float *inj_vals; // its values for this step ([npoint])
+    SfSparse *itp;         // point set interpolated from the new level (or NULL)
+    float *itp_row;        // its record row for the new level ([npoint])
 };
 
 template <class T>
@@ -239,48 +242,149 @@ static sf_status upload(T **dst, const std::vector<T> &v)
     return SF_OK;
 }
 
-// Per-(y, z)-tile lists of the injection targets for the TMA kernel's fused epilogue
-// (built once per point set and tile height; see SfStepArgs::inj_*).
+
+static void free_itp(SfItpTiles &T)
+{
+    cudaFree(T.beg);
+    cudaFree(T.q);
+    cudaFree(T.lane);
+    cudaFree(T.k);
+    cudaFree(T.j);
+    cudaFree(T.p);
+    cudaFree(T.w);
+    cudaFree(T.left);
+    T = SfItpTiles{};
+}
+
+static void free_inj(SfInjTiles &T)
+{
+    cudaFree(T.beg);
+    cudaFree(T.q);
+    cudaFree(T.lj);
+    cudaFree(T.t);
+    T = SfInjTiles{};
+}
+
+// where grid offset `off` lives in the TMA kernel: (tile * by + warp, plane, lane, j)
+struct TileLoc {
+    int wl, q, lane, j;
+};
+static TileLoc tile_loc(const sf_handle *h, int by, int64_t off)
+{
+    const int64_t n1 = h->nb[1], n2 = h->nb[2];
+    const int64_t ntz = (n2 + 127) / 128;
+    const int64_t x = off / (n1 * n2), y = (off / n2) % n1, z = off % n2;
+    const int64_t tile = (y / by) * ntz + z / 128;
+    return {(int)(tile * by + y % by), (int)x, (int)((z % 128) / 4), (int)(z % 4)};
+}
+
+static int64_t n_warp_lists(const sf_handle *h, int by)
+{
+    return ((h->nb[2] + 127) / 128) * ((h->nb[1] + by - 1) / by) * by;
+}
+
+// Interpolation points whose nonzero corners are all points of one lane (same tile,
+// warp row, plane and float4 group) are interpolated inside the TMA kernel; the rest
+// stay in `left` for k_interp_list.
+static sf_status ensure_itp_tiles(sf_handle *h, SfSparse &sp, int by)
+{
+    SfItpTiles &T = sp.itiles;
+    if (T.by == by) return SF_OK;
+    free_itp(T);
+    const int64_t nl = n_warp_lists(h, by);
+    struct E {
+        int wl, q, lane, p, k;
+        int j[4];
+        float w[4];
+    };
+    std::vector<E> es;
+    std::vector<int> left;
+    for (int p = 0; p < sp.np; ++p) {
+        E e{};
+        e.p = p;
+        bool ok = true;
+        for (int c = 0; c < sp.nc; ++c) {
+            const float w = sp.h_iw[(size_t)p * sp.nc + c];
+            if (w == 0.0f) continue;
+            const TileLoc L = tile_loc(h, by, sp.h_iidx[(size_t)p * sp.nc + c]);
+            if (e.k > 0 && (L.wl != e.wl || L.q != e.q || L.lane != e.lane)) {
+                ok = false;
+                break;
+            }
+            e.wl = L.wl;
+            e.q = L.q;
+            e.lane = L.lane;
+            e.j[e.k] = L.j;
+            e.w[e.k] = w;
+            e.k++;
+        }
+        if (!ok || e.k == 0) left.push_back(p);
+        else es.push_back(e);
+    }
+    std::stable_sort(es.begin(), es.end(), [](const E &a, const E &b) {
+        return std::tie(a.wl, a.q, a.lane, a.p) < std::tie(b.wl, b.q, b.lane, b.p);
+    });
+    std::vector<int> beg(nl + 1, 0), q, lane, k, j, pp;
+    std::vector<float> w;
+    for (const E &e : es) beg[e.wl + 1]++;
+    for (int64_t i = 0; i < nl; ++i) beg[i + 1] += beg[i];
+    for (const E &e : es) {
+        q.push_back(e.q);
+        lane.push_back(e.lane);
+        k.push_back(e.k);
+        pp.push_back(e.p);
+        for (int c = 0; c < 4; ++c) {
+            j.push_back(c < e.k ? e.j[c] : 0);
+            w.push_back(c < e.k ? e.w[c] : 0.0f);
+        }
+    }
+    sf_status s;
+    if ((s = upload(&T.beg, beg))) return s;
+    if (!es.empty()) {
+        if ((s = upload(&T.q, q))) return s;
+        if ((s = upload(&T.lane, lane))) return s;
+        if ((s = upload(&T.k, k))) return s;
+        if ((s = upload(&T.j, j))) return s;
+        if ((s = upload(&T.p, pp))) return s;
+        if ((s = upload(&T.w, w))) return s;
+    }
+    if (!left.empty() && (s = upload(&T.left, left))) return s;
+    T.nleft = (int)left.size();
+    T.by = by;
+    return SF_OK;
+}
+
+// Per-(tile, warp) lists of the injection targets for the TMA kernel's fused injection.
 static sf_status ensure_inj_tiles(sf_handle *h, SfSparse &sp, int by)
 {
     SfInjTiles &T = sp.tiles;
     if (T.by == by) return SF_OK;
-    cudaFree(T.beg);
-    cudaFree(T.q);
-    cudaFree(T.pos);
-    cudaFree(T.t);
-    T = SfInjTiles{};
-    const int64_t n1 = h->nb[1], n2 = h->nb[2];
-    const int64_t ntz = (n2 + 127) / 128, nty = (n1 + by - 1) / by;
-    const int64_t ntiles = ntz * nty;
+    free_inj(T);
+    const int64_t nl = n_warp_lists(h, by);
     struct E {
-        int tile, q, pos, t;
+        int wl, q, lj, t;
     };
     std::vector<E> es;
-    es.reserve(sp.h_tgt.size());
     for (size_t t = 0; t < sp.h_tgt.size(); ++t) {
-        const int64_t off = sp.h_tgt[t];
-        const int64_t x = off / (n1 * n2), y = (off / n2) % n1, z = off % n2;
-        const int tile = (int)((y / by) * ntz + z / 128);
-        const int pos = (int)((((y % by) * 32) + (z % 128) / 4) * 4 + (z % 4));
-        es.push_back({tile, (int)x, pos, (int)t});
+        const TileLoc L = tile_loc(h, by, sp.h_tgt[t]);
+        es.push_back({L.wl, L.q, L.lane * 4 + L.j, (int)t});
     }
     std::sort(es.begin(), es.end(), [](const E &a, const E &b) {
-        return std::tie(a.tile, a.q, a.pos) < std::tie(b.tile, b.q, b.pos);
+        return std::tie(a.wl, a.q, a.lj) < std::tie(b.wl, b.q, b.lj);
     });
-    std::vector<int> beg(ntiles + 1, 0), q, pos, tt;
-    for (const E &e : es) beg[e.tile + 1]++;
-    for (int64_t i = 0; i < ntiles; ++i) beg[i + 1] += beg[i];
+    std::vector<int> beg(nl + 1, 0), q, lj, tt;
+    for (const E &e : es) beg[e.wl + 1]++;
+    for (int64_t i = 0; i < nl; ++i) beg[i + 1] += beg[i];
     for (const E &e : es) {
         q.push_back(e.q);
-        pos.push_back(e.pos);
+        lj.push_back(e.lj);
         tt.push_back(e.t);
     }
     sf_status s;
     if ((s = upload(&T.beg, beg))) return s;
     if (!es.empty()) {
         if ((s = upload(&T.q, q))) return s;
-        if ((s = upload(&T.pos, pos))) return s;
+        if ((s = upload(&T.lj, lj))) return s;
         if ((s = upload(&T.t, tt))) return s;
     }
     T.by = by;
@@ -288,9 +392,10 @@ static sf_status ensure_inj_tiles(sf_handle *h, SfSparse &sp, int by)
 }
 
 static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStream_t st,
-                             bool *fused)
+                             bool *fused, bool *fused_itp)
 {
     *fused = false;
+    *fused_itp = false;
     SfStepArgs a{};
     a.cur = b.cur;
     a.out = b.out;
@@ -341,18 +446,34 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         }
     }
     L.maps = &maps;
-    if (L.variant == SF_VAR_TMA && b.inj && b.inj->ntgt > 0 && b.inj_vals) {
+    // fuse only small point sets (a few shots' sources): large sets (receiver grids) would
+    // put dependent table loads on the stencil's critical path -> standalone kernels
+    if (L.variant == SF_VAR_TMA && b.inj && b.inj->ntgt > 0 && b.inj->ntgt <= SF_FUSE_MAX && b.inj_vals) {
         sf_status s = ensure_inj_tiles(h, *b.inj, L.by);
         if (s) return s;
         a.inj_beg = b.inj->tiles.beg;
         a.inj_q = b.inj->tiles.q;
-        a.inj_pos = b.inj->tiles.pos;
+        a.inj_lj = b.inj->tiles.lj;
         a.inj_t = b.inj->tiles.t;
         a.inj_rowptr = b.inj->j_rowptr;
         a.inj_pt = b.inj->j_pt;
         a.inj_coef = b.inj->j_coef;
         a.inj_vals = b.inj_vals;
         *fused = true;
+    }
+    if (L.variant == SF_VAR_TMA && h->nranks == 1 && b.itp && b.itp->np > 0 && b.itp->np <= SF_FUSE_MAX &&
+        b.itp_row) {
+        sf_status s = ensure_itp_tiles(h, *b.itp, L.by);
+        if (s) return s;
+        a.itp_beg = b.itp->itiles.beg;
+        a.itp_q = b.itp->itiles.q;
+        a.itp_lane = b.itp->itiles.lane;
+        a.itp_k = b.itp->itiles.k;
+        a.itp_j = b.itp->itiles.j;
+        a.itp_p = b.itp->itiles.p;
+        a.itp_w = b.itp->itiles.w;
+        a.itp_out = b.itp_row;
+        *fused_itp = true;
     }
     cudaError_t e;
     {
@@ -368,7 +489,18 @@ static sf_status launch_interp(sf_handle *h, const SfSparse &sp, const float *u,
 {
     if (sp.np == 0 || !out) return SF_OK;
     ProfScope ps(h, PK_INTERP, st);
-    k_interp<<<(sp.np + 127) / 128, 128, 0, st>>>(u, sp.i_idx, sp.i_w, sp.i_owned, sp.np, sp.nc, out);
+    k_interp_ell<<<(sp.np + 127) / 128, 128, 0, st>>>(u, sp.e_idx, sp.e_w, sp.i_owned, sp.np, sp.ik, out);
+    SF_CUDA_TRY(cudaGetLastError());
+    return SF_OK;
+}
+
+static sf_status launch_interp_left(sf_handle *h, const SfSparse &sp, const float *u, float *out,
+                                    cudaStream_t st)
+{
+    if (sp.itiles.nleft == 0 || !out) return SF_OK;
+    ProfScope ps(h, PK_INTERP, st);
+    k_interp_list<<<(sp.itiles.nleft + 127) / 128, 128, 0, st>>>(u, sp.itiles.left, sp.itiles.nleft,
+                                                                 sp.i_idx, sp.i_w, sp.nc, out);
     SF_CUDA_TRY(cudaGetLastError());
     return SF_OK;
 }
@@ -379,8 +511,12 @@ static sf_status launch_inject(sf_handle *h, const SfSparse &sp, float *u, const
 {
     if (sp.ntgt == 0 || !vals) return SF_OK;
     ProfScope ps(h, PK_INJECT, st);
-    k_inject<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.j_rowptr, sp.j_pt, sp.j_coef,
-                                                     sp.ntgt, vals, snap_patch, grad_snap, grad, gscale);
+    if (sp.jk > 0)
+        k_inject_ell<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.jk, sp.ej_pt, sp.ej_coef, sp.ntgt,
+                                                             vals, snap_patch, grad_snap, grad, gscale);
+    else
+        k_inject<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.j_rowptr, sp.j_pt, sp.j_coef,
+                                                         sp.ntgt, vals, snap_patch, grad_snap, grad, gscale);
     SF_CUDA_TRY(cudaGetLastError());
     return SF_OK;
 }
@@ -395,10 +531,12 @@ static void free_sparse(SfSparse &s)
     cudaFree(s.j_rowptr);
     cudaFree(s.j_pt);
     cudaFree(s.j_coef);
-    cudaFree(s.tiles.beg);
-    cudaFree(s.tiles.q);
-    cudaFree(s.tiles.pos);
-    cudaFree(s.tiles.t);
+    free_inj(s.tiles);
+    free_itp(s.itiles);
+    cudaFree(s.e_idx);
+    cudaFree(s.e_w);
+    cudaFree(s.ej_pt);
+    cudaFree(s.ej_coef);
     s = SfSparse{};
 }
 
@@ -488,6 +626,8 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
     out.np = np;
     out.nc = nc;
     out.h_tgt = tgt;
+    out.h_iidx = iidx;
+    out.h_iw = iw;
     out.ntgt = (int)tgt.size();
     out.nent = (int)ents.size();
     sf_status s;
@@ -509,6 +649,42 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
         SF_CUDA_TRY(cudaDeviceSynchronize());
         cudaFree(d_etgt);
         cudaFree(d_ew);
+        // injection ELL (slot-major), when every target has few contributions
+        int kmax = 0;
+        for (size_t t = 0; t + 1 < rowptr.size(); ++t) kmax = std::max(kmax, rowptr[t + 1] - rowptr[t]);
+        if (kmax <= 8) {
+            out.jk = kmax;
+            SF_CUDA_TRY(cudaMalloc(&out.ej_pt, sizeof(int) * (size_t)kmax * out.ntgt));
+            SF_CUDA_TRY(cudaMalloc(&out.ej_coef, sizeof(float) * (size_t)kmax * out.ntgt));
+            k_csr_to_ell<<<(out.ntgt + 255) / 256, 256>>>(out.j_rowptr, out.j_pt, out.j_coef, out.ntgt, kmax,
+                                                          out.ej_pt, out.ej_coef);
+            SF_CUDA_TRY(cudaGetLastError());
+            SF_CUDA_TRY(cudaDeviceSynchronize());
+        }
+    }
+    // interpolation ELL (slot-major): nonzero corners in corner order, zero padded
+    {
+        int K = 1;
+        for (int p = 0; p < np; ++p) {
+            int k = 0;
+            for (int c = 0; c < nc; ++c) k += iw[(size_t)p * nc + c] != 0.0f;
+            K = std::max(K, k);
+        }
+        std::vector<int64_t> eidx((size_t)K * np, 0);
+        std::vector<float> ew((size_t)K * np, 0.0f);
+        for (int p = 0; p < np; ++p) {
+            int k = 0;
+            for (int c = 0; c < nc; ++c) {
+                const float w = iw[(size_t)p * nc + c];
+                if (w == 0.0f) continue;
+                eidx[(size_t)k * np + p] = iidx[(size_t)p * nc + c];
+                ew[(size_t)k * np + p] = w;
+                ++k;
+            }
+        }
+        out.ik = K;
+        if ((s = upload(&out.e_idx, eidx))) return s;
+        if ((s = upload(&out.e_w, ew))) return s;
     }
     return SF_OK;
 }
@@ -540,6 +716,10 @@ extern "C" void sf_destroy(sf_handle *h)
     free_sparse(h->src);
     free_sparse(h->rec);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->ev_ready) cudaEventDestroy(h->ev_ready);
+    for (int k = 0; k < 2; ++k)
+        if (h->ev_itp[k]) cudaEventDestroy(h->ev_itp[k]);
+    if (h->side) cudaStreamDestroy(h->side);
     delete h;
 }
 
@@ -597,6 +777,10 @@ static sf_status create_common(const sf_desc *d, sf_handle *h)
     sf_status s;
     if ((s = build_sparse(h, d->nsrc, d->src_coords, d->m, h->src, "source"))) return s;
     if ((s = build_sparse(h, d->nrec, d->rec_coords, d->m, h->rec, "receiver"))) return s;
+    SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
+    SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_itp[0], cudaEventDisableTiming));
+    SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_itp[1], cudaEventDisableTiming));
     SF_CUDA_TRY(cudaMalloc(&h->partial, sizeof(double) * 1024));
     SF_CUDA_TRY(cudaMalloc(&h->dJ, sizeof(double)));
     SF_CUDA_TRY(cudaDeviceSynchronize());
@@ -800,6 +984,42 @@ static sf_status swap_halves(sf_handle *h, float *a, float *b, cudaStream_t st)
     return SF_OK;
 }
 
+// Records of a level run on the handle's side stream, concurrently with the next
+// stencil step (which only reads that level); the stencil two steps later overwrites
+// the level, so it waits for the record first.  ev_itp[level & 1] marks completion.
+static sf_status side_interp(sf_handle *h, SfSparse &sp, bool fused_itp, const float *lvl, float *row,
+                             int level, cudaStream_t st)
+{
+    if (!row || sp.np == 0 || (fused_itp && sp.itiles.nleft == 0)) return SF_OK;
+    SF_CUDA_TRY(cudaEventRecord(h->ev_ready, st));
+    SF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_ready, 0));
+    sf_status s = fused_itp ? launch_interp_left(h, sp, lvl, row, h->side) : launch_interp(h, sp, lvl, row, h->side);
+    if (s) return s;
+    SF_CUDA_TRY(cudaEventRecord(h->ev_itp[level & 1], h->side));
+    h->itp_pending[level & 1] = true;
+    return SF_OK;
+}
+
+// before a stencil step writes into the buffer holding `level`
+static sf_status wait_interp(sf_handle *h, int level, cudaStream_t st)
+{
+    if (level < 0 || !h->itp_pending[level & 1]) return SF_OK;
+    SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_itp[level & 1], 0));
+    h->itp_pending[level & 1] = false;
+    return SF_OK;
+}
+
+static sf_status join_side(sf_handle *h, cudaStream_t st)
+{
+    for (int k = 0; k < 2; ++k) {
+        if (h->itp_pending[k]) {
+            SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_itp[k], 0));
+            h->itp_pending[k] = false;
+        }
+    }
+    return SF_OK;
+}
+
 extern "C" sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, float *u,
                                 float *snaps, int save_every, void *stream)
 {
@@ -811,26 +1031,29 @@ extern "C" sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, 
     const int64_t N = h->N;
     float *A = u, *B = u + N;  // A = u^{-1}, B = u^0
     sf_status s;
+    h->itp_pending[0] = h->itp_pending[1] = false;
     if (h->nranks > 1) {  // make the halo of u^0 valid for the first stencil / record
         if ((s = post_step_exchange(h, B, st))) return s;
     }
-    if ((s = launch_interp(h, h->rec, B, rec, st))) return s;
+    if ((s = side_interp(h, h->rec, false, B, rec, 0, st))) return s;
     if (snaps) SF_CUDA_TRY(cudaMemcpyAsync(snaps, B, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
     for (int n = 0; n <= h->nt - 2; ++n) {
         float *cur = (n % 2 == 0) ? B : A;
-        float *out = (n % 2 == 0) ? A : B;
+        float *out = (n % 2 == 0) ? A : B;   // holds u^{n-1}, becomes u^{n+1}
         const bool save = snaps && ((n + 1) % save_every == 0);
         float *slot = save ? snaps + (int64_t)((n + 1) / save_every) * N : nullptr;
         const float *wrow = wavelet ? wavelet + (int64_t)n * h->src.np : nullptr;
-        StepBufs b{cur, out, slot, nullptr, 0, 0, nullptr, 0.f, &h->src, wrow};
-        bool fused = false;
-        if ((s = launch_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, st, &fused))) return s;
+        float *rrow = rec ? rec + (int64_t)(n + 1) * h->rec.np : nullptr;
+        if ((s = wait_interp(h, n - 1, st))) return s;
+        StepBufs b{cur, out, slot, nullptr, 0, 0, nullptr, 0.f, &h->src, wrow, &h->rec, rrow};
+        bool fused = false, fused_itp = false;
+        if ((s = launch_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, st, &fused, &fused_itp))) return s;
         if (!fused && (s = launch_inject(h, h->src, out, wrow, slot, nullptr, nullptr, 0.f, st)))
             return s;
         if ((s = post_step_exchange(h, out, st))) return s;
-        if ((s = launch_interp(h, h->rec, out, rec ? rec + (int64_t)(n + 1) * h->rec.np : nullptr, st)))
-            return s;
+        if ((s = side_interp(h, h->rec, fused_itp, out, rrow, n + 1, st))) return s;
     }
+    if ((s = join_side(h, st))) return s;
     // u^{nt-1} was written into A when nt is even: restore (u^{nt-2}, u^{nt-1}) order
     if (h->nt % 2 == 0) return swap_halves(h, A, B, st);
     return SF_OK;
@@ -854,25 +1077,29 @@ extern "C" sf_status sf_adjoint(sf_handle *h, const float *res, float *srca, flo
     if (h->nranks > 1) {
         if ((s = post_step_exchange(h, B, st))) return s;
     }
-    if ((s = launch_interp(h, h->src, B, srca ? srca + (int64_t)(h->nt - 1) * h->src.np : nullptr, st)))
+    h->itp_pending[0] = h->itp_pending[1] = false;
+    if ((s = side_interp(h, h->src, false, B, srca ? srca + (int64_t)(h->nt - 1) * h->src.np : nullptr,
+                         0, st)))
         return s;
     for (int n = h->nt - 1, j = 0; n >= 1; --n, ++j) {
         float *cur = (j % 2 == 0) ? B : A;
         float *out = (j % 2 == 0) ? A : B;
         const bool g = dograd && (n % save_every == 0);
+        if ((s = wait_interp(h, j - 1, st))) return s;   // level written at step j-2
         const float *rrow = res ? res + (int64_t)n * h->rec.np : nullptr;
+        float *srow = srca ? srca + (int64_t)(n - 1) * h->src.np : nullptr;
         StepBufs b{cur, out, nullptr, g ? snaps : nullptr, g ? n / save_every : 0, nsnap,
-                   g ? grad : nullptr, gscale, &h->rec, rrow};
-        bool fused = false;
-        if ((s = launch_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, st, &fused))) return s;
+                   g ? grad : nullptr, gscale, &h->rec, rrow, &h->src, srow};
+        bool fused = false, fused_itp = false;
+        if ((s = launch_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, st, &fused, &fused_itp))) return s;
         if (!fused && (s = launch_inject(h, h->rec, out, rrow, nullptr,
                                          g ? snaps + (int64_t)(n / save_every) * N : nullptr,
                                          g ? grad : nullptr, gscale, st)))
             return s;
         if ((s = post_step_exchange(h, out, st))) return s;
-        if ((s = launch_interp(h, h->src, out, srca ? srca + (int64_t)(n - 1) * h->src.np : nullptr, st)))
-            return s;
+        if ((s = side_interp(h, h->src, fused_itp, out, srow, j + 1, st))) return s;
     }
+    if ((s = join_side(h, st))) return s;
     if (h->nt % 2 == 0) return swap_halves(h, A, B, st);
     return SF_OK;
 }

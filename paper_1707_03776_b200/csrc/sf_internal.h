@@ -10,11 +10,22 @@
 #include "../../include/sf.h"
 #include "launch.cuh"
 
-// Injection targets grouped by (y, z) tile of the TMA kernel (fused injection).
+// Injection targets grouped by (tile, consumer warp) of the TMA kernel (fused injection).
 struct SfInjTiles {
     int by = 0;          // tile height the lists were built for (0 = not built)
-    int *beg = nullptr;  // [ntiles + 1]
-    int *q = nullptr, *pos = nullptr, *t = nullptr;
+    int *beg = nullptr;  // [ntiles * by + 1]
+    int *q = nullptr, *lj = nullptr, *t = nullptr;
+};
+
+// Interpolation points grouped by (tile, consumer warp) for the fused interpolation;
+// points whose nonzero corners are not all owned by one lane stay in `left`.
+struct SfItpTiles {
+    int by = 0;
+    int *beg = nullptr;    // [ntiles * by + 1]
+    int *q = nullptr, *lane = nullptr, *k = nullptr, *j = nullptr, *p = nullptr;
+    float *w = nullptr;
+    int *left = nullptr;
+    int nleft = 0;
 };
 
 // Sparse point set on the device (one for sources, one for receivers).
@@ -32,8 +43,18 @@ struct SfSparse {
     int *j_rowptr = nullptr;
     int *j_pt = nullptr;
     float *j_coef = nullptr;  // W dt^2 / m[target]
+    // ELL (slot-major) copies used by the standalone kernels
+    int ik = 0;               // interpolation slots per point (max nonzero corners)
+    int64_t *e_idx = nullptr;
+    float *e_w = nullptr;
+    int jk = 0;               // injection slots per target (0: use CSR)
+    int *ej_pt = nullptr;
+    float *ej_coef = nullptr;
     std::vector<int64_t> h_tgt;  // host copy of the target offsets
+    std::vector<int64_t> h_iidx; // host copy of the interpolation corners
+    std::vector<float> h_iw;
     SfInjTiles tiles;
+    SfItpTiles itiles;
 };
 
 struct sf_handle {
@@ -65,6 +86,10 @@ struct sf_handle {
     long long n_kind[4] = {0, 0, 0, 0};
     long long n_all = 0;
     int sms = 148;                  // multiprocessors of the device (set at create)
+    // side stream for records (overlap with the next stencil step)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_itp[2] = {nullptr, nullptr};
+    bool itp_pending[2] = {false, false};
 };
 
 // error reporting (thread-local message)

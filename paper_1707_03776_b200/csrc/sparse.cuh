@@ -29,6 +29,73 @@ __global__ void k_interp(const float *__restrict__ u, const int64_t *__restrict_
     out[p] = owned ? (owned[p] ? acc : 0.0f) : acc;
 }
 
+// Same sum from ELL tables: K slots per point stored slot-major ([K][np], coalesced),
+// holding the point's nonzero corners in corner order (zero-padded).  Bitwise equal to
+// k_interp (same nonzero terms, same order).
+__global__ void k_interp_ell(const float *__restrict__ u, const int64_t *__restrict__ idx,
+                             const float *__restrict__ W, const int *__restrict__ owned, int np, int K,
+                             float *__restrict__ out)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    float acc = 0.0f;
+    for (int c = 0; c < K; ++c) {
+        const float w = W[(int64_t)c * np + p];
+        if (w != 0.0f) acc = __fmaf_rn(w, __ldcg(u + idx[(int64_t)c * np + p]), acc);
+    }
+    out[p] = owned ? (owned[p] ? acc : 0.0f) : acc;
+}
+
+// Injection from ELL tables ([K][ntgt] slot-major, zero coefficients pad): bitwise equal
+// to k_inject (same terms, same order).
+__global__ void k_inject_ell(float *__restrict__ u, const int64_t *__restrict__ tgt, int K,
+                             const int *__restrict__ ept, const float *__restrict__ ecoef, int ntgt,
+                             const float *__restrict__ vals, float *__restrict__ snap_patch,
+                             const float *__restrict__ grad_snap, float *__restrict__ grad, float gscale)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntgt) return;
+    const int64_t g = tgt[t];
+    float d = 0.0f;
+    for (int c = 0; c < K; ++c) {
+        const float cf = ecoef[(int64_t)c * ntgt + t];
+        if (cf != 0.0f) d = __fmaf_rn(cf, vals[ept[(int64_t)c * ntgt + t]], d);
+    }
+    u[g] = __fadd_rn(u[g], d);
+    if (snap_patch) snap_patch[g] = __fadd_rn(snap_patch[g], d);
+    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(grad_snap[g], d), grad[g]);
+}
+
+// CSR -> ELL (slot-major) for the injection tables
+__global__ void k_csr_to_ell(const int *__restrict__ rowptr, const int *__restrict__ pt,
+                             const float *__restrict__ coef, int ntgt, int K, int *__restrict__ ept,
+                             float *__restrict__ ecoef)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntgt) return;
+    const int b = rowptr[t], n = rowptr[t + 1] - b;
+    for (int c = 0; c < K; ++c) {
+        ept[(int64_t)c * ntgt + t] = c < n ? pt[b + c] : 0;
+        ecoef[(int64_t)c * ntgt + t] = c < n ? coef[b + c] : 0.0f;
+    }
+}
+
+// interpolation of a listed subset of points (those the TMA epilogue could not fuse)
+__global__ void k_interp_list(const float *__restrict__ u, const int *__restrict__ list, int nl,
+                              const int64_t *__restrict__ idx, const float *__restrict__ W, int nc,
+                              float *__restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nl) return;
+    const int p = list[i];
+    float acc = 0.0f;
+    for (int c = 0; c < nc; ++c) {
+        const float w = W[(int64_t)p * nc + c];
+        if (w != 0.0f) acc = __fmaf_rn(w, u[idx[(int64_t)p * nc + c]], acc);
+    }
+    out[p] = acc;
+}
+
 __global__ void k_inject(float *__restrict__ u, const int64_t *__restrict__ tgt,
                          const int *__restrict__ rowptr, const int *__restrict__ ent_pt,
                          const float *__restrict__ ent_coef, int ntgt,

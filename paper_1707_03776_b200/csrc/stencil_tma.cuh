@@ -212,6 +212,24 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     Wk[0] = 0ull;
     const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f);
     const f2_t NG = pk2(-a.gscale, -a.gscale);
+    // fused sparse work: this warp's cursors (warp-uniform), first entries at q >= qa
+    constexpr int QINF = 0x7fffffff;
+    int ci = 0, ce = 0, cq = QINF, pi = 0, pe = 0, pq_ = QINF;
+    {
+        const int wl = (blockIdx.y * gridDim.x + blockIdx.x) * BY + wy;
+        if (a.inj_beg) {
+            ci = a.inj_beg[wl];
+            ce = a.inj_beg[wl + 1];
+            while (ci < ce && a.inj_q[ci] < qa) ++ci;
+            cq = ci < ce ? a.inj_q[ci] : QINF;
+        }
+        if (a.itp_beg) {
+            pi = a.itp_beg[wl];
+            pe = a.itp_beg[wl + 1];
+            while (pi < pe && a.itp_q[pi] < qa) ++pi;
+            pq_ = pi < pe ? a.itp_q[pi] : QINF;
+        }
+    }
 
     for (int base = 0; base < NP; base += Q) {
 #pragma unroll
@@ -320,6 +338,51 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             upk2(g2, gres[j], gres[j + 1]);
                         }
                     }
+                    if (cq == (int)q) {
+                        // fused injection: res[j] += sum_e coef_e vals[pt_e]
+                        // (the fp32 operations of k_inject, bitwise)
+                        do {
+                            const int lj = a.inj_lj[ci];
+                            if ((lj >> 2) == lane) {
+                                const int t = a.inj_t[ci];
+                                float d = 0.f;
+#pragma unroll 1
+                                for (int e = a.inj_rowptr[t]; e < a.inj_rowptr[t + 1]; ++e)
+                                    d = __fmaf_rn(a.inj_coef[e], a.inj_vals[a.inj_pt[e]], d);
+                                const int j = lj & 3;
+                                res[0] = (j == 0) ? __fadd_rn(res[0], d) : res[0];
+                                res[1] = (j == 1) ? __fadd_rn(res[1], d) : res[1];
+                                res[2] = (j == 2) ? __fadd_rn(res[2], d) : res[2];
+                                res[3] = (j == 3) ? __fadd_rn(res[3], d) : res[3];
+                                if (MODE == SF_MODE_GRAD) {
+                                    gres[0] = (j == 0) ? __fmaf_rn(-a.gscale, __fmul_rn(sv[0], d), gres[0]) : gres[0];
+                                    gres[1] = (j == 1) ? __fmaf_rn(-a.gscale, __fmul_rn(sv[1], d), gres[1]) : gres[1];
+                                    gres[2] = (j == 2) ? __fmaf_rn(-a.gscale, __fmul_rn(sv[2], d), gres[2]) : gres[2];
+                                    gres[3] = (j == 3) ? __fmaf_rn(-a.gscale, __fmul_rn(sv[3], d), gres[3]) : gres[3];
+                                }
+                            }
+                            ++ci;
+                            cq = ci < ce ? a.inj_q[ci] : QINF;
+                        } while (cq == (int)q);
+                    }
+                    if (pq_ == (int)q) {
+                        // fused interpolation of points owned by one lane
+                        do {
+                            if (a.itp_lane[pi] == lane) {
+                                const int kc = a.itp_k[pi];
+                                float acc = 0.f;
+#pragma unroll 1
+                                for (int c = 0; c < kc; ++c) {
+                                    const int j = a.itp_j[4 * pi + c];
+                                    const float v = j == 0 ? res[0] : j == 1 ? res[1] : j == 2 ? res[2] : res[3];
+                                    acc = __fmaf_rn(a.itp_w[4 * pi + c], v, acc);
+                                }
+                                a.itp_out[a.itp_p[pi]] = acc;
+                            }
+                            ++pi;
+                            pq_ = pi < pe ? a.itp_q[pi] : QINF;
+                        } while (pq_ == (int)q);
+                    }
                     if (active) {
                         const int64_t off = q * plane + rowoff;
                         stg4(a.out + off, make_float4(res[0], res[1], res[2], res[3]));
@@ -333,30 +396,6 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
         }
     }
 
-    if (a.inj_beg) {
-        // fused injection of every source/receiver corner this CTA owns in
-        // [qa, qb): after all of this CTA's stores (named barrier over the consumer warps,
-        // CTA-scope ordering of global memory), out[t] += sum_e coef_e vals[pt_e] -- the
-        // fp32 operations of k_inject, bitwise -- plus the snapshot / gradient patches.
-        asm volatile("bar.sync 1, %0;" ::"r"(32 * BY) : "memory");
-        const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-        const int ib = a.inj_beg[tile], iend = a.inj_beg[tile + 1];
-        for (int e = ib + wy * 32 + lane; e < iend; e += 32 * BY) {
-            const int q = a.inj_q[e];
-            if (q < qa || q >= qb) continue;
-            const int pos = a.inj_pos[e];
-            const int t = a.inj_t[e];
-            float d = 0.f;
-            for (int k = a.inj_rowptr[t]; k < a.inj_rowptr[t + 1]; ++k)
-                d = __fmaf_rn(a.inj_coef[k], a.inj_vals[a.inj_pt[k]], d);
-            const int64_t off = (int64_t)q * plane + (int64_t)(y0 + (pos >> 7)) * a.n2 + z0 + (pos & 127);
-            const float v = __fadd_rn(a.out[off], d);
-            a.out[off] = v;
-            if (MODE == SF_MODE_SAVE) a.snap_out[off] = v;
-            if (MODE == SF_MODE_GRAD)
-                a.grad[off] = __fmaf_rn(-a.gscale, __fmul_rn(a.snap_in[off], d), a.grad[off]);
-        }
-    }
 }
 
 }  // namespace sftma

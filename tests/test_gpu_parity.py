@@ -309,8 +309,8 @@ def test_profiling_counts():
     prop.set_profiling(True)
     prop.forward(dev(p.wavelet))
     prof = prop.profile()
-    assert prof["stencil_launches"] == p.nt - 1 and prof["stencil_ms"] > 0 and prof["interp_launches"] == p.nt
-    assert prof["launches"] >= 3 * (p.nt - 1)
+    assert prof["stencil_launches"] == p.nt - 1 and prof["stencil_ms"] > 0 and prof["interp_launches"] >= 1
+    assert prof["launches"] >= p.nt - 1
 
 
 @pytest.mark.parametrize("k", [1, 4])
@@ -346,3 +346,25 @@ def test_config2_full_grid_short_gradient():
     torch.cuda.synchronize()
     assert rel(g.cpu().numpy(), go["grad"]) <= TOL, rel(g.cpu().numpy(), go["grad"])
     assert abs(J - go["J"]) <= 1e-4 * go["J"]
+
+
+def test_fused_sparse_epilogue_mixed_receivers():
+    """TMA kernel's fused injection + interpolation epilogue: on-node surface receivers
+    (fused), receivers straddling planes/tiles (left to k_interp_list) and sources on
+    tile boundaries -- vs the oracle and bitwise vs the generic (unfused) variant."""
+    p = synth.make_config(1, scale=0.25, nt=90)
+    rng = np.random.default_rng(5)
+    n = np.array(p.shape)
+    extra = rng.uniform(0.5, 1.0, (40, 3)) * (n - 1) * p.h * 0.9
+    extra[:5, 1] = 15.5 * p.h          # y straddles the BY=16 tile boundary
+    extra[5:10, 2] = 127.5 * p.h if n[2] > 128 else extra[5:10, 2]
+    # <= 256 points so the TMA kernel interpolates them in-kernel (SF_FUSE_MAX)
+    p.rec_coords = np.concatenate([p.rec_coords[::71][:100], extra.astype(np.float32)])
+    p.src_coords = np.array([[40.0 * p.h, 16.0 * p.h, 40.3 * p.h], [20.5 * p.h, 31.5 * p.h, 60.0 * p.h]],
+                            dtype=np.float32)
+    p.wavelet = np.stack([p.wavelet[:, 0], 0.5 * p.wavelet[:, 0]], axis=1)
+    ro, uo, _ = oracle_forward(p)
+    rg, ug, _ = gpu_forward(p, variant=2)
+    assert rel(rg, ro) <= TOL and rel(ug[1], uo[1]) <= TOL
+    rg1, ug1, _ = gpu_forward(p, variant=1)
+    assert np.array_equal(rg, rg1) and np.array_equal(ug, ug1)
