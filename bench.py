@@ -50,8 +50,8 @@ def peaks():
 
 def ncu_traffic():
     """Per-launch DRAM bytes of the stencil kernel from the committed ncu --set full
-    capture summary (profiles/stencil_ncu_summary.json), or None."""
-    path = os.path.join(ROOT, "profiles", "stencil_ncu_summary.json")
+    capture summary (profiles/r01_stencil_ncu_full.json, scripts/ncu_summary.py), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_stencil_ncu_full.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -231,7 +231,10 @@ def run_ours(args):
                              "4 fields streamed per update)",
                        "kernel_tuning": tuning},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "frac": round(achieved / peak, 4),
+                         "traffic": None if traffic is None else int(traffic),
+                         "traffic_source": "profiles/r01_stencil_ncu_full.json (ncu --set full, dram "
+                                           "read+write per launch, random-init wavefield)",
                          "peak_source": peak_src,
                          "kernel": "k_tma3d (stencil step, fwd)" if tuning["variant"] == 2 else "k_generic3d",
                          "algorithmic_bytes_per_launch": alg_bytes,

@@ -1,0 +1,11 @@
+# ncu evidence for profiles/: launch list of the bench command + one full capture of the
+# stencil kernel on an incompressible (random) wavefield.  Run under gpurun.
+set -x
+mkdir -p gpurun_out
+CMD="python bench.py --steps 1 --warmup 3 --nt 40 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/plain_bench.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -s 150 -c 150 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+CMD2="python scripts/tune.py --nt 12 --random-init --by 16 --chunks 0"
+$CMD2 > gpurun_out/plain_tune.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_tma3d -s 14 -c 1 -o gpurun_out/prof_stencil $CMD2 > gpurun_out/ncu_full.log 2>&1
+tail -3 gpurun_out/ncu_full.log
