@@ -161,6 +161,13 @@ SF_API sf_status sf_slab_plan(int64_t n0, int space_order, int rank, int nranks,
 SF_API sf_status sf_sparse_owner(int64_t n0, int space_order, int nranks, double h, double coord0,
                           int *owner);
 
+/* Host-only: the halo exchange sf_forward / sf_adjoint perform after every step on a
+ * rank's local buffer [n0_loc + 2r][...] (planes, counted along axis 0):
+ *   plan[0] = first plane sent to rank-1        plan[1] = first plane received from rank-1
+ *   plan[2] = first plane sent to rank+1        plan[3] = first plane received from rank+1
+ *   plan[4] = planes per message (r); plan[5] = has left neighbour; plan[6] = has right. */
+SF_API sf_status sf_slab_halo_plan(int64_t n0, int space_order, int rank, int nranks, int64_t plan[7]);
+
 /* NCCL bootstrap: rank 0 calls sf_nccl_unique_id, broadcasts the 128 bytes (e.g. over
  * torch.distributed), every rank calls sf_nccl_comm_init.  The comm is caller-owned. */
 SF_API sf_status sf_nccl_unique_id(char id_out[128]);

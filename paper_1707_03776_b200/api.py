@@ -17,7 +17,7 @@ import torch
 
 from ._lib import SfDesc, SfError, check, lib
 
-__all__ = ["Propagator", "fd_weights", "forward_host", "slab_plan", "sparse_owner", "SfError",
+__all__ = ["Propagator", "fd_weights", "forward_host", "slab_plan", "slab_halo_plan", "sparse_owner", "SfError",
            "nccl_unique_id", "nccl_comm_init", "nccl_comm_destroy", "allreduce_gradient"]
 
 
@@ -48,6 +48,14 @@ def slab_plan(n0: int, space_order: int, rank: int, nranks: int):
     x0, nl = ctypes.c_int64(), ctypes.c_int64()
     check(lib().sf_slab_plan(n0, space_order, rank, nranks, ctypes.byref(x0), ctypes.byref(nl)))
     return x0.value, nl.value
+
+
+def slab_halo_plan(n0: int, space_order: int, rank: int, nranks: int) -> dict:
+    """The per-step halo exchange of a slab rank (sf_slab_halo_plan), in local planes."""
+    plan = (ctypes.c_int64 * 7)()
+    check(lib().sf_slab_halo_plan(n0, space_order, rank, nranks, plan))
+    return {"send_left": plan[0], "recv_left": plan[1], "send_right": plan[2], "recv_right": plan[3],
+            "planes": plan[4], "has_left": bool(plan[5]), "has_right": bool(plan[6])}
 
 
 def sparse_owner(n0: int, space_order: int, nranks: int, h: float, coord0: float) -> int:

@@ -115,19 +115,19 @@ sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st)
 {
     sf_status s = need_nccl();
     if (s) return s;
-    const int r = h->r;
+    int64_t plan[7];
+    if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank, h->nranks, plan))) return s;
     const int64_t plane = h->N / h->nb[0];
-    const size_t cnt = (size_t)r * (size_t)plane;
-    const int64_t nl = h->n0_loc;
+    const size_t cnt = (size_t)plan[4] * (size_t)plane;
     ncclComm_t c = static_cast<ncclComm_t>(h->comm);
     SF_NCCL_TRY(api().GroupStart());
-    if (h->rank > 0) {
-        SF_NCCL_TRY(api().Send(buf + (int64_t)r * plane, cnt, ncclFloat, h->rank - 1, c, st));
-        SF_NCCL_TRY(api().Recv(buf, cnt, ncclFloat, h->rank - 1, c, st));
+    if (plan[5]) {
+        SF_NCCL_TRY(api().Send(buf + plan[0] * plane, cnt, ncclFloat, h->rank - 1, c, st));
+        SF_NCCL_TRY(api().Recv(buf + plan[1] * plane, cnt, ncclFloat, h->rank - 1, c, st));
     }
-    if (h->rank < h->nranks - 1) {
-        SF_NCCL_TRY(api().Send(buf + nl * plane, cnt, ncclFloat, h->rank + 1, c, st));
-        SF_NCCL_TRY(api().Recv(buf + (nl + r) * plane, cnt, ncclFloat, h->rank + 1, c, st));
+    if (plan[6]) {
+        SF_NCCL_TRY(api().Send(buf + plan[2] * plane, cnt, ncclFloat, h->rank + 1, c, st));
+        SF_NCCL_TRY(api().Recv(buf + plan[3] * plane, cnt, ncclFloat, h->rank + 1, c, st));
     }
     SF_NCCL_TRY(api().GroupEnd());
     h->n_all++;

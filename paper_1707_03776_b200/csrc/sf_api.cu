@@ -832,6 +832,23 @@ extern "C" sf_status sf_slab_plan(int64_t n0, int space_order, int rank, int nra
     return SF_OK;
 }
 
+extern "C" sf_status sf_slab_halo_plan(int64_t n0, int space_order, int rank, int nranks, int64_t plan[7])
+{
+    if (!plan) return sf_set_error(SF_ERR_INVALID_ARG, "plan is NULL");
+    int64_t x0, nl;
+    sf_status s = sf_slab_plan(n0, space_order, rank, nranks, &x0, &nl);
+    if (s) return s;
+    const int64_t r = space_order / 2;
+    plan[0] = r;        // owned planes [r, 2r) -> left neighbour's right halo
+    plan[1] = 0;        // left halo [0, r) <- left neighbour's last owned planes
+    plan[2] = nl;       // owned planes [nl, nl + r) -> right neighbour's left halo
+    plan[3] = nl + r;   // right halo [nl + r, nl + 2r) <- right neighbour's first owned planes
+    plan[4] = r;
+    plan[5] = rank > 0;
+    plan[6] = rank < nranks - 1;
+    return SF_OK;
+}
+
 extern "C" sf_status sf_sparse_owner(int64_t n0, int space_order, int nranks, double h,
                                      double coord0, int *owner)
 {
