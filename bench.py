@@ -107,11 +107,13 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- workload
-def build_problem(nt_override=None, rank=0, nranks=1):
+def build_problem(nt_override=None, rank=0, nranks=1, cfg=1):
     import synth
-    p = synth.make_config(1, nt=nt_override)
+    p = synth.make_config(cfg, nt=nt_override)
     if nranks == 1:
         return p, p.m, p.damp, p.shape
+    if cfg != 1:
+        raise SystemExit("multi-GPU bench runs configs[1] weak-scaled (slab decomposition)")
     # weak scaling: global grid (336 N) x 336 x 336 = the configs[1] model tiled along x
     # (its physical part is x-invariant); the absorbing layer stays at the global x edges.
     r = p.space_order // 2
@@ -132,6 +134,17 @@ def build_problem(nt_override=None, rank=0, nranks=1):
     rec[:, 0] = rec[:, 0] + (nranks - 1) * n0 * p.h / 2.0
     p.src_coords, p.rec_coords = src, rec
     return p, m_loc, eta_loc, gshape
+
+
+WORKLOADS = {
+    0: "configs[0]: 2D acoustic forward 101^2 phys + nbl 20 -> 141x141, so4, nt=500, 101 receivers",
+    1: "configs[1]: 3D acoustic forward 256^3 phys + nbl 40 -> 336^3 comp, so8, nt=1000, "
+       "65536 receivers, 1 source",
+    2: "configs[2]: 3D FWI gradient 256^3 phys + nbl 40 -> 336^3, so8, nt=1000, save every 4 "
+       "(fwd+save, residual, adjoint+correlation; d_obs from the true model outside the timed region)",
+    3: "configs[3]: 3D acoustic forward 1024x512x512, so16, nt=500, no damping layer, 1 GPU",
+    4: "configs[4]: one shot of the multi-shot FWI gradient, 400^3, so12, nt=1500, save every 3",
+}
 
 
 def run_ours(args):
@@ -156,9 +169,11 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    p, m_loc, eta_loc, gshape = build_problem(args.nt, rank, world)
+    cfg = args.config
+    p, m_loc, eta_loc, gshape = build_problem(args.nt, rank, world, cfg)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
-    m_d, eta_d = dev(m_loc), dev(eta_loc)
+    m_d = dev(m_loc)
+    eta_d = None if eta_loc is None else dev(eta_loc)
     prop = sf.Propagator(m_d, eta_d, shape=gshape, h=p.h, space_order=p.space_order, nt=p.nt,
                          dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords,
                          comm=comm, rank=rank, nranks=world)
@@ -169,9 +184,26 @@ def run_ours(args):
     tuning = prop.tuning()
     log(f"[bench] rank {rank}/{world} grid {gshape} local {prop.local_shape} nt {p.nt} tuning {tuning}")
 
+    grad_mode = cfg in (2, 4)
+    passes = 2 if grad_mode else 1          # propagations per step (fwd + adj for gradients)
+    if grad_mode:
+        k = p.save_every
+        # observed data from the true model (input preparation, outside the timed region)
+        prop_true = sf.Propagator(dev(p.m_true), eta_d, shape=gshape, h=p.h, space_order=p.space_order,
+                                  nt=p.nt, dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords)
+        d_obs, _, _ = prop_true.forward(wav)
+        torch.cuda.synchronize()
+        prop_true.close()
+        del prop_true
+        ws = torch.empty(prop.gradient_workspace_bytes(k), dtype=torch.uint8, device="cuda")
+        grad = torch.empty(prop.local_shape, device="cuda")
+
     def step():
-        u.zero_()
-        prop.forward(wav, u=u, rec=rec)
+        if grad_mode:
+            prop.gradient(wav, d_obs, save_every=k, grad=grad, ws=ws)
+        else:
+            u.zero_()
+            prop.forward(wav, u=u, rec=rec)
 
     for _ in range(args.warmup):
         step()
@@ -196,11 +228,14 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    updates = npts_local * world * (p.nt - 1) * args.steps
+    updates = npts_local * world * (p.nt - 1) * args.steps * passes
     value = updates / (ms_max * 1e-3) / 1e9
 
     # roofline of the dominant kernel (stencil step): algorithmic bytes per launch
     bpp = 20 if eta_loc is not None else 16      # u^n, u^{n-1}, out, c3(+beta) fp32
+    # (gradient configs: the average over plain, save and fused-correlation launches is
+    # reported against the plain-step byte count; the extra save / correlation bytes are
+    # listed separately in per_update_us)
     launch_ms = prof["stencil_ms"] / max(prof["stencil_launches"], 1)
     alg_bytes = bpp * npts_local
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
@@ -211,7 +246,7 @@ def run_ours(args):
     if rank == 0:
         # end to end through the public C-ABI with HOST buffers (pinned), N=1 form
         e2e = None
-        if world == 1 and not args.no_e2e:
+        if world == 1 and not args.no_e2e and cfg in (0, 1, 3):
             e2e = run_e2e(p, args)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -222,13 +257,14 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded configs[1] model: two layers, 40-pt quadratic damping layer, "
                     "15 Hz Ricker; no dataset in the paper)",
-            "config": {"workload": "configs[1]: 3D acoustic forward 256^3 phys + nbl 40 -> "
-                                   f"{'x'.join(map(str, gshape))} comp, so8, nt={p.nt}, "
-                                   f"{p.rec_coords.shape[0]} receivers, 1 source",
+            "config": {"workload": WORKLOADS[cfg] + (f" (weak-scaled: {'x'.join(map(str, gshape))} "
+                                                     f"global, slab per GPU)" if world > 1 else ""),
                        "grid": list(gshape), "space_order": p.space_order, "nt": p.nt,
                        "points_per_rank": npts_local, "parallelism": f"slab{world}" if world > 1 else "1gpu",
-                       "l2": "inputs larger than L2 (each 336^3 fp32 field = 152 MB > 126 MB L2; "
-                             "4 fields streamed per update)",
+                       "l2": "inputs larger than L2 (each fp32 field >= 152 MB > 126 MB L2; "
+                             "4-5 fields streamed per update)" if npts_local * 4 > 126e6 else
+                             "grid smaller than L2 (configs[0]: launch-bound toy)",
+                       "propagations_per_step": passes,
                        "kernel_tuning": tuning},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
@@ -236,7 +272,8 @@ def run_ours(args):
                          "traffic_source": "profiles/r01_stencil_ncu_full.json (ncu --set full, dram "
                                            "read+write per launch, random-init wavefield)",
                          "peak_source": peak_src,
-                         "kernel": "k_tma3d (stencil step, fwd)" if tuning["variant"] == 2 else "k_generic3d",
+                         "kernel": "k_tma3d (stencil step)" if tuning["variant"] == 2 else
+                                   ("k_generic3d" if len(gshape) == 3 else "k_generic2d"),
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "bytes_per_point": bpp, "avg_launch_ms": round(launch_ms, 5),
                          "stencil_share_of_step": round(prof["stencil_ms"] / max(ms, 1e-9), 4),
@@ -301,11 +338,14 @@ def cpu_baseline(p, seconds):
     t = time.perf_counter() - t0
     return {"value": round(N * (k - 1) / t / 1e9, 5), "unit": UNIT, "cores": oracle.num_threads(),
             "kind": "oracle", "seconds": round(t, 2),
-            "sample": f"configs[1] full 336^3 grid, first {k} of {p.nt} time samples "
-                      f"({k - 1} updates), fp64 C oracle"}
+            "sample": f"{p.name}: full {'x'.join(map(str, p.shape))} grid, first {k} of {p.nt} time "
+                      f"samples ({k - 1} forward updates), fp64 C oracle"}
 
 
 def run_reference(args):
+    """--impl reference: the paper ships no code (PAPER.md only), so the reference arm is
+    the fp64 C oracle, timed as it stands on the host cores, on a bounded sample of the
+    same workload (the first `--ref-steps-nt` time samples of the config per step)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1 and rank != 0:
@@ -313,23 +353,24 @@ def run_reference(args):
     import oracle
     import synth
     oracle.build()
-    p = synth.make_config(1, nt=args.nt)
+    p = synth.make_config(args.config, nt=args.nt)
     N = int(np.prod(p.shape))
-    k = args.ref_steps_nt
-    for _ in range(args.warmup and 1):
+    k = min(args.ref_steps_nt, p.nt)
+    for _ in range(min(args.warmup, 1)):
         oracle.forward(p, nt=2, wavelet=p.wavelet[:2])
     t0 = time.perf_counter()
     for _ in range(args.steps):
         oracle.forward(p, nt=k, wavelet=p.wavelet[:k])
     t = time.perf_counter() - t0
     v = N * (k - 1) * args.steps / t / 1e9
+    sample = f"{p.name}: full {'x'.join(map(str, p.shape))} grid, {k} of {p.nt} time samples per step"
     cpu = {"value": round(v, 5), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-           "sample": f"configs[1] full 336^3 grid, {k} time samples per step"}
+           "sample": sample}
     return {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t / args.steps * 1e3, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"configs[1] 336^3 so8, bounded sample of {k} of {p.nt} time samples"},
+            "config": {"workload": WORKLOADS[args.config] + f" -- bounded sample: {sample}"},
             "cpu_baseline": cpu,
             "e2e": {"value": round(v, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -340,7 +381,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--nt", type=int, default=None, help="override nt (default: configs[1] 1000)")
+    ap.add_argument("--nt", type=int, default=None, help="override nt (default: the config's)")
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4],
+                    help="BASELINE configs[i] workload (default 1: the metric's headline config)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
