@@ -21,9 +21,12 @@ STATUS = {0: "SF_OK", 1: "SF_ERR_INVALID_ARG", 2: "SF_ERR_SHAPE", 3: "SF_ERR_ORD
 # every symbol include/sf.h declares
 EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint", "sf_residual",
            "sf_gradient_workspace_bytes", "sf_gradient", "sf_forward_host", "sf_set_profiling",
-           "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_get_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
+           "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_create_slab",
            "sf_allreduce_gradient", "sf_last_error", "sf_version"]
+
+
+SF_OPT_L2_PREFETCH, SF_OPT_SPLIT, SF_OPT_FUSE_MAX = 1, 2, 3
 
 
 class SfError(RuntimeError):
@@ -74,6 +77,7 @@ def lib():
             "sf_get_profile": [P, P, P, P, I],
             "sf_get_profile_detail": [P, P, P, I],
             "sf_set_tuning": [P, I, I, I],
+            "sf_set_option": [P, I, I],
             "sf_get_tuning": [P, P, P, P],
             "sf_slab_plan": [I64, I, I, I, P, P],
             "sf_slab_halo_plan": [I64, I, I, I, P],

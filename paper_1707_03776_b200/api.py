@@ -154,6 +154,10 @@ class Propagator:
     def set_tuning(self, variant: int = 0, by: int = 0, chunks: int = 0):
         check(lib().sf_set_tuning(self._h, variant, by, chunks))
 
+    def set_option(self, option: int, value: int):
+        """sf_set_option: 1 L2 prefetch distance, 2 split boundary launches, 3 fuse-max points."""
+        check(lib().sf_set_option(self._h, int(option), int(value)))
+
     def tuning(self):
         v, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         check(lib().sf_get_tuning(self._h, ctypes.byref(v), ctypes.byref(b), ctypes.byref(c)))

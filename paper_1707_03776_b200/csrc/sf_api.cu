@@ -20,7 +20,6 @@
 #include "sparse.cuh"
 
 #define SF_VERSION 1
-#define SF_FUSE_MAX 256  // largest sparse point set handled inside the stencil kernel
 
 static thread_local char g_err[1024] = "";
 
@@ -158,10 +157,10 @@ static int resolve_by(const sf_handle *h)
 // tiles fit in one wave we take the largest chunk count that keeps a single wave
 // (fewest 2r warm-up planes); otherwise balance whole waves against the warm-up
 // planes each chunk re-reads (SURVEY H2 model).
-static int resolve_chunks(const sf_handle *h, int by)
+static int resolve_chunks(const sf_handle *h, int by, int64_t planes)
 {
-    if (h->chunks > 0) return h->chunks;
-    const int64_t planes = h->xb - h->xa;
+    if (planes <= 0) planes = h->xb - h->xa;
+    if (h->chunks > 0) return (int)std::min<int64_t>(h->chunks, std::max<int64_t>(1, planes));
     const int64_t tiles = ((h->nb[2] + 127) / 128) * ((h->nb[1] + by - 1) / by);
     const int sms = h->sms;
     const int per_sm = (by == 8 && h->r <= 4) ? 2 : 1;
@@ -231,6 +230,7 @@ struct StepBufs {
     const float *inj_vals; // its values for this step ([npoint])
     SfSparse *itp;         // point set interpolated from the new level (or NULL)
     float *itp_row;        // its record row for the new level ([npoint])
+    int64_t xa = 0, xb = 0;  // planes to compute (xa == xb: the handle's full range)
 };
 
 template <class T>
@@ -414,15 +414,16 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         a.n1 = 1;
         a.n2 = h->nb[1];
     }
-    a.xa = h->xa;
-    a.xb = h->xb;
+    a.xa = b.xa < b.xb ? b.xa : h->xa;
+    a.xb = b.xa < b.xb ? b.xb : h->xb;
     a.w = h->w;
+    a.l2_prefetch = h->l2_prefetch;
 
     SfLaunch L{};
     L.ndim = h->ndim;
     L.variant = resolve_variant(h);
     L.by = resolve_by(h);
-    L.chunks = resolve_chunks(h, L.by);
+    L.chunks = resolve_chunks(h, L.by, a.xb - a.xa);
     L.damp = h->beta != nullptr;
     L.mode = mode;
     L.snap_slot = b.snap_slot;
@@ -448,7 +449,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     L.maps = &maps;
     // fuse only small point sets (a few shots' sources): large sets (receiver grids) would
     // put dependent table loads on the stencil's critical path -> standalone kernels
-    if (L.variant == SF_VAR_TMA && b.inj && b.inj->ntgt > 0 && b.inj->ntgt <= SF_FUSE_MAX && b.inj_vals) {
+    if (L.variant == SF_VAR_TMA && b.inj && b.inj->ntgt > 0 && b.inj->ntgt <= h->fuse_max && b.inj_vals) {
         sf_status s = ensure_inj_tiles(h, *b.inj, L.by);
         if (s) return s;
         a.inj_beg = b.inj->tiles.beg;
@@ -461,7 +462,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         a.inj_vals = b.inj_vals;
         *fused = true;
     }
-    if (L.variant == SF_VAR_TMA && h->nranks == 1 && b.itp && b.itp->np > 0 && b.itp->np <= SF_FUSE_MAX &&
+    if (L.variant == SF_VAR_TMA && h->nranks == 1 && b.itp && b.itp->np > 0 && b.itp->np <= h->fuse_max &&
         b.itp_row) {
         sf_status s = ensure_itp_tiles(h, *b.itp, L.by);
         if (s) return s;
@@ -537,6 +538,8 @@ static void free_sparse(SfSparse &s)
     cudaFree(s.e_w);
     cudaFree(s.ej_pt);
     cudaFree(s.ej_coef);
+    cudaFree(s.jl_bnd);
+    cudaFree(s.jl_int);
     s = SfSparse{};
 }
 
@@ -720,11 +723,15 @@ extern "C" void sf_destroy(sf_handle *h)
     for (int k = 0; k < 2; ++k)
         if (h->ev_itp[k]) cudaEventDestroy(h->ev_itp[k]);
     if (h->side) cudaStreamDestroy(h->side);
+    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
+    if (h->ev_xch) cudaEventDestroy(h->ev_xch);
     delete h;
 }
 
 static sf_status create_common(const sf_desc *d, sf_handle *h)
 {
+    if (const char *e = getenv("SF_L2_PREFETCH")) h->l2_prefetch = atoi(e);
     {
         int dev = 0, v = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -778,6 +785,10 @@ static sf_status create_common(const sf_desc *d, sf_handle *h)
     if ((s = build_sparse(h, d->nsrc, d->src_coords, d->m, h->src, "source"))) return s;
     if ((s = build_sparse(h, d->nrec, d->rec_coords, d->m, h->rec, "receiver"))) return s;
     SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+    SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming));
+    SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_xch, cudaEventDisableTiming));
+    h->split = h->nranks > 1;
     SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
     SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_itp[0], cudaEventDisableTiming));
     SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_itp[1], cudaEventDisableTiming));
@@ -925,6 +936,27 @@ extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int by, int chunks
     return SF_OK;
 }
 
+extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
+{
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    switch (option) {
+    case SF_OPT_L2_PREFETCH:
+        if (value < 0 || value > 64) return sf_set_error(SF_ERR_INVALID_ARG, "prefetch distance %d", value);
+        h->l2_prefetch = value;
+        return SF_OK;
+    case SF_OPT_SPLIT:
+        if (h->nranks > 1 && !value) return sf_set_error(SF_ERR_INVALID_ARG, "slab mode always splits");
+        h->split = value != 0;
+        return SF_OK;
+    case SF_OPT_FUSE_MAX:
+        if (value < 0) return sf_set_error(SF_ERR_INVALID_ARG, "fuse max %d", value);
+        h->fuse_max = value;
+        return SF_OK;
+    default:
+        return sf_set_error(SF_ERR_INVALID_ARG, "unknown option %d", option);
+    }
+}
+
 extern "C" sf_status sf_get_tuning(const sf_handle *h, int *variant, int *by, int *chunks)
 {
     if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
@@ -932,7 +964,7 @@ extern "C" sf_status sf_get_tuning(const sf_handle *h, int *variant, int *by, in
     const int b = resolve_by(h);
     if (variant) *variant = v;
     if (by) *by = v == SF_VAR_TMA ? b : 0;
-    if (chunks) *chunks = v == SF_VAR_TMA ? resolve_chunks(h, b) : 0;
+    if (chunks) *chunks = v == SF_VAR_TMA ? resolve_chunks(h, b, 0) : 0;
     return SF_OK;
 }
 
@@ -1001,6 +1033,88 @@ static sf_status swap_halves(sf_handle *h, float *a, float *b, cudaStream_t st)
     return SF_OK;
 }
 
+// target rows of a point set split into boundary planes [xa, xa+r) U [xb-r, xb) and the
+// interior (built once per handle)
+static sf_status ensure_split_lists(sf_handle *h, SfSparse &sp)
+{
+    if (sp.n_bnd >= 0) return SF_OK;
+    const int64_t plane = h->N / h->nb[0];
+    std::vector<int> bnd, itr;
+    for (size_t t = 0; t < sp.h_tgt.size(); ++t) {
+        const int64_t x = sp.h_tgt[t] / plane;
+        if (x < h->xa + h->r || x >= h->xb - h->r) bnd.push_back((int)t);
+        else itr.push_back((int)t);
+    }
+    sf_status s;
+    if ((s = upload(&sp.jl_bnd, bnd))) return s;
+    if ((s = upload(&sp.jl_int, itr))) return s;
+    sp.n_bnd = (int)bnd.size();
+    sp.n_int = (int)itr.size();
+    return SF_OK;
+}
+
+static sf_status launch_inject_list(sf_handle *h, const SfSparse &sp, float *u, const float *vals,
+                                    const int *list, int nl, float *snap_patch, const float *grad_snap,
+                                    float *grad, float gscale, cudaStream_t st)
+{
+    if (nl <= 0 || !vals) return SF_OK;
+    ProfScope ps(h, PK_INJECT, st);
+    if (sp.jk > 0) {
+        k_inject_ell_list<<<(nl + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.jk, sp.ej_pt, sp.ej_coef, sp.ntgt,
+                                                            list, nl, vals, snap_patch, grad_snap, grad, gscale);
+    } else {
+        return sf_set_error(SF_ERR_INVALID_ARG, "split injection needs <= 8 contributions per target");
+    }
+    SF_CUDA_TRY(cudaGetLastError());
+    return SF_OK;
+}
+
+// One time step: stencil (+ fused sparse work), standalone injection if not fused, and in
+// slab mode the halo exchange.  Split mode computes the r boundary planes at each end
+// first, injects there, hands them to NCCL on the comm stream and computes the interior
+// while the halos travel; the stream then waits for the exchange.
+static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, const float *grad_snap,
+                         cudaStream_t st, bool *fused_itp)
+{
+    sf_status s;
+    bool fused = false;
+    const int64_t r = h->r, xa = h->xa, xb = h->xb;
+    if (!h->split || xb - xa <= 2 * r) {
+        if ((s = launch_step(h, b, mode, st, &fused, fused_itp))) return s;
+        if (!fused && (s = launch_inject(h, *b.inj, b.out, b.inj_vals, snap_patch, grad_snap, b.grad,
+                                         b.gscale, st)))
+            return s;
+        if (h->nranks > 1) return sf_comm_halo_exchange(h, b.out, st);
+        return SF_OK;
+    }
+    bool f2 = false, fi2 = false;
+    StepBufs bl = b, br = b, bi = b;
+    bl.xa = xa, bl.xb = xa + r;
+    br.xa = xb - r, br.xb = xb;
+    bi.xa = xa + r, bi.xb = xb - r;
+    if ((s = launch_step(h, bl, mode, st, &fused, fused_itp))) return s;
+    if ((s = launch_step(h, br, mode, st, &f2, &fi2))) return s;
+    const bool need_inj = !fused && b.inj && b.inj->ntgt > 0 && b.inj_vals;
+    if (need_inj) {
+        if ((s = ensure_split_lists(h, *b.inj))) return s;
+        if ((s = launch_inject_list(h, *b.inj, b.out, b.inj_vals, b.inj->jl_bnd, b.inj->n_bnd, snap_patch,
+                                    grad_snap, b.grad, b.gscale, st)))
+            return s;
+    }
+    if (h->nranks > 1) {
+        SF_CUDA_TRY(cudaEventRecord(h->ev_bnd, st));
+        SF_CUDA_TRY(cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
+        if ((s = sf_comm_halo_exchange(h, b.out, h->comm_stream))) return s;
+        SF_CUDA_TRY(cudaEventRecord(h->ev_xch, h->comm_stream));
+    }
+    if ((s = launch_step(h, bi, mode, st, &f2, &fi2))) return s;
+    if (need_inj && (s = launch_inject_list(h, *b.inj, b.out, b.inj_vals, b.inj->jl_int, b.inj->n_int, snap_patch,
+                                            grad_snap, b.grad, b.gscale, st)))
+        return s;
+    if (h->nranks > 1) SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_xch, 0));
+    return SF_OK;
+}
+
 // Records of a level run on the handle's side stream, concurrently with the next
 // stencil step (which only reads that level); the stencil two steps later overwrites
 // the level, so it waits for the record first.  ev_itp[level & 1] marks completion.
@@ -1063,11 +1177,8 @@ extern "C" sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, 
         float *rrow = rec ? rec + (int64_t)(n + 1) * h->rec.np : nullptr;
         if ((s = wait_interp(h, n - 1, st))) return s;
         StepBufs b{cur, out, slot, nullptr, 0, 0, nullptr, 0.f, &h->src, wrow, &h->rec, rrow};
-        bool fused = false, fused_itp = false;
-        if ((s = launch_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, st, &fused, &fused_itp))) return s;
-        if (!fused && (s = launch_inject(h, h->src, out, wrow, slot, nullptr, nullptr, 0.f, st)))
-            return s;
-        if ((s = post_step_exchange(h, out, st))) return s;
+        bool fused_itp = false;
+        if ((s = do_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, slot, nullptr, st, &fused_itp))) return s;
         if ((s = side_interp(h, h->rec, fused_itp, out, rrow, n + 1, st))) return s;
     }
     if ((s = join_side(h, st))) return s;
@@ -1107,13 +1218,10 @@ extern "C" sf_status sf_adjoint(sf_handle *h, const float *res, float *srca, flo
         float *srow = srca ? srca + (int64_t)(n - 1) * h->src.np : nullptr;
         StepBufs b{cur, out, nullptr, g ? snaps : nullptr, g ? n / save_every : 0, nsnap,
                    g ? grad : nullptr, gscale, &h->rec, rrow, &h->src, srow};
-        bool fused = false, fused_itp = false;
-        if ((s = launch_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, st, &fused, &fused_itp))) return s;
-        if (!fused && (s = launch_inject(h, h->rec, out, rrow, nullptr,
-                                         g ? snaps + (int64_t)(n / save_every) * N : nullptr,
-                                         g ? grad : nullptr, gscale, st)))
+        bool fused_itp = false;
+        if ((s = do_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, nullptr,
+                         g ? snaps + (int64_t)(n / save_every) * N : nullptr, st, &fused_itp)))
             return s;
-        if ((s = post_step_exchange(h, out, st))) return s;
         if ((s = side_interp(h, h->src, fused_itp, out, srow, j + 1, st))) return s;
     }
     if ((s = join_side(h, st))) return s;

@@ -50,6 +50,9 @@ struct SfSparse {
     int jk = 0;               // injection slots per target (0: use CSR)
     int *ej_pt = nullptr;
     float *ej_coef = nullptr;
+    // split launches: target rows in the boundary planes / in the interior
+    int *jl_bnd = nullptr, *jl_int = nullptr;
+    int n_bnd = -1, n_int = 0;
     std::vector<int64_t> h_tgt;  // host copy of the target offsets
     std::vector<int64_t> h_iidx; // host copy of the interpolation corners
     std::vector<float> h_iw;
@@ -74,6 +77,7 @@ struct sf_handle {
     double *dJ = nullptr;
     // tuning
     int variant = SF_VAR_AUTO, by = 0, chunks = 0;
+    int l2_prefetch = 4;            // TMA L2 prefetch distance (planes); env SF_L2_PREFETCH
     // slab decomposition
     int rank = 0, nranks = 1;
     void *comm = nullptr;
@@ -90,6 +94,11 @@ struct sf_handle {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_itp[2] = {nullptr, nullptr};
     bool itp_pending[2] = {false, false};
+    // boundary-first split launches (always in slab mode; optional on one GPU)
+    bool split = false;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_bnd = nullptr, ev_xch = nullptr;
+    int fuse_max = 256;
 };
 
 // error reporting (thread-local message)

@@ -66,6 +66,27 @@ __global__ void k_inject_ell(float *__restrict__ u, const int64_t *__restrict__ 
     if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(grad_snap[g], d), grad[g]);
 }
 
+// k_inject_ell restricted to a list of target rows (split boundary / interior launches)
+__global__ void k_inject_ell_list(float *__restrict__ u, const int64_t *__restrict__ tgt, int K,
+                                  const int *__restrict__ ept, const float *__restrict__ ecoef, int ntgt,
+                                  const int *__restrict__ list, int nl, const float *__restrict__ vals,
+                                  float *__restrict__ snap_patch, const float *__restrict__ grad_snap,
+                                  float *__restrict__ grad, float gscale)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nl) return;
+    const int t = list[i];
+    const int64_t g = tgt[t];
+    float d = 0.0f;
+    for (int c = 0; c < K; ++c) {
+        const float cf = ecoef[(int64_t)c * ntgt + t];
+        if (cf != 0.0f) d = __fmaf_rn(cf, vals[ept[(int64_t)c * ntgt + t]], d);
+    }
+    u[g] = __fadd_rn(u[g], d);
+    if (snap_patch) snap_patch[g] = __fadd_rn(snap_patch[g], d);
+    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(grad_snap[g], d), grad[g]);
+}
+
 // CSR -> ELL (slot-major) for the injection tables
 __global__ void k_csr_to_ell(const int *__restrict__ rowptr, const int *__restrict__ pt,
                              const float *__restrict__ coef, int ntgt, int K, int *__restrict__ ept,

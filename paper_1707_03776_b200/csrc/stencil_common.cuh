@@ -123,6 +123,7 @@ struct SfStepArgs {
     int64_t n0b, n1, n2;   // buffer extents (n0b includes slab halo planes)
     int64_t xa, xb;        // planes [xa, xb) of the buffer to compute
     SfWeights w;
+    int l2_prefetch;       // TMA kernel: L2 prefetch distance in planes (0 = off)
     // Fused sparse work of the TMA kernel (NULL *_beg = none).  Lists are per consumer
     // warp w of tile t = blockIdx.y * gridDim.x + blockIdx.x: entries
     // [beg[t * BY + w], beg[t * BY + w + 1]) sorted by output plane q; every entry is

@@ -82,6 +82,15 @@ __device__ __forceinline__ void tma_load4(void *dst, const CUtensorMap *tm, int 
         : "memory");
 }
 
+// L2 prefetch of a TMA box (no shared memory, no completion tracking)
+__device__ __forceinline__ void tma_prefetch3(const CUtensorMap *tm, int c0, int c1, int c2)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
 {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
@@ -124,6 +133,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 {
     using C = Cfg<R, BY, DAMP, MODE>;
     constexpr int Q = C::Q, TZ = C::TZ, HZ = C::HZ, W = C::W, S = C::S, PR = C::PRING;
+    const int PD = a.l2_prefetch;  // planes of L2 prefetch beyond the smem ring (0 = off)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // keep the address space visible to the compiler (LDS, not generic LD): align by
     // offsetting the shared array itself
@@ -182,6 +192,17 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                         tma_load4(pl, &tm_snap, z0, y0, q, snap_slot, &full[st]);
                         pl += C::PL_BYTES;
                         tma_load3(pl, &tm_grad, z0, y0, q, &full[st]);
+                    }
+                }
+                // warm L2 PD planes ahead of the smem ring: the smem stages then fill from
+                // L2 and the ring depth no longer has to cover the full HBM latency
+                if (PD > 0 && i + PD < NP) {
+                    const int pp = p + PD, qq = q + PD;
+                    tma_prefetch3(&tm_cur, z0 - HZ, y0 - R, pp);
+                    if (i + PD >= 2 * R) {
+                        tma_prefetch3(&tm_old, z0, y0, qq);
+                        tma_prefetch3(&tm_c3, z0, y0, qq);
+                        if (DAMP) tma_prefetch3(&tm_beta, z0, y0, qq);
                     }
                 }
                 if (++st == S) {
