@@ -12,11 +12,11 @@
 
 namespace {
 
-template <int BY, bool DAMP, int MODE>
+template <int BY, int VZ, bool DAMP, int MODE>
 cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    using C = sftma::Cfg<SF_R, BY, DAMP, MODE>;
-    auto kern = sftma::k_tma3d<SF_R, BY, DAMP, MODE>;
+    using C = sftma::Cfg<SF_R, BY, VZ, DAMP, MODE>;
+    auto kern = sftma::k_tma3d<SF_R, BY, VZ, DAMP, MODE>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -49,38 +49,48 @@ cudaError_t launch_generic(const SfLaunch &L, const SfStepArgs &a, cudaStream_t 
     return cudaGetLastError();
 }
 
-template <int BY>
+template <int BY, int VZ>
 cudaError_t launch_tma_by(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     if (L.damp) {
         switch (L.mode) {
-        case SF_MODE_PLAIN: return launch_tma<BY, true, SF_MODE_PLAIN>(L, a, st);
-        case SF_MODE_SAVE: return launch_tma<BY, true, SF_MODE_SAVE>(L, a, st);
-        default: return launch_tma<BY, true, SF_MODE_GRAD>(L, a, st);
+        case SF_MODE_PLAIN: return launch_tma<BY, VZ, true, SF_MODE_PLAIN>(L, a, st);
+        case SF_MODE_SAVE: return launch_tma<BY, VZ, true, SF_MODE_SAVE>(L, a, st);
+        default: return launch_tma<BY, VZ, true, SF_MODE_GRAD>(L, a, st);
         }
     }
     switch (L.mode) {
-    case SF_MODE_PLAIN: return launch_tma<BY, false, SF_MODE_PLAIN>(L, a, st);
-    case SF_MODE_SAVE: return launch_tma<BY, false, SF_MODE_SAVE>(L, a, st);
-    default: return launch_tma<BY, false, SF_MODE_GRAD>(L, a, st);
+    case SF_MODE_PLAIN: return launch_tma<BY, VZ, false, SF_MODE_PLAIN>(L, a, st);
+    case SF_MODE_SAVE: return launch_tma<BY, VZ, false, SF_MODE_SAVE>(L, a, st);
+    default: return launch_tma<BY, VZ, false, SF_MODE_GRAD>(L, a, st);
     }
 }
 
-template <int BY, bool DAMP, int MODE>
-int smem_of() { return sftma::Cfg<SF_R, BY, DAMP, MODE>::SMEM; }
+template <int BY, int VZ, bool DAMP, int MODE>
+int smem_of() { return sftma::Cfg<SF_R, BY, VZ, DAMP, MODE>::SMEM; }
+
+template <int BY, int VZ>
+int smem_by(int damp, int mode)
+{
+    if (damp) return mode == 0 ? smem_of<BY, VZ, true, 0>() : mode == 1 ? smem_of<BY, VZ, true, 1>() : smem_of<BY, VZ, true, 2>();
+    return mode == 0 ? smem_of<BY, VZ, false, 0>() : mode == 1 ? smem_of<BY, VZ, false, 1>() : smem_of<BY, VZ, false, 2>();
+}
 
 }  // namespace
 
-// BY = 16 only where the 2 x (2R+1) x 4 register queues fit 128 registers/thread.
-#define SF_BY16_OK (SF_R <= 4)
-
+// Tile shapes: r <= 4: BY = 16 or 8 warps of 4 z per lane (128-column tiles); r >= 5:
+// BY = 8 with 4 z per lane, or BY = 16 with 2 z per lane (64-column tiles) -- the
+// (2r+1)-deep register queues must fit the 96-register budget of 17 warps.
 cudaError_t SF_CAT(sf_launch_step_r, SF_R)(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     if (L.variant == SF_VAR_TMA) {
-#if SF_BY16_OK
-        if (L.by == 16) return launch_tma_by<16>(L, a, st);
+#if SF_R <= 4
+        if (L.by == 16) return launch_tma_by<16, 4>(L, a, st);
+        return launch_tma_by<8, 4>(L, a, st);
+#else
+        if (L.by == 16) return launch_tma_by<16, 2>(L, a, st);
+        return launch_tma_by<8, 4>(L, a, st);
 #endif
-        return launch_tma_by<8>(L, a, st);
     }
     switch (L.mode) {
     case SF_MODE_PLAIN: return launch_generic<SF_MODE_PLAIN>(L, a, st);
@@ -91,13 +101,11 @@ cudaError_t SF_CAT(sf_launch_step_r, SF_R)(const SfLaunch &L, const SfStepArgs &
 
 int SF_CAT(sf_tma_smem_r, SF_R)(int by, int damp, int mode)
 {
-#if SF_BY16_OK
-    if (by == 16) {
-        if (damp) return mode == 0 ? smem_of<16, true, 0>() : mode == 1 ? smem_of<16, true, 1>() : smem_of<16, true, 2>();
-        return mode == 0 ? smem_of<16, false, 0>() : mode == 1 ? smem_of<16, false, 1>() : smem_of<16, false, 2>();
-    }
+#if SF_R <= 4
+    if (by == 16) return smem_by<16, 4>(damp, mode);
+    return smem_by<8, 4>(damp, mode);
+#else
+    if (by == 16) return smem_by<16, 2>(damp, mode);
+    return smem_by<8, 4>(damp, mode);
 #endif
-    if (by != 8) return 0;
-    if (damp) return mode == 0 ? smem_of<8, true, 0>() : mode == 1 ? smem_of<8, true, 1>() : smem_of<8, true, 2>();
-    return mode == 0 ? smem_of<8, false, 0>() : mode == 1 ? smem_of<8, false, 1>() : smem_of<8, false, 2>();
 }

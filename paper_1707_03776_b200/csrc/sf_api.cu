@@ -147,10 +147,14 @@ static int resolve_variant(const sf_handle *h)
 
 static int resolve_by(const sf_handle *h)
 {
-    if (h->by == 8) return 8;
-    if (h->by == 16 && h->r <= 4) return 16;
-    return h->r <= 4 ? 16 : 8;
+    if (h->by == 8 || h->by == 16) return h->by;
+    return 16;
 }
+
+// z points per lane of the TMA kernel: 4 (128-column tiles), or 2 (64-column tiles) for
+// r >= 5 with 16 warps (register budget; inst_body.cuh)
+static int tile_vz(const sf_handle *h, int by) { return (h->r >= 5 && by == 16) ? 2 : 4; }
+static int tile_tz(const sf_handle *h, int by) { return 32 * tile_vz(h, by); }
 
 // x-chunks per tile column.  Measured on B200 (scripts/tune.py, profiles/): with the
 // TMA pipeline one partial wave of CTAs already saturates HBM, so when the (y, z)
@@ -161,7 +165,8 @@ static int resolve_chunks(const sf_handle *h, int by, int64_t planes)
 {
     if (planes <= 0) planes = h->xb - h->xa;
     if (h->chunks > 0) return (int)std::min<int64_t>(h->chunks, std::max<int64_t>(1, planes));
-    const int64_t tiles = ((h->nb[2] + 127) / 128) * ((h->nb[1] + by - 1) / by);
+    const int tz = tile_tz(h, by);
+    const int64_t tiles = ((h->nb[2] + tz - 1) / tz) * ((h->nb[1] + by - 1) / by);
     const int sms = h->sms;
     const int per_sm = (by == 8 && h->r <= 4) ? 2 : 1;
     const int64_t slots = (int64_t)sms * per_sm;
@@ -272,15 +277,17 @@ struct TileLoc {
 static TileLoc tile_loc(const sf_handle *h, int by, int64_t off)
 {
     const int64_t n1 = h->nb[1], n2 = h->nb[2];
-    const int64_t ntz = (n2 + 127) / 128;
+    const int tz = tile_tz(h, by), vz = tile_vz(h, by);
+    const int64_t ntz = (n2 + tz - 1) / tz;
     const int64_t x = off / (n1 * n2), y = (off / n2) % n1, z = off % n2;
-    const int64_t tile = (y / by) * ntz + z / 128;
-    return {(int)(tile * by + y % by), (int)x, (int)((z % 128) / 4), (int)(z % 4)};
+    const int64_t tile = (y / by) * ntz + z / tz;
+    return {(int)(tile * by + y % by), (int)x, (int)((z % tz) / vz), (int)(z % vz)};
 }
 
 static int64_t n_warp_lists(const sf_handle *h, int by)
 {
-    return ((h->nb[2] + 127) / 128) * ((h->nb[1] + by - 1) / by) * by;
+    const int tz = tile_tz(h, by);
+    return ((h->nb[2] + tz - 1) / tz) * ((h->nb[1] + by - 1) / by) * by;
 }
 
 // Interpolation points whose nonzero corners are all points of one lane (same tile,
@@ -431,9 +438,10 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     memset(&maps, 0, sizeof maps);
     if (L.variant == SF_VAR_TMA) {
         const int HZ = ((h->r + 3) / 4) * 4;
+        const int TZ = tile_tz(h, L.by);
         const int64_t d3[3] = {h->nb[2], h->nb[1], h->nb[0]};
-        const uint32_t bcur[3] = {(uint32_t)(128 + 2 * HZ), (uint32_t)(L.by + 2 * h->r), 1};
-        const uint32_t bpl[3] = {128, (uint32_t)L.by, 1};
+        const uint32_t bcur[3] = {(uint32_t)(TZ + 2 * HZ), (uint32_t)(L.by + 2 * h->r), 1};
+        const uint32_t bpl[3] = {(uint32_t)TZ, (uint32_t)L.by, 1};
         sf_status s;
         if ((s = make_map(&maps.cur, b.cur, 3, d3, bcur))) return s;
         if ((s = make_map(&maps.old, b.out, 3, d3, bpl))) return s;
@@ -441,7 +449,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         if (h->beta && (s = make_map(&maps.beta, h->beta, 3, d3, bpl))) return s;
         if (mode == SF_MODE_GRAD) {
             const int64_t d4[4] = {h->nb[2], h->nb[1], h->nb[0], b.nsnap};
-            const uint32_t b4[4] = {128, (uint32_t)L.by, 1, 1};
+            const uint32_t b4[4] = {(uint32_t)TZ, (uint32_t)L.by, 1, 1};
             if ((s = make_map(&maps.snap, b.snaps, 4, d4, b4))) return s;
             if ((s = make_map(&maps.grad, b.grad, 3, d3, bpl))) return s;
         }
@@ -449,7 +457,8 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     L.maps = &maps;
     // fuse only small point sets (a few shots' sources): large sets (receiver grids) would
     // put dependent table loads on the stencil's critical path -> standalone kernels
-    if (L.variant == SF_VAR_TMA && b.inj && b.inj->ntgt > 0 && b.inj->ntgt <= h->fuse_max && b.inj_vals) {
+    if (L.variant == SF_VAR_TMA && mode != SF_MODE_GRAD && b.inj && b.inj->ntgt > 0 &&
+        b.inj->ntgt <= h->fuse_max && b.inj_vals) {
         sf_status s = ensure_inj_tiles(h, *b.inj, L.by);
         if (s) return s;
         a.inj_beg = b.inj->tiles.beg;
@@ -462,20 +471,9 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         a.inj_vals = b.inj_vals;
         *fused = true;
     }
-    if (L.variant == SF_VAR_TMA && h->nranks == 1 && b.itp && b.itp->np > 0 && b.itp->np <= h->fuse_max &&
-        b.itp_row) {
-        sf_status s = ensure_itp_tiles(h, *b.itp, L.by);
-        if (s) return s;
-        a.itp_beg = b.itp->itiles.beg;
-        a.itp_q = b.itp->itiles.q;
-        a.itp_lane = b.itp->itiles.lane;
-        a.itp_k = b.itp->itiles.k;
-        a.itp_j = b.itp->itiles.j;
-        a.itp_p = b.itp->itiles.p;
-        a.itp_w = b.itp->itiles.w;
-        a.itp_out = b.itp_row;
-        *fused_itp = true;
-    }
+    // (records are interpolated by k_interp_ell on the side stream, concurrently with the
+    //  next step: no in-kernel interpolation)
+
     cudaError_t e;
     {
         ProfScope ps(h, PK_STENCIL, st);

@@ -101,9 +101,9 @@ __device__ __forceinline__ void stg4(float *p, float4 v)
     *reinterpret_cast<float4 *>(p) = v;
 }
 
-template <int R, int BY, bool DAMP, int MODE>
+template <int R, int BY, int VZ, bool DAMP, int MODE>
 struct Cfg {
-    static constexpr int TZ = 128;                       // z columns per CTA (32 lanes x 4)
+    static constexpr int TZ = 32 * VZ;                   // z columns per CTA (32 lanes x VZ)
     static constexpr int HZ = ((R + 3) / 4) * 4;         // z halo rounded up to 4 floats
     static constexpr int W = TZ + 2 * HZ;                // smem row pitch of the u^n tile
     static constexpr int H = BY + 2 * R;                 // rows of the u^n tile
@@ -112,26 +112,70 @@ struct Cfg {
     static constexpr int PL_BYTES = TZ * BY * 4;         // one plane without halo
     static constexpr int NPL = 2 + (DAMP ? 1 : 0) + (MODE == SF_MODE_GRAD ? 2 : 0);
     static constexpr int STAGE_BYTES = CUR_BYTES + NPL * PL_BYTES;
-    static constexpr int PRING = R + 1;                  // in-plane partials kept for R planes
+    static constexpr int PRING = R;                      // in-plane partials kept for R planes
+                                                          // (slot read for plane p-R, then rewritten with p)
     static constexpr int PRING_BYTES = PRING * PL_BYTES;
     static constexpr int S_MAX = (220 * 1024 - PRING_BYTES) / STAGE_BYTES;
-    static constexpr int S = S_MAX >= 4 ? 4 : S_MAX;      // pipeline depth
+    // pipeline depth: 4 stages for r <= 4 (measured equal to 5 on configs[1]; keeps two
+    // BY = 8 CTAs per SM), 5 for r >= 5 (4 % faster on configs[3])
+    static constexpr int S_WANT = R >= 5 ? 5 : 4;
+    static constexpr int S = S_MAX >= S_WANT ? S_WANT : S_MAX;
     static constexpr int SMEM = S * STAGE_BYTES + PRING_BYTES + 128;  // + alignment slack
     static constexpr int THREADS = 32 * (BY + 1);         // BY consumer warps + 1 TMA producer warp
     static_assert(S >= 2, "stage does not fit shared memory");
+    static_assert(VZ == 2 || VZ == 4, "VZ");
 };
 
-// One CTA = BY consumer warps (one y row each, 4 z per lane) + 1 producer warp whose
-// elected lane issues every TMA load.  Per stage: `full` (TMA transaction bytes) and
-// `empty` (one arrive per consumer warp) mbarriers.
-template <int R, int BY, bool DAMP, int MODE>
+// VZ consecutive floats <-> VZ/2 fp32x2 pair registers (LDS/STS/STG .64 / .128)
+template <int VZ>
+__device__ __forceinline__ void ldp(const float *p, f2_t *v)
+{
+    if (VZ == 4) {
+        const ulonglong2 t = *reinterpret_cast<const ulonglong2 *>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+    } else {
+        v[0] = *reinterpret_cast<const unsigned long long *>(p);
+    }
+}
+template <int VZ>
+__device__ __forceinline__ void stp(float *p, const f2_t *v)
+{
+    if (VZ == 4) *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(v[0], v[1]);
+    else *reinterpret_cast<unsigned long long *>(p) = v[0];
+}
+
+// VZ consecutive floats <-> registers (LDS.64 / LDS.128, STG.64 / STG.128)
+template <int VZ>
+__device__ __forceinline__ void ldv(const float *p, float *v)
+{
+    if (VZ == 4) {
+        const float4 t = *reinterpret_cast<const float4 *>(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+        const float2 t = *reinterpret_cast<const float2 *>(p);
+        v[0] = t.x; v[1] = t.y;
+    }
+}
+template <int VZ>
+__device__ __forceinline__ void stv(float *p, const float *v)
+{
+    if (VZ == 4) *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    else *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+}
+
+// One CTA = BY consumer warps (one y row each, VZ consecutive z per lane) + 1 producer
+// warp whose elected lane issues every TMA load.  Per stage: `full` (TMA transaction
+// bytes) and `empty` (one arrive per consumer warp) mbarriers.
+template <int R, int BY, int VZ, bool DAMP, int MODE>
 __global__ void __launch_bounds__(32 * (BY + 1), (BY == 8 && R <= 4) ? 2 : 1)
 k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_old,
         const __grid_constant__ CUtensorMap tm_c3, const __grid_constant__ CUtensorMap tm_beta,
         const __grid_constant__ CUtensorMap tm_snap, const __grid_constant__ CUtensorMap tm_grad,
         const SfStepArgs a, const int snap_slot, const int chunk)
 {
-    using C = Cfg<R, BY, DAMP, MODE>;
+    using C = Cfg<R, BY, VZ, DAMP, MODE>;
+    constexpr int NJ = VZ / 2;  // fp32x2 pairs per lane
     constexpr int Q = C::Q, TZ = C::TZ, HZ = C::HZ, W = C::W, S = C::S, PR = C::PRING;
     const int PD = a.l2_prefetch;  // planes of L2 prefetch beyond the smem ring (0 = off)
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -215,14 +259,14 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     }
 
     // ---------------------------------------------------- consumer warps
-    float V[Q][4];  // u at planes, slot = iteration index mod Q
+    f2_t V[Q][NJ];  // u at planes (fp32 pairs), slot = iteration index mod Q
     const int rown = R + wy;
-    const int zg = z0 + 4 * lane;
+    const int zg = z0 + VZ * lane;
     const int yg = y0 + wy;
     const bool active = (zg < a.n2) && (yg < a.n1);
     const int64_t plane = a.n1 * a.n2;
     const int64_t rowoff = (int64_t)yg * a.n2 + zg;
-    const int po = wy * TZ + 4 * lane;   // this thread's float4 in a halo-free plane
+    const int po = wy * TZ + VZ * lane;  // this thread's VZ floats in a halo-free plane
     float *myP = pring + po;            // private ring of in-plane partials (stride PL floats)
     int st = 0, pw = 0;
     uint32_t ph = 0;
@@ -232,10 +276,10 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     for (int k = 1; k <= R; ++k) Wk[k] = pk2(a.w.w[k], a.w.w[k]);
     Wk[0] = 0ull;
     const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f);
-    const f2_t NG = pk2(-a.gscale, -a.gscale);
+    const f2_t NG = pk2(-a.gscale, -a.gscale), ONE2 = pk2(1.f, 1.f);
     // fused sparse work: this warp's cursors (warp-uniform), first entries at q >= qa
     constexpr int QINF = 0x7fffffff;
-    int ci = 0, ce = 0, cq = QINF, pi = 0, pe = 0, pq_ = QINF;
+    int ci = 0, ce = 0, cq = QINF;
     {
         const int wl = (blockIdx.y * gridDim.x + blockIdx.x) * BY + wy;
         if (a.inj_beg) {
@@ -243,12 +287,6 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
             ce = a.inj_beg[wl + 1];
             while (ci < ce && a.inj_q[ci] < qa) ++ci;
             cq = ci < ce ? a.inj_q[ci] : QINF;
-        }
-        if (a.itp_beg) {
-            pi = a.itp_beg[wl];
-            pe = a.itp_beg[wl + 1];
-            while (pi < pe && a.itp_q[pi] < qa) ++pi;
-            pq_ = pi < pe ? a.itp_q[pi] : QINF;
         }
     }
 
@@ -260,58 +298,58 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                 mbar_wait(&full[st], ph);
                 const unsigned char *sb = smem + st * C::STAGE_BYTES;
                 const float *cs = reinterpret_cast<const float *>(sb);
-                // z row of this thread: columns [4 lane, 4 lane + 2 HZ + 4)
-                float zr[2 * HZ + 4];
+                // z row of this thread as aligned fp32 pairs: floats [VZ lane, VZ lane + 2 HZ + VZ)
+                constexpr int NZP = (2 * HZ + VZ) / 2;
+                f2_t zp[NZP];
 #pragma unroll
-                for (int c = 0; c < (2 * HZ + 4) / 4; ++c) {
-                    const float4 t = *reinterpret_cast<const float4 *>(cs + rown * W + 4 * lane + 4 * c);
-                    zr[4 * c + 0] = t.x;
-                    zr[4 * c + 1] = t.y;
-                    zr[4 * c + 2] = t.z;
-                    zr[4 * c + 3] = t.w;
+                for (int c = 0; c < (2 * HZ + VZ) / VZ; ++c) ldp<VZ>(cs + rown * W + VZ * lane + VZ * c, zp + NJ * c);
+                // odd-offset pairs (floats 2c+1, 2c+2), needed by odd radii
+                f2_t zo[NZP - 1];
+#pragma unroll
+                for (int c = 0; c < NZP - 1; ++c) {
+                    float a0, a1, b0, b1;
+                    upk2(zp[c], a0, a1);
+                    upk2(zp[c + 1], b0, b1);
+                    zo[c] = pk2(a1, b0);
                 }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) V[s][j] = zr[HZ + j];
-                // in-plane partial P_p = sum_k w_k ((y-k + y+k) + (z-k + z+k) - 4u), as
-                // two fp32x2 lanes (points j, j+1)
-                f2_t pp2[2] = {0ull, 0ull};
+                for (int jp = 0; jp < NJ; ++jp) V[s][jp] = zp[HZ / 2 + jp];
+                // in-plane partial P_p = sum_k w_k ((y-k + y+k) + (z-k + z+k) - 4u), fp32x2
+                f2_t pp2[NJ];
+#pragma unroll
+                for (int jp = 0; jp < NJ; ++jp) pp2[jp] = 0ull;
 #pragma unroll
                 for (int k = 1; k <= R; ++k) {
-                    const float4 m4 = *reinterpret_cast<const float4 *>(cs + (rown - k) * W + HZ + 4 * lane);
-                    const float4 p4 = *reinterpret_cast<const float4 *>(cs + (rown + k) * W + HZ + 4 * lane);
-                    const f2_t ym2[2] = {pk2(m4.x, m4.y), pk2(m4.z, m4.w)};
-                    const f2_t yp2[2] = {pk2(p4.x, p4.y), pk2(p4.z, p4.w)};
+                    f2_t ym2[NJ], yp2[NJ];
+                    ldp<VZ>(cs + (rown - k) * W + HZ + VZ * lane, ym2);
+                    ldp<VZ>(cs + (rown + k) * W + HZ + VZ * lane, yp2);
 #pragma unroll
-                    for (int jp = 0; jp < 2; ++jp) {
-                        const int j = 2 * jp;
-                        const f2_t t = sf_inplane3_x2(ym2[jp], yp2[jp], pk2(zr[HZ + j - k], zr[HZ + j + 1 - k]),
-                                                      pk2(zr[HZ + j + k], zr[HZ + j + 1 + k]),
-                                                      pk2(zr[HZ + j], zr[HZ + j + 1]), M4);
+                    for (int jp = 0; jp < NJ; ++jp) {
+                        const int fm = HZ + 2 * jp - k, fpp = HZ + 2 * jp + k;  // float index of the pair start
+                        const f2_t zm = (k & 1) ? zo[(fm - 1) / 2] : zp[fm / 2];
+                        const f2_t zq = (k & 1) ? zo[(fpp - 1) / 2] : zp[fpp / 2];
+                        const f2_t t = sf_inplane3_x2(ym2[jp], yp2[jp], zm, zq, V[s][jp], M4);
                         pp2[jp] = fma2(Wk[k], t, pp2[jp]);
                     }
                 }
-                float pp[4];
-                upk2(pp2[0], pp[0], pp[1]);
-                upk2(pp2[1], pp[2], pp[3]);
                 const bool outp = (i >= 2 * R);
-                float ov[4], cv[4], bv[4] = {1.f, 1.f, 1.f, 1.f}, sv[4], gv[4], pq[4];
+                f2_t ov[NJ], cv[NJ], bv[NJ], sv[NJ], gv[NJ], pq[NJ];
+                if (!DAMP) {
+#pragma unroll
+                    for (int jp = 0; jp < NJ; ++jp) bv[jp] = ONE2;
+                }
                 if (outp) {
                     const float *pl = reinterpret_cast<const float *>(sb + C::CUR_BYTES);
-                    const float4 o4 = *reinterpret_cast<const float4 *>(pl + po);
-                    const float4 c4 = *reinterpret_cast<const float4 *>(pl + TZ * BY + po);
-                    ov[0] = o4.x; ov[1] = o4.y; ov[2] = o4.z; ov[3] = o4.w;
-                    cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
+                    ldp<VZ>(pl + po, ov);
+                    ldp<VZ>(pl + TZ * BY + po, cv);
                     int nxt = 2;
                     if (DAMP) {
-                        const float4 b4 = *reinterpret_cast<const float4 *>(pl + 2 * TZ * BY + po);
-                        bv[0] = b4.x; bv[1] = b4.y; bv[2] = b4.z; bv[3] = b4.w;
+                        ldp<VZ>(pl + 2 * TZ * BY + po, bv);
                         nxt = 3;
                     }
                     if (MODE == SF_MODE_GRAD) {
-                        const float4 s4 = *reinterpret_cast<const float4 *>(pl + nxt * TZ * BY + po);
-                        const float4 g4 = *reinterpret_cast<const float4 *>(pl + (nxt + 1) * TZ * BY + po);
-                        sv[0] = s4.x; sv[1] = s4.y; sv[2] = s4.z; sv[3] = s4.w;
-                        gv[0] = g4.x; gv[1] = g4.y; gv[2] = g4.z; gv[3] = g4.w;
+                        ldp<VZ>(pl + nxt * TZ * BY + po, sv);
+                        ldp<VZ>(pl + (nxt + 1) * TZ * BY + po, gv);
                     }
                 }
                 // this warp is done with the stage: release it to the producer
@@ -321,102 +359,67 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                     st = 0;
                     ph ^= 1u;
                 }
-                // P ring (thread-private slots): read P_{p-R} (slot pw+1), write P_p (slot pw)
-                int pr = pw + 1;
-                if (pr == PR) pr = 0;
-                if (outp) {
-                    const float4 t = *reinterpret_cast<const float4 *>(myP + pr * (TZ * BY));
-                    pq[0] = t.x; pq[1] = t.y; pq[2] = t.z; pq[3] = t.w;
-                }
-                *reinterpret_cast<float4 *>(myP + pw * (TZ * BY)) = make_float4(pp[0], pp[1], pp[2], pp[3]);
-                pw = pr;
+                // P ring (thread-private slots, R deep): slot pw holds P_{p-R}; read it, then
+                // overwrite it with P_p (same thread, program order)
+                if (outp) ldp<VZ>(myP + pw * (TZ * BY), pq);
+                stp<VZ>(myP + pw * (TZ * BY), pp2);
+                if (++pw == PR) pw = 0;
                 // ---- finish output plane q = p - R from the register queue ----
                 if (outp) {
                     const int sq = (s - R + Q) % Q;  // compile-time after unrolling
                     const int64_t q = qa + (i - 2 * R);
-                    float res[4], gres[4];
+                    f2_t res2[NJ], gres2[NJ];
 #pragma unroll
-                    for (int jp = 0; jp < 2; ++jp) {
-                        const int j = 2 * jp;
-                        const f2_t u = pk2(V[sq][j], V[sq][j + 1]);
+                    for (int jp = 0; jp < NJ; ++jp) {
+                        const f2_t u = V[sq][jp];
                         f2_t X = 0ull;
 #pragma unroll
-                        for (int k = 1; k <= R; ++k) {
-                            const int sm = (sq - k + Q) % Q, sp = (sq + k) % Q;
-                            X = fma2(Wk[k], sf_xterm_x2(pk2(V[sm][j], V[sm][j + 1]), pk2(V[sp][j], V[sp][j + 1]), u, M2),
-                                     X);
-                        }
-                        const f2_t lap = add2(pk2(pq[j], pq[j + 1]), X);
+                        for (int k = 1; k <= R; ++k)
+                            X = fma2(Wk[k], sf_xterm_x2(V[(sq - k + Q) % Q][jp], V[(sq + k) % Q][jp], u, M2), X);
+                        const f2_t lap = add2(pq[jp], X);
                         // out = u + beta (u - old) + c3 lap   (== sf_update per lane)
-                        const f2_t d = fma2(M1, pk2(ov[j], ov[j + 1]), u);
-                        const f2_t b2 = pk2(bv[j], bv[j + 1]), c2 = pk2(cv[j], cv[j + 1]);
-                        const f2_t o = fma2(c2, lap, fma2(b2, d, u));
-                        upk2(o, res[j], res[j + 1]);
+                        const f2_t d = fma2(M1, ov[jp], u);
+                        res2[jp] = fma2(cv[jp], lap, fma2(bv[jp], d, u));
                         if (MODE == SF_MODE_GRAD) {
                             // S = (beta - 1) d + c3 lap ; g -= gscale * snap * S   (== sf_d2 / sf_grad)
-                            const f2_t S2 = fma2(add2(b2, M1), d, mul2(c2, lap));
-                            const f2_t g2 = fma2(NG, mul2(pk2(sv[j], sv[j + 1]), S2), pk2(gv[j], gv[j + 1]));
-                            upk2(g2, gres[j], gres[j + 1]);
+                            const f2_t S2 = fma2(add2(bv[jp], M1), d, mul2(cv[jp], lap));
+                            gres2[jp] = fma2(NG, mul2(sv[jp], S2), gv[jp]);
                         }
                     }
-                    if (cq == (int)q) {
-                        // fused injection: res[j] += sum_e coef_e vals[pt_e]
+                    if (MODE != SF_MODE_GRAD && cq == (int)q) {  // GRAD steps inject standalone
+                        // fused injection, rare path: res[j] += sum_e coef_e vals[pt_e]
                         // (the fp32 operations of k_inject, bitwise)
+                        float res[VZ];
+#pragma unroll
+                        for (int jp = 0; jp < NJ; ++jp) upk2(res2[jp], res[2 * jp], res[2 * jp + 1]);
                         do {
                             const int lj = a.inj_lj[ci];
                             if ((lj >> 2) == lane) {
                                 const int t = a.inj_t[ci];
-                                float d = 0.f;
+                                float dd = 0.f;
 #pragma unroll 1
                                 for (int e = a.inj_rowptr[t]; e < a.inj_rowptr[t + 1]; ++e)
-                                    d = __fmaf_rn(a.inj_coef[e], a.inj_vals[a.inj_pt[e]], d);
+                                    dd = __fmaf_rn(a.inj_coef[e], a.inj_vals[a.inj_pt[e]], dd);
                                 const int j = lj & 3;
-                                res[0] = (j == 0) ? __fadd_rn(res[0], d) : res[0];
-                                res[1] = (j == 1) ? __fadd_rn(res[1], d) : res[1];
-                                res[2] = (j == 2) ? __fadd_rn(res[2], d) : res[2];
-                                res[3] = (j == 3) ? __fadd_rn(res[3], d) : res[3];
-                                if (MODE == SF_MODE_GRAD) {
-                                    gres[0] = (j == 0) ? __fmaf_rn(-a.gscale, __fmul_rn(sv[0], d), gres[0]) : gres[0];
-                                    gres[1] = (j == 1) ? __fmaf_rn(-a.gscale, __fmul_rn(sv[1], d), gres[1]) : gres[1];
-                                    gres[2] = (j == 2) ? __fmaf_rn(-a.gscale, __fmul_rn(sv[2], d), gres[2]) : gres[2];
-                                    gres[3] = (j == 3) ? __fmaf_rn(-a.gscale, __fmul_rn(sv[3], d), gres[3]) : gres[3];
-                                }
+#pragma unroll
+                                for (int jj = 0; jj < VZ; ++jj) res[jj] = (j == jj) ? __fadd_rn(res[jj], dd) : res[jj];
                             }
                             ++ci;
                             cq = ci < ce ? a.inj_q[ci] : QINF;
                         } while (cq == (int)q);
-                    }
-                    if (pq_ == (int)q) {
-                        // fused interpolation of points owned by one lane
-                        do {
-                            if (a.itp_lane[pi] == lane) {
-                                const int kc = a.itp_k[pi];
-                                float acc = 0.f;
-#pragma unroll 1
-                                for (int c = 0; c < kc; ++c) {
-                                    const int j = a.itp_j[4 * pi + c];
-                                    const float v = j == 0 ? res[0] : j == 1 ? res[1] : j == 2 ? res[2] : res[3];
-                                    acc = __fmaf_rn(a.itp_w[4 * pi + c], v, acc);
-                                }
-                                a.itp_out[a.itp_p[pi]] = acc;
-                            }
-                            ++pi;
-                            pq_ = pi < pe ? a.itp_q[pi] : QINF;
-                        } while (pq_ == (int)q);
+#pragma unroll
+                        for (int jp = 0; jp < NJ; ++jp) res2[jp] = pk2(res[2 * jp], res[2 * jp + 1]);
                     }
                     if (active) {
                         const int64_t off = q * plane + rowoff;
-                        stg4(a.out + off, make_float4(res[0], res[1], res[2], res[3]));
-                        if (MODE == SF_MODE_SAVE)
-                            stg4(a.snap_out + off, make_float4(res[0], res[1], res[2], res[3]));
-                        if (MODE == SF_MODE_GRAD)
-                            stg4(a.grad + off, make_float4(gres[0], gres[1], gres[2], gres[3]));
+                        stp<VZ>(a.out + off, res2);
+                        if (MODE == SF_MODE_SAVE) stp<VZ>(a.snap_out + off, res2);
+                        if (MODE == SF_MODE_GRAD) stp<VZ>(a.grad + off, gres2);
                     }
                 }
             }
         }
     }
-
 }
 
 }  // namespace sftma

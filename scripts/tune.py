@@ -43,8 +43,6 @@ def main():
         res = torch.randn((p.nt, p.rec_coords.shape[0]), device="cuda")
     for by, ch in itertools.product([int(x) for x in args.by.split(",")],
                                     [int(x) for x in args.chunks.split(",")]):
-        if by == 16 and p.space_order > 8:
-            continue
         try:
             prop.set_tuning(2, by, ch)
         except sf.SfError:
