@@ -177,6 +177,8 @@ def run_ours(args):
     prop = sf.Propagator(m_d, eta_d, shape=gshape, h=p.h, space_order=p.space_order, nt=p.nt,
                          dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords,
                          comm=comm, rank=rank, nranks=world)
+    if args.split:
+        prop.set_option(2, 1)
     wav = dev(p.wavelet)
     u = prop.zeros_state()
     rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
@@ -265,6 +267,7 @@ def run_ours(args):
                              "4-5 fields streamed per update)" if npts_local * 4 > 126e6 else
                              "grid smaller than L2 (configs[0]: launch-bound toy)",
                        "propagations_per_step": passes,
+                       "schedule": "split (boundary planes, then interior)" if (args.split or world > 1) else "single launch per step",
                        "kernel_tuning": tuning},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
@@ -385,6 +388,9 @@ def main():
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4],
                     help="BASELINE configs[i] workload (default 1: the metric's headline config)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--split", action="store_true",
+                    help="1 GPU: run the slab schedule (boundary planes first, interior second) "
+                         "to measure its cost without communication")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-steps-nt", type=int, default=6,

@@ -26,7 +26,7 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
     const int64_t planes = a.xb - a.xa;
     const int nchunks = L.chunks > 0 ? L.chunks : 1;
     const int chunk = (int)((planes + nchunks - 1) / nchunks);
-    const int nch = (int)((planes + chunk - 1) / chunk);
+    const int nch = (int)((planes + chunk - 1) / chunk) + (int)((a.xb2 - a.xa2 + chunk - 1) / chunk);
     dim3 grid((unsigned)((a.n2 + C::TZ - 1) / C::TZ), (unsigned)((a.n1 + BY - 1) / BY), (unsigned)nch);
     dim3 block(32, BY + 1);  // BY consumer warps + 1 TMA producer warp
     kern<<<grid, block, C::SMEM, st>>>(L.maps->cur, L.maps->old, L.maps->c3, L.maps->beta,
@@ -37,7 +37,7 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 template <int MODE>
 cudaError_t launch_generic(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    const int64_t planes = a.xb - a.xa;
+    const int64_t planes = (a.xb - a.xa) + (a.xb2 - a.xa2);
     dim3 block(32, 8);
     if (L.ndim == 3) {
         dim3 grid((unsigned)((a.n2 + 31) / 32), (unsigned)((a.n1 + 7) / 8), (unsigned)planes);

@@ -20,6 +20,7 @@
 #include "sparse.cuh"
 
 #define SF_VERSION 1
+#define SF_SIDE_MIN_POINTS (1 << 22)  // grids below this record in stream order
 
 static thread_local char g_err[1024] = "";
 
@@ -236,6 +237,7 @@ struct StepBufs {
     SfSparse *itp;         // point set interpolated from the new level (or NULL)
     float *itp_row;        // its record row for the new level ([npoint])
     int64_t xa = 0, xb = 0;  // planes to compute (xa == xb: the handle's full range)
+    int64_t xa2 = 0, xb2 = 0;  // optional second range in the same launch
 };
 
 template <class T>
@@ -423,6 +425,8 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     }
     a.xa = b.xa < b.xb ? b.xa : h->xa;
     a.xb = b.xa < b.xb ? b.xb : h->xb;
+    a.xa2 = b.xa2;
+    a.xb2 = b.xb2;
     a.w = h->w;
     a.l2_prefetch = h->l2_prefetch;
 
@@ -722,6 +726,8 @@ extern "C" void sf_destroy(sf_handle *h)
         if (h->ev_itp[k]) cudaEventDestroy(h->ev_itp[k]);
     if (h->side) cudaStreamDestroy(h->side);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+    if (h->hi_stream) cudaStreamDestroy(h->hi_stream);
+    if (h->ev_pre) cudaEventDestroy(h->ev_pre);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
     if (h->ev_xch) cudaEventDestroy(h->ev_xch);
     delete h;
@@ -784,6 +790,12 @@ static sf_status create_common(const sf_desc *d, sf_handle *h)
     if ((s = build_sparse(h, d->nrec, d->rec_coords, d->m, h->rec, "receiver"))) return s;
     SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+    {
+        int lo = 0, hi = 0;
+        SF_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SF_CUDA_TRY(cudaStreamCreateWithPriority(&h->hi_stream, cudaStreamNonBlocking, hi));
+    }
+    SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_pre, cudaEventDisableTiming));
     SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming));
     SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_xch, cudaEventDisableTiming));
     h->split = h->nranks > 1;
@@ -1085,22 +1097,24 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
         if (h->nranks > 1) return sf_comm_halo_exchange(h, b.out, st);
         return SF_OK;
     }
+    // boundary planes at both ends in ONE launch on the high-priority stream, overlapping
+    // the interior launch on `st`; then the exchange on the comm stream
     bool f2 = false, fi2 = false;
-    StepBufs bl = b, br = b, bi = b;
-    bl.xa = xa, bl.xb = xa + r;
-    br.xa = xb - r, br.xb = xb;
+    StepBufs bb = b, bi = b;
+    bb.xa = xa, bb.xb = xa + r, bb.xa2 = xb - r, bb.xb2 = xb;
     bi.xa = xa + r, bi.xb = xb - r;
-    if ((s = launch_step(h, bl, mode, st, &fused, fused_itp))) return s;
-    if ((s = launch_step(h, br, mode, st, &f2, &fi2))) return s;
+    SF_CUDA_TRY(cudaEventRecord(h->ev_pre, st));
+    SF_CUDA_TRY(cudaStreamWaitEvent(h->hi_stream, h->ev_pre, 0));
+    if ((s = launch_step(h, bb, mode, h->hi_stream, &fused, fused_itp))) return s;
     const bool need_inj = !fused && b.inj && b.inj->ntgt > 0 && b.inj_vals;
     if (need_inj) {
         if ((s = ensure_split_lists(h, *b.inj))) return s;
         if ((s = launch_inject_list(h, *b.inj, b.out, b.inj_vals, b.inj->jl_bnd, b.inj->n_bnd, snap_patch,
-                                    grad_snap, b.grad, b.gscale, st)))
+                                    grad_snap, b.grad, b.gscale, h->hi_stream)))
             return s;
     }
+    SF_CUDA_TRY(cudaEventRecord(h->ev_bnd, h->hi_stream));
     if (h->nranks > 1) {
-        SF_CUDA_TRY(cudaEventRecord(h->ev_bnd, st));
         SF_CUDA_TRY(cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
         if ((s = sf_comm_halo_exchange(h, b.out, h->comm_stream))) return s;
         SF_CUDA_TRY(cudaEventRecord(h->ev_xch, h->comm_stream));
@@ -1109,7 +1123,7 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
     if (need_inj && (s = launch_inject_list(h, *b.inj, b.out, b.inj_vals, b.inj->jl_int, b.inj->n_int, snap_patch,
                                             grad_snap, b.grad, b.gscale, st)))
         return s;
-    if (h->nranks > 1) SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_xch, 0));
+    SF_CUDA_TRY(cudaStreamWaitEvent(st, h->nranks > 1 ? h->ev_xch : h->ev_bnd, 0));
     return SF_OK;
 }
 
@@ -1120,6 +1134,11 @@ static sf_status side_interp(sf_handle *h, SfSparse &sp, bool fused_itp, const f
                              int level, cudaStream_t st)
 {
     if (!row || sp.np == 0 || (fused_itp && sp.itiles.nleft == 0)) return SF_OK;
+    if (h->N < SF_SIDE_MIN_POINTS) {
+        // small grids are launch-bound: the cross-stream events would cost more than the
+        // overlap buys -> interpolate in stream order
+        return fused_itp ? launch_interp_left(h, sp, lvl, row, st) : launch_interp(h, sp, lvl, row, st);
+    }
     SF_CUDA_TRY(cudaEventRecord(h->ev_ready, st));
     SF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_ready, 0));
     sf_status s = fused_itp ? launch_interp_left(h, sp, lvl, row, h->side) : launch_interp(h, sp, lvl, row, h->side);

@@ -96,8 +96,8 @@ struct sf_handle {
     bool itp_pending[2] = {false, false};
     // boundary-first split launches (always in slab mode; optional on one GPU)
     bool split = false;
-    cudaStream_t comm_stream = nullptr;
-    cudaEvent_t ev_bnd = nullptr, ev_xch = nullptr;
+    cudaStream_t comm_stream = nullptr, hi_stream = nullptr;
+    cudaEvent_t ev_pre = nullptr, ev_bnd = nullptr, ev_xch = nullptr;
     int fuse_max = 256;
 };
 

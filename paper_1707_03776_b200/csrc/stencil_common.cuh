@@ -122,6 +122,7 @@ struct SfStepArgs {
     float gscale;          // GRAD: k / dt^2
     int64_t n0b, n1, n2;   // buffer extents (n0b includes slab halo planes)
     int64_t xa, xb;        // planes [xa, xb) of the buffer to compute
+    int64_t xa2, xb2;      // optional second range [xa2, xb2) in the same launch (xa2 == xb2: none)
     SfWeights w;
     int l2_prefetch;       // TMA kernel: L2 prefetch distance in planes (0 = off)
     // Fused sparse work of the TMA kernel (NULL *_beg = none).  Lists are per consumer

@@ -14,8 +14,9 @@ k_generic3d(SfStepArgs a)
 {
     const int64_t z = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
-    const int64_t x = a.xa + blockIdx.z;
-    if (z >= a.n2 || y >= a.n1 || x >= a.xb) return;
+    const int64_t n1st = a.xb - a.xa;
+    const int64_t x = (blockIdx.z < n1st) ? a.xa + blockIdx.z : a.xa2 + (blockIdx.z - n1st);
+    if (z >= a.n2 || y >= a.n1 || (blockIdx.z < n1st ? x >= a.xb : x >= a.xb2)) return;
     const int64_t sx = a.n1 * a.n2, sy = a.n2;
     const int64_t idx = (x * a.n1 + y) * a.n2 + z;
     const float *__restrict__ c = a.cur;
@@ -54,8 +55,10 @@ __global__ void __launch_bounds__(256)
 k_generic2d(SfStepArgs a)
 {
     const int64_t z = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t x = a.xa + (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
-    if (z >= a.n2 || x >= a.xb) return;
+    const int64_t row = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+    const int64_t n1st = a.xb - a.xa;
+    const int64_t x = row < n1st ? a.xa + row : a.xa2 + (row - n1st);
+    if (z >= a.n2 || (row < n1st ? x >= a.xb : x >= a.xb2)) return;
     const int64_t sx = a.n2;
     const int64_t idx = x * a.n2 + z;
     const float *__restrict__ c = a.cur;

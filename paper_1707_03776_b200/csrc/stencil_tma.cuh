@@ -188,8 +188,18 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 
     const int lane = threadIdx.x, wy = threadIdx.y;
     const int z0 = blockIdx.x * TZ, y0 = blockIdx.y * BY;
-    const int64_t qa = a.xa + (int64_t)blockIdx.z * chunk;
-    const int64_t qb = min(qa + (int64_t)chunk, a.xb);
+    // chunk -> planes [qa, qb): chunks of the first range, then of the optional second
+    int64_t zc = blockIdx.z, ra = a.xa, rb = a.xb;
+    {
+        const int64_t nch1 = (a.xb - a.xa + chunk - 1) / chunk;
+        if (zc >= nch1) {
+            zc -= nch1;
+            ra = a.xa2;
+            rb = a.xb2;
+        }
+    }
+    const int64_t qa = ra + zc * chunk;
+    const int64_t qb = min(qa + (int64_t)chunk, rb);
     if (qa >= qb) return;  // uniform over the CTA
     const int NP = (int)(qb - qa) + 2 * R;
 
