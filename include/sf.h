@@ -145,18 +145,21 @@ SF_API sf_status sf_get_profile_detail(sf_handle *h, double *ms_by_kind, long lo
                                        int reset);
 
 /* Tuning: kernel variant (0 auto, 1 generic thread-per-point, 2 TMA 2.5D streaming),
- * warps per CTA along y (0 auto, 8 or 16) and x-chunks per column (0 auto). */
-SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int by, int chunks);
+ * TMA rows per thread `vy` (0 auto = 2: 14-row tiles; 1: 7-row tiles) and the number of
+ * persistent TMA CTAs `ctas` (0 auto = one per SM; the (tile, plane) work is split into
+ * `ctas` equal runs; every setting gives the same bits).  SF_ERR_INVALID_ARG for other
+ * values. */
+SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
 /* Options (sf_set_option): */
-#define SF_OPT_L2_PREFETCH 1   /* TMA kernel: L2 prefetch distance in planes (default 4, 0 = off)   */
+#define SF_OPT_L2_PREFETCH 1   /* TMA kernel: L2 prefetch distance in planes (default 8, 0 = off)   */
 #define SF_OPT_SPLIT 2         /* 1: boundary planes first, then interior (always on in slab mode;
                                   on one GPU it only reorders work: results are bitwise identical) */
 #define SF_OPT_FUSE_MAX 3      /* largest point set injected / interpolated inside the stencil
                                   kernel (default 256); larger sets use standalone kernels       */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 
-/* Which variant / by / chunks the next launch will use (after auto selection). */
-SF_API sf_status sf_get_tuning(const sf_handle *h, int *variant, int *by, int *chunks);
+/* Which variant / vy / ctas the next launch will use (after auto selection). */
+SF_API sf_status sf_get_tuning(const sf_handle *h, int *variant, int *vy, int *ctas);
 
 /* ---- multi-GPU (slab decomposition along axis 0; one process per GPU, NCCL) ---- */
 

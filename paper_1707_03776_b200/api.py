@@ -151,8 +151,10 @@ class Propagator:
     def zeros_state(self):
         return torch.zeros((2,) + self.local_shape, device=self.device, dtype=torch.float32)
 
-    def set_tuning(self, variant: int = 0, by: int = 0, chunks: int = 0):
-        check(lib().sf_set_tuning(self._h, variant, by, chunks))
+    def set_tuning(self, variant: int = 0, vy: int = 0, ctas: int = 0):
+        """sf_set_tuning: variant (0 auto, 1 generic, 2 TMA), rows per thread (0 auto, 1, 2),
+        persistent CTAs (0 = one per SM)."""
+        check(lib().sf_set_tuning(self._h, variant, vy, ctas))
 
     def set_option(self, option: int, value: int):
         """sf_set_option: 1 L2 prefetch distance, 2 split boundary launches, 3 fuse-max points."""
@@ -161,7 +163,7 @@ class Propagator:
     def tuning(self):
         v, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         check(lib().sf_get_tuning(self._h, ctypes.byref(v), ctypes.byref(b), ctypes.byref(c)))
-        return {"variant": v.value, "by": b.value, "chunks": c.value}
+        return {"variant": v.value, "vy": b.value, "ctas": c.value}
 
     def set_profiling(self, on: bool = True):
         check(lib().sf_set_profiling(self._h, 1 if on else 0))

@@ -1,5 +1,6 @@
 // inst_body.cuh -- instantiates every stencil-step kernel for one radius SF_R
 // (included by inst_r<R>.cu).  Dispatch: variant x (by, damp, mode).
+#include <algorithm>
 #include "launch.cuh"
 #include "stencil_generic.cuh"
 #include "stencil_tma.cuh"
@@ -12,25 +13,41 @@
 
 namespace {
 
-template <int BY, int VZ, bool DAMP, int MODE>
+template <int VY, bool DAMP, int MODE>
 cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    using C = sftma::Cfg<SF_R, BY, VZ, DAMP, MODE>;
-    auto kern = sftma::k_tma3d<SF_R, BY, VZ, DAMP, MODE>;
+    using C = sftma::Cfg<SF_R, VY, DAMP, MODE>;
+    auto kern = sftma::k_tma3d<SF_R, VY, DAMP, MODE>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int64_t planes = a.xb - a.xa;
-    const int nchunks = L.chunks > 0 ? L.chunks : 1;
-    const int chunk = (int)((planes + nchunks - 1) / nchunks);
-    const int nch = (int)((planes + chunk - 1) / chunk) + (int)((a.xb2 - a.xa2 + chunk - 1) / chunk);
-    dim3 grid((unsigned)((a.n2 + C::TZ - 1) / C::TZ), (unsigned)((a.n1 + BY - 1) / BY), (unsigned)nch);
-    dim3 block(32, BY + 1);  // BY consumer warps + 1 TMA producer warp
-    kern<<<grid, block, C::SMEM, st>>>(L.maps->cur, L.maps->old, L.maps->c3, L.maps->beta,
-                                       L.maps->snap, L.maps->grad, a, L.snap_slot, chunk);
+    // persistent grid: (tile, x-chunk) items, at most one CTA per SM (shared memory admits
+    // one), items dealt round-robin.  The chunk count minimises rounds x (chunk + 2r): each
+    // item re-reads 2r warm-up planes of u^n.  L.ctas overrides the CTA count.
+    const int64_t PT = (a.xb - a.xa) + (a.xb2 - a.xa2);
+    const int64_t tiles = ((a.n2 + C::TZ - 1) / C::TZ) * ((a.n1 + C::BY - 1) / C::BY);
+    if (PT <= 0 || tiles <= 0) return cudaSuccess;
+    const int64_t slots = L.ctas > 0 ? L.ctas : L.sms;
+    double best = 1e300;
+    int64_t chunk = PT, nch = 1;
+    for (int64_t c = 1; c <= std::min<int64_t>(PT, 256); ++c) {
+        const int64_t ch = (PT + c - 1) / c, ce = (PT + ch - 1) / ch;
+        const int64_t items = tiles * ce, g = std::min(items, slots);
+        const double t = (double)((items + g - 1) / g) * (double)(ch + 2 * SF_R);
+        if (t < best - 1e-9) {
+            best = t;
+            chunk = ch;
+            nch = ce;
+        }
+    }
+    const int64_t g = std::min(tiles * nch, slots);
+    dim3 block(32, C::NW + 1);  // NW consumer warps + 1 TMA producer warp
+    kern<<<(unsigned)g, block, C::SMEM, st>>>(L.maps->cur, L.maps->old, L.maps->c3, L.maps->beta,
+                                              L.maps->snap, L.maps->grad, a, L.snap_slot, (int)chunk,
+                                              (int)nch);
     return cudaGetLastError();
 }
 
@@ -49,48 +66,42 @@ cudaError_t launch_generic(const SfLaunch &L, const SfStepArgs &a, cudaStream_t 
     return cudaGetLastError();
 }
 
-template <int BY, int VZ>
-cudaError_t launch_tma_by(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
+template <int VY>
+cudaError_t launch_tma_vy(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     if (L.damp) {
         switch (L.mode) {
-        case SF_MODE_PLAIN: return launch_tma<BY, VZ, true, SF_MODE_PLAIN>(L, a, st);
-        case SF_MODE_SAVE: return launch_tma<BY, VZ, true, SF_MODE_SAVE>(L, a, st);
-        default: return launch_tma<BY, VZ, true, SF_MODE_GRAD>(L, a, st);
+        case SF_MODE_PLAIN: return launch_tma<VY, true, SF_MODE_PLAIN>(L, a, st);
+        case SF_MODE_SAVE: return launch_tma<VY, true, SF_MODE_SAVE>(L, a, st);
+        default: return launch_tma<VY, true, SF_MODE_GRAD>(L, a, st);
         }
     }
     switch (L.mode) {
-    case SF_MODE_PLAIN: return launch_tma<BY, VZ, false, SF_MODE_PLAIN>(L, a, st);
-    case SF_MODE_SAVE: return launch_tma<BY, VZ, false, SF_MODE_SAVE>(L, a, st);
-    default: return launch_tma<BY, VZ, false, SF_MODE_GRAD>(L, a, st);
+    case SF_MODE_PLAIN: return launch_tma<VY, false, SF_MODE_PLAIN>(L, a, st);
+    case SF_MODE_SAVE: return launch_tma<VY, false, SF_MODE_SAVE>(L, a, st);
+    default: return launch_tma<VY, false, SF_MODE_GRAD>(L, a, st);
     }
 }
 
-template <int BY, int VZ, bool DAMP, int MODE>
-int smem_of() { return sftma::Cfg<SF_R, BY, VZ, DAMP, MODE>::SMEM; }
+template <int VY, bool DAMP, int MODE>
+int smem_of() { return sftma::Cfg<SF_R, VY, DAMP, MODE>::SMEM; }
 
-template <int BY, int VZ>
-int smem_by(int damp, int mode)
+template <int VY>
+int smem_vy(int damp, int mode)
 {
-    if (damp) return mode == 0 ? smem_of<BY, VZ, true, 0>() : mode == 1 ? smem_of<BY, VZ, true, 1>() : smem_of<BY, VZ, true, 2>();
-    return mode == 0 ? smem_of<BY, VZ, false, 0>() : mode == 1 ? smem_of<BY, VZ, false, 1>() : smem_of<BY, VZ, false, 2>();
+    if (damp) return mode == 0 ? smem_of<VY, true, 0>() : mode == 1 ? smem_of<VY, true, 1>() : smem_of<VY, true, 2>();
+    return mode == 0 ? smem_of<VY, false, 0>() : mode == 1 ? smem_of<VY, false, 1>() : smem_of<VY, false, 2>();
 }
 
 }  // namespace
 
-// Tile shapes: r <= 4: BY = 16 or 8 warps of 4 z per lane (128-column tiles); r >= 5:
-// BY = 8 with 4 z per lane, or BY = 16 with 2 z per lane (64-column tiles) -- the
-// (2r+1)-deep register queues must fit the 96-register budget of 17 warps.
+// Tile shapes (stencil_tma.cuh Geo): vy = 2 -> two rows per thread (14-row tiles; 128
+// columns for r <= 4, 64 for r >= 5); vy = 1 -> one row per thread, 7 x 128 tiles.
 cudaError_t SF_CAT(sf_launch_step_r, SF_R)(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     if (L.variant == SF_VAR_TMA) {
-#if SF_R <= 4
-        if (L.by == 16) return launch_tma_by<16, 4>(L, a, st);
-        return launch_tma_by<8, 4>(L, a, st);
-#else
-        if (L.by == 16) return launch_tma_by<16, 2>(L, a, st);
-        return launch_tma_by<8, 4>(L, a, st);
-#endif
+        if (L.vy == 1) return launch_tma_vy<1>(L, a, st);
+        return launch_tma_vy<2>(L, a, st);
     }
     switch (L.mode) {
     case SF_MODE_PLAIN: return launch_generic<SF_MODE_PLAIN>(L, a, st);
@@ -99,13 +110,8 @@ cudaError_t SF_CAT(sf_launch_step_r, SF_R)(const SfLaunch &L, const SfStepArgs &
     }
 }
 
-int SF_CAT(sf_tma_smem_r, SF_R)(int by, int damp, int mode)
+int SF_CAT(sf_tma_smem_r, SF_R)(int vy, int damp, int mode)
 {
-#if SF_R <= 4
-    if (by == 16) return smem_by<16, 4>(damp, mode);
-    return smem_by<8, 4>(damp, mode);
-#else
-    if (by == 16) return smem_by<16, 2>(damp, mode);
-    return smem_by<8, 4>(damp, mode);
-#endif
+    if (vy == 1) return smem_vy<1>(damp, mode);
+    return smem_vy<2>(damp, mode);
 }

@@ -14,16 +14,17 @@ struct SfTmaMaps {
 struct SfLaunch {
     int ndim;
     int variant;      // SF_VAR_GENERIC or SF_VAR_TMA (resolved)
-    int by;           // TMA: warps (y rows) per CTA, 8 or 16
-    int chunks;       // TMA: x-chunks per (y, z) tile column
+    int vy;           // TMA: rows per thread, 2 (14-row tiles) or 1 (7-row tiles)
+    int ctas;         // TMA: persistent CTAs (0 = one per SM)
+    int sms;          // multiprocessors of the device
     int damp;         // beta array present
     int mode;         // SfMode
     int snap_slot;    // GRAD: snapshot slot for the 4D snapshot tensor map
     const SfTmaMaps *maps;
 };
 
-// shared-memory bytes of the TMA kernel for (r, by, damp, mode); 0 if unsupported
-int sf_tma_smem_bytes(int r, int by, int damp, int mode);
+// shared-memory bytes of the TMA kernel for (r, vy, damp, mode); 0 if unsupported
+int sf_tma_smem_bytes(int r, int vy, int damp, int mode);
 
 #define SF_DECL_LAUNCH(R) \
     cudaError_t sf_launch_step_r##R(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st);
@@ -37,7 +38,7 @@ SF_DECL_LAUNCH(7)
 SF_DECL_LAUNCH(8)
 #undef SF_DECL_LAUNCH
 
-#define SF_DECL_SMEM(R) int sf_tma_smem_r##R(int by, int damp, int mode);
+#define SF_DECL_SMEM(R) int sf_tma_smem_r##R(int vy, int damp, int mode);
 SF_DECL_SMEM(1)
 SF_DECL_SMEM(2)
 SF_DECL_SMEM(3)

@@ -119,17 +119,17 @@ static cudaError_t launch_step_r(int r, const SfLaunch &L, const SfStepArgs &a, 
     }
 }
 
-int sf_tma_smem_bytes(int r, int by, int damp, int mode)
+int sf_tma_smem_bytes(int r, int vy, int damp, int mode)
 {
     switch (r) {
-    case 1: return sf_tma_smem_r1(by, damp, mode);
-    case 2: return sf_tma_smem_r2(by, damp, mode);
-    case 3: return sf_tma_smem_r3(by, damp, mode);
-    case 4: return sf_tma_smem_r4(by, damp, mode);
-    case 5: return sf_tma_smem_r5(by, damp, mode);
-    case 6: return sf_tma_smem_r6(by, damp, mode);
-    case 7: return sf_tma_smem_r7(by, damp, mode);
-    default: return sf_tma_smem_r8(by, damp, mode);
+    case 1: return sf_tma_smem_r1(vy, damp, mode);
+    case 2: return sf_tma_smem_r2(vy, damp, mode);
+    case 3: return sf_tma_smem_r3(vy, damp, mode);
+    case 4: return sf_tma_smem_r4(vy, damp, mode);
+    case 5: return sf_tma_smem_r5(vy, damp, mode);
+    case 6: return sf_tma_smem_r6(vy, damp, mode);
+    case 7: return sf_tma_smem_r7(vy, damp, mode);
+    default: return sf_tma_smem_r8(vy, damp, mode);
     }
 }
 
@@ -146,48 +146,20 @@ static int resolve_variant(const sf_handle *h)
     return SF_VAR_GENERIC;
 }
 
-static int resolve_by(const sf_handle *h)
+static int resolve_vy(const sf_handle *h)
 {
-    if (h->by == 8 || h->by == 16) return h->by;
-    return 16;
+    return h->vy == 1 ? 1 : 2;
 }
 
-// z points per lane of the TMA kernel: 4 (128-column tiles), or 2 (64-column tiles) for
-// r >= 5 with 16 warps (register budget; inst_body.cuh)
-static int tile_vz(const sf_handle *h, int by) { return (h->r >= 5 && by == 16) ? 2 : 4; }
-static int tile_tz(const sf_handle *h, int by) { return 32 * tile_vz(h, by); }
+// TMA kernel tile geometry (stencil_tma.cuh Geo): VY rows per thread (tuning `vy`, auto
+// 2), 7 consumer warps -> BY = 7 VY tile rows; 4 z per lane -> 128-column tiles.
+static const int TILE_NW = 7;
+static int tile_vz(const sf_handle *, int) { return 4; }
+static int tile_tz(const sf_handle *h, int vy) { return 32 * tile_vz(h, vy); }
+static int tile_by(int vy) { return TILE_NW * vy; }
 
-// x-chunks per tile column.  Measured on B200 (scripts/tune.py, profiles/): with the
-// TMA pipeline one partial wave of CTAs already saturates HBM, so when the (y, z)
-// tiles fit in one wave we take the largest chunk count that keeps a single wave
-// (fewest 2r warm-up planes); otherwise balance whole waves against the warm-up
-// planes each chunk re-reads (SURVEY H2 model).
-static int resolve_chunks(const sf_handle *h, int by, int64_t planes)
-{
-    if (planes <= 0) planes = h->xb - h->xa;
-    if (h->chunks > 0) return (int)std::min<int64_t>(h->chunks, std::max<int64_t>(1, planes));
-    const int tz = tile_tz(h, by);
-    const int64_t tiles = ((h->nb[2] + tz - 1) / tz) * ((h->nb[1] + by - 1) / by);
-    const int sms = h->sms;
-    const int per_sm = (by == 8 && h->r <= 4) ? 2 : 1;
-    const int64_t slots = (int64_t)sms * per_sm;
-    const int64_t cmax = std::max<int64_t>(1, planes / std::max(2 * h->r, 8));
-    if (tiles <= slots) return (int)std::max<int64_t>(1, std::min<int64_t>(cmax, slots / tiles));
-    double best = 1e300;
-    int bestc = 1;
-    for (int64_t c = 1; c <= cmax && c <= 4096; ++c) {
-        const int64_t chunk = (planes + c - 1) / c;
-        const int64_t nch = (planes + chunk - 1) / chunk;
-        const int64_t ctas = tiles * nch;
-        const int64_t waves = (ctas + slots - 1) / slots;
-        const double t = (double)waves * ((double)chunk + 1.0 * h->r);
-        if (t < best - 1e-9) {
-            best = t;
-            bestc = (int)c;
-        }
-    }
-    return bestc;
-}
+// persistent CTAs of the TMA kernel (0 = one per SM)
+static int resolve_ctas(const sf_handle *h) { return h->ctas > 0 ? h->ctas : h->sms; }
 
 // ---- profiling: CUDA events around every launch, grouped by kind (stream-ordered)
 enum { PK_STENCIL = 0, PK_INJECT = 1, PK_INTERP = 2, PK_OTHER = 3, PK_N = 4 };
@@ -272,95 +244,26 @@ static void free_inj(SfInjTiles &T)
     T = SfInjTiles{};
 }
 
-// where grid offset `off` lives in the TMA kernel: (tile * by + warp, plane, lane, j)
+// where grid offset `off` lives in the TMA kernel: (tile * NW + warp, plane, lane, row of
+// the warp jy, z in the lane jz)
 struct TileLoc {
-    int wl, q, lane, j;
+    int wl, q, lane, jy, j;
 };
-static TileLoc tile_loc(const sf_handle *h, int by, int64_t off)
+static TileLoc tile_loc(const sf_handle *h, int vy, int64_t off)
 {
     const int64_t n1 = h->nb[1], n2 = h->nb[2];
-    const int tz = tile_tz(h, by), vz = tile_vz(h, by);
+    const int tz = tile_tz(h, vy), vz = tile_vz(h, vy), by = tile_by(vy);
     const int64_t ntz = (n2 + tz - 1) / tz;
     const int64_t x = off / (n1 * n2), y = (off / n2) % n1, z = off % n2;
     const int64_t tile = (y / by) * ntz + z / tz;
-    return {(int)(tile * by + y % by), (int)x, (int)((z % tz) / vz), (int)(z % vz)};
+    return {(int)(tile * TILE_NW + (y % by) / vy), (int)x, (int)((z % tz) / vz), (int)((y % by) % vy),
+            (int)(z % vz)};
 }
 
-static int64_t n_warp_lists(const sf_handle *h, int by)
+static int64_t n_warp_lists(const sf_handle *h, int vy)
 {
-    const int tz = tile_tz(h, by);
-    return ((h->nb[2] + tz - 1) / tz) * ((h->nb[1] + by - 1) / by) * by;
-}
-
-// Interpolation points whose nonzero corners are all points of one lane (same tile,
-// warp row, plane and float4 group) are interpolated inside the TMA kernel; the rest
-// stay in `left` for k_interp_list.
-static sf_status ensure_itp_tiles(sf_handle *h, SfSparse &sp, int by)
-{
-    SfItpTiles &T = sp.itiles;
-    if (T.by == by) return SF_OK;
-    free_itp(T);
-    const int64_t nl = n_warp_lists(h, by);
-    struct E {
-        int wl, q, lane, p, k;
-        int j[4];
-        float w[4];
-    };
-    std::vector<E> es;
-    std::vector<int> left;
-    for (int p = 0; p < sp.np; ++p) {
-        E e{};
-        e.p = p;
-        bool ok = true;
-        for (int c = 0; c < sp.nc; ++c) {
-            const float w = sp.h_iw[(size_t)p * sp.nc + c];
-            if (w == 0.0f) continue;
-            const TileLoc L = tile_loc(h, by, sp.h_iidx[(size_t)p * sp.nc + c]);
-            if (e.k > 0 && (L.wl != e.wl || L.q != e.q || L.lane != e.lane)) {
-                ok = false;
-                break;
-            }
-            e.wl = L.wl;
-            e.q = L.q;
-            e.lane = L.lane;
-            e.j[e.k] = L.j;
-            e.w[e.k] = w;
-            e.k++;
-        }
-        if (!ok || e.k == 0) left.push_back(p);
-        else es.push_back(e);
-    }
-    std::stable_sort(es.begin(), es.end(), [](const E &a, const E &b) {
-        return std::tie(a.wl, a.q, a.lane, a.p) < std::tie(b.wl, b.q, b.lane, b.p);
-    });
-    std::vector<int> beg(nl + 1, 0), q, lane, k, j, pp;
-    std::vector<float> w;
-    for (const E &e : es) beg[e.wl + 1]++;
-    for (int64_t i = 0; i < nl; ++i) beg[i + 1] += beg[i];
-    for (const E &e : es) {
-        q.push_back(e.q);
-        lane.push_back(e.lane);
-        k.push_back(e.k);
-        pp.push_back(e.p);
-        for (int c = 0; c < 4; ++c) {
-            j.push_back(c < e.k ? e.j[c] : 0);
-            w.push_back(c < e.k ? e.w[c] : 0.0f);
-        }
-    }
-    sf_status s;
-    if ((s = upload(&T.beg, beg))) return s;
-    if (!es.empty()) {
-        if ((s = upload(&T.q, q))) return s;
-        if ((s = upload(&T.lane, lane))) return s;
-        if ((s = upload(&T.k, k))) return s;
-        if ((s = upload(&T.j, j))) return s;
-        if ((s = upload(&T.p, pp))) return s;
-        if ((s = upload(&T.w, w))) return s;
-    }
-    if (!left.empty() && (s = upload(&T.left, left))) return s;
-    T.nleft = (int)left.size();
-    T.by = by;
-    return SF_OK;
+    const int tz = tile_tz(h, vy), by = tile_by(vy);
+    return ((h->nb[2] + tz - 1) / tz) * ((h->nb[1] + by - 1) / by) * TILE_NW;
 }
 
 // Per-(tile, warp) lists of the injection targets for the TMA kernel's fused injection.
@@ -376,7 +279,7 @@ static sf_status ensure_inj_tiles(sf_handle *h, SfSparse &sp, int by)
     std::vector<E> es;
     for (size_t t = 0; t < sp.h_tgt.size(); ++t) {
         const TileLoc L = tile_loc(h, by, sp.h_tgt[t]);
-        es.push_back({L.wl, L.q, L.lane * 4 + L.j, (int)t});
+        es.push_back({L.wl, L.q, (L.jy * 32 + L.lane) * 4 + L.j, (int)t});
     }
     std::sort(es.begin(), es.end(), [](const E &a, const E &b) {
         return std::tie(a.wl, a.q, a.lj) < std::tie(b.wl, b.q, b.lj);
@@ -433,8 +336,9 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     SfLaunch L{};
     L.ndim = h->ndim;
     L.variant = resolve_variant(h);
-    L.by = resolve_by(h);
-    L.chunks = resolve_chunks(h, L.by, a.xb - a.xa);
+    L.vy = resolve_vy(h);
+    L.ctas = resolve_ctas(h);
+    L.sms = h->sms;
     L.damp = h->beta != nullptr;
     L.mode = mode;
     L.snap_slot = b.snap_slot;
@@ -442,10 +346,10 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     memset(&maps, 0, sizeof maps);
     if (L.variant == SF_VAR_TMA) {
         const int HZ = ((h->r + 3) / 4) * 4;
-        const int TZ = tile_tz(h, L.by);
+        const int TZ = tile_tz(h, L.vy), BY = tile_by(L.vy);
         const int64_t d3[3] = {h->nb[2], h->nb[1], h->nb[0]};
-        const uint32_t bcur[3] = {(uint32_t)(TZ + 2 * HZ), (uint32_t)(L.by + 2 * h->r), 1};
-        const uint32_t bpl[3] = {(uint32_t)TZ, (uint32_t)L.by, 1};
+        const uint32_t bcur[3] = {(uint32_t)(TZ + 2 * HZ), (uint32_t)(BY + 2 * h->r), 1};
+        const uint32_t bpl[3] = {(uint32_t)TZ, (uint32_t)BY, 1};
         sf_status s;
         if ((s = make_map(&maps.cur, b.cur, 3, d3, bcur))) return s;
         if ((s = make_map(&maps.old, b.out, 3, d3, bpl))) return s;
@@ -453,7 +357,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         if (h->beta && (s = make_map(&maps.beta, h->beta, 3, d3, bpl))) return s;
         if (mode == SF_MODE_GRAD) {
             const int64_t d4[4] = {h->nb[2], h->nb[1], h->nb[0], b.nsnap};
-            const uint32_t b4[4] = {(uint32_t)TZ, (uint32_t)L.by, 1, 1};
+            const uint32_t b4[4] = {(uint32_t)TZ, (uint32_t)BY, 1, 1};
             if ((s = make_map(&maps.snap, b.snaps, 4, d4, b4))) return s;
             if ((s = make_map(&maps.grad, b.grad, 3, d3, bpl))) return s;
         }
@@ -463,7 +367,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     // put dependent table loads on the stencil's critical path -> standalone kernels
     if (L.variant == SF_VAR_TMA && mode != SF_MODE_GRAD && b.inj && b.inj->ntgt > 0 &&
         b.inj->ntgt <= h->fuse_max && b.inj_vals) {
-        sf_status s = ensure_inj_tiles(h, *b.inj, L.by);
+        sf_status s = ensure_inj_tiles(h, *b.inj, L.vy);
         if (s) return s;
         a.inj_beg = b.inj->tiles.beg;
         a.inj_q = b.inj->tiles.q;
@@ -933,16 +837,16 @@ extern "C" sf_status sf_create_slab(const sf_desc *d, void *comm, int rank, int 
 }
 
 // ------------------------------------------------------------------ tuning / profiling
-extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int by, int chunks)
+extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas)
 {
     if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
-    if (variant < 0 || variant > 2 || (by != 0 && by != 8 && by != 16) || chunks < 0)
-        return sf_set_error(SF_ERR_INVALID_ARG, "bad tuning (%d, %d, %d)", variant, by, chunks);
+    if (variant < 0 || variant > 2 || vy < 0 || vy > 2 || ctas < 0)
+        return sf_set_error(SF_ERR_INVALID_ARG, "bad tuning (%d, %d, %d)", variant, vy, ctas);
     if (variant == SF_VAR_TMA && !tma_ok(h))
         return sf_set_error(SF_ERR_INVALID_ARG, "TMA variant needs 3D and n2 %% 4 == 0");
     h->variant = variant;
-    h->by = by;
-    h->chunks = chunks;
+    h->vy = vy;
+    h->ctas = ctas;
     return SF_OK;
 }
 
@@ -967,14 +871,14 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
     }
 }
 
-extern "C" sf_status sf_get_tuning(const sf_handle *h, int *variant, int *by, int *chunks)
+extern "C" sf_status sf_get_tuning(const sf_handle *h, int *variant, int *vy, int *ctas)
 {
     if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
     const int v = resolve_variant(h);
-    const int b = resolve_by(h);
+    const int b = resolve_vy(h);
     if (variant) *variant = v;
-    if (by) *by = v == SF_VAR_TMA ? b : 0;
-    if (chunks) *chunks = v == SF_VAR_TMA ? resolve_chunks(h, b, 0) : 0;
+    if (vy) *vy = v == SF_VAR_TMA ? b : 0;
+    if (ctas) *ctas = v == SF_VAR_TMA ? resolve_ctas(h) : 0;
     return SF_OK;
 }
 

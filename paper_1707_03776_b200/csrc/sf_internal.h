@@ -12,7 +12,7 @@
 
 // Injection targets grouped by (tile, consumer warp) of the TMA kernel (fused injection).
 struct SfInjTiles {
-    int by = 0;          // tile height the lists were built for (0 = not built)
+    int by = 0;          // rows per thread (VY) the lists were built for (0 = not built)
     int *beg = nullptr;  // [ntiles * by + 1]
     int *q = nullptr, *lj = nullptr, *t = nullptr;
 };
@@ -76,8 +76,8 @@ struct sf_handle {
     double *partial = nullptr;  // residual partial sums
     double *dJ = nullptr;
     // tuning
-    int variant = SF_VAR_AUTO, by = 0, chunks = 0;
-    int l2_prefetch = 4;            // TMA L2 prefetch distance (planes); env SF_L2_PREFETCH
+    int variant = SF_VAR_AUTO, vy = 0, ctas = 0;
+    int l2_prefetch = 8;            // TMA L2 prefetch distance (planes); env SF_L2_PREFETCH
     // slab decomposition
     int rank = 0, nranks = 1;
     void *comm = nullptr;

@@ -1,25 +1,38 @@
-// stencil_tma.cuh -- sm_100a 2.5D streaming stencil step, TMA-fed, register-rotated.
+// stencil_tma.cuh -- sm_100a 2.5D streaming stencil step, TMA-fed, register-rotated,
+// persistent (one CTA per SM, each walking (tile, x-chunk) items).
 //
-// Hot kernel of the path (memory-bandwidth bound):
-// each CTA owns a (y, z) tile of BY rows x 128 columns and streams along x (the
-// outermost, slab axis) over a chunk of planes.  Per plane p:
-//   * one elected thread issues TMA (cp.async.bulk.tensor) loads into an S-stage
-//     shared-memory ring, completion tracked by mbarrier transaction counts:
-//       - u^n plane p with its (y, z) halo: box (128 + 2 HZ) x (BY + 2R); the TMA
-//         out-of-bounds zero fill IS the zero ghost halo (reading C6),
-//       - old / c3 / beta (and snapshot / gradient in GRAD mode) of output plane q = p - R;
-//   * every thread (4 consecutive z of one y row) reads its z-row and 2R y-neighbour
-//     rows as float4 (conflict-free), forms the in-plane partial P_p at arrival and
-//     pushes u_p and P_p into register queues of depth 2R+1 (compile-time rotated by
-//     unrolling the plane loop by 2R+1: no register moves);
-//   * output plane q = p - R is finished from the queues: X = sum_k w_k((u_{q-k}+u_{q+k})-2u_q),
-//     Lap = P_q + X, out = u + beta (u - old) + c3 Lap, stored with STG.128 in place
-//     over `old` (plus the snapshot copy / fused gradient correlation).
-// HBM traffic per point (compulsory): read u^n, old, c3 (+beta) and write out:
-// 16 B (20 B with damping); x-chunk warm-up re-reads 2R planes of u^n per chunk.
+// Hot kernel of the path (memory-bandwidth bound).  A tile
+// is BY = 7 VY rows (y) x TZ = 32 VZ columns (z); a CTA walks its (tile, x-chunk) items --
+// each a run of planes of one tile column streamed along x (the outermost, slab axis) --
+// keeping its TMA pipeline running across items.  Per plane p of a segment:
+//   * the producer warp's elected lane issues TMA (cp.async.bulk.tensor) loads:
+//       - u^n plane p with its (y, z) halo into a DU-deep u ring: box (TZ + 2 HZ) x (BY + 2R);
+//         the TMA out-of-bounds zero fill IS the zero ghost halo (reading C6);
+//       - old / c3 / beta (+ snapshot / gradient in GRAD mode) of output plane q = p - R
+//         into a DC-deep coefficient ring;
+//     completion via mbarrier transaction counts (full), slot reuse via one arrive per
+//     consumer warp (empty);
+//   * each consumer warp (VY rows, VZ consecutive z per lane) pushes its own u values of
+//     plane p into a register queue of depth 2R+1 (compile-time rotated by unrolling the
+//     plane loop by 2R+1: no register moves), then finishes output plane q = p - R:
+//       in-plane  P = sum_k w_k (((y-k + y+k) + (z-k + z+k)) - 4u)  from the u tile of plane q
+//                 (still in the ring: DU >= R + 1; each y row is loaded once for all VY rows),
+//       x term    X = sum_k w_k ((u_{q-k} + u_{q+k}) - 2u)           from the register queue,
+//       update    out = u + beta (u - old) + c3 (P + X),  stored in place over `old`
+//     (plus the snapshot copy / fused gradient correlation; small source sets injected by
+//     the owning lane before the store).
+// HBM traffic per point (compulsory): read u^n, old, c3 (+beta), write out: 16 B (20 B
+// with damping); each segment re-reads 2R warm-up planes of u^n.  Shared-memory traffic
+// per point (the measured limiter of the previous one-row design): y rows (2R/VY + 1) x 4 B,
+// z halo 2 HZ/VZ x 4 B, coefficients 4 B each, + the TMA fills -- no partial-sum ring.
 #pragma once
 #include <cuda.h>
+#include <type_traits>
 #include "stencil_common.cuh"
+
+#ifndef SF_MBAR_SUSPEND_NS
+#define SF_MBAR_SUSPEND_NS 0x100000
+#endif
 
 namespace sftma {
 
@@ -28,57 +41,55 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p)
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
 {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
 {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+// try_wait with a suspend-time hint: a waiting warp sleeps until the phase completes (or
+// the hint expires) instead of spinning, leaving the issue slots to the other warps
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
     uint32_t done = 0;
-    const uint32_t a = smem_u32(bar);
     while (!done) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(a), "r"(parity)
+            : "r"(bar), "r"(parity), "r"(SF_MBAR_SUSPEND_NS)
             : "memory");
     }
 }
 
-__device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
-                                          uint64_t *bar)
+__device__ __forceinline__ void tma_load3(uint32_t dst, const CUtensorMap *tm, int c0, int c1, int c2,
+                                          uint32_t bar)
 {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
         : "memory");
 }
 
-__device__ __forceinline__ void tma_load4(void *dst, const CUtensorMap *tm, int c0, int c1, int c2,
-                                          int c3, uint64_t *bar)
+__device__ __forceinline__ void tma_load4(uint32_t dst, const CUtensorMap *tm, int c0, int c1, int c2,
+                                          int c3, uint32_t bar)
 {
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-        "r"(smem_u32(bar))
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
         : "memory");
 }
 
@@ -96,37 +107,48 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
 }
 
-__device__ __forceinline__ void stg4(float *p, float4 v)
-{
-    *reinterpret_cast<float4 *>(p) = v;
-}
-
-template <int R, int BY, int VZ, bool DAMP, int MODE>
-struct Cfg {
-    static constexpr int TZ = 32 * VZ;                   // z columns per CTA (32 lanes x VZ)
-    static constexpr int HZ = ((R + 3) / 4) * 4;         // z halo rounded up to 4 floats
-    static constexpr int W = TZ + 2 * HZ;                // smem row pitch of the u^n tile
-    static constexpr int H = BY + 2 * R;                 // rows of the u^n tile
-    static constexpr int Q = 2 * R + 1;                  // register queue depth
-    static constexpr int CUR_BYTES = ((W * H * 4 + 127) / 128) * 128;
-    static constexpr int PL_BYTES = TZ * BY * 4;         // one plane without halo
-    static constexpr int NPL = 2 + (DAMP ? 1 : 0) + (MODE == SF_MODE_GRAD ? 2 : 0);
-    static constexpr int STAGE_BYTES = CUR_BYTES + NPL * PL_BYTES;
-    static constexpr int PRING = R;                      // in-plane partials kept for R planes
-                                                          // (slot read for plane p-R, then rewritten with p)
-    static constexpr int PRING_BYTES = PRING * PL_BYTES;
-    static constexpr int S_MAX = (220 * 1024 - PRING_BYTES) / STAGE_BYTES;
-    // pipeline depth: 4 stages for r <= 4 (measured equal to 5 on configs[1]; keeps two
-    // BY = 8 CTAs per SM), 5 for r >= 5 (4 % faster on configs[3])
-    static constexpr int S_WANT = R >= 5 ? 5 : 4;
-    static constexpr int S = S_MAX >= S_WANT ? S_WANT : S_MAX;
-    static constexpr int SMEM = S * STAGE_BYTES + PRING_BYTES + 128;  // + alignment slack
-    static constexpr int THREADS = 32 * (BY + 1);         // BY consumer warps + 1 TMA producer warp
-    static_assert(S >= 2, "stage does not fit shared memory");
-    static_assert(VZ == 2 || VZ == 4, "VZ");
+// Tile geometry / shared-memory plan.  VY = 2 rows x VZ = 4 columns per thread: y-neighbour
+// loads cost (2R/VY) x 4 B per point and z-halo loads (2 HZ/VZ) x 4 B, so a 2 x 4 block keeps
+// shared-memory traffic under ~75 B per point even at r = 8, and its (2r+1) x 8-float
+// register queue still fits in 255 registers (<= 244 used at r = 8, no spills).
+// 7 consumer warps + 1 producer = 8 warps = 2 per SM sub-partition, which leaves each
+// thread the full 255 registers (a ninth warp would put 3 warps on one sub-partition and
+// cap every thread at 168 registers).
+template <int R, int VY>
+struct Geo {
+    static constexpr int VZ = 4;
+    static constexpr int NW = 7;                        // consumer warps
+    static constexpr int BY = NW * VY;                  // rows per tile
+    static constexpr int TZ = 32 * VZ;                  // columns per tile
+    static constexpr int HZ = ((R + 3) / 4) * 4;        // z halo rounded up to 16 B
 };
 
-// VZ consecutive floats <-> VZ/2 fp32x2 pair registers (LDS/STS/STG .64 / .128)
+template <int R, int VY, bool DAMP, int MODE>
+struct Cfg {
+    using G = Geo<R, VY>;
+    static constexpr int VZ = G::VZ, NW = G::NW, BY = G::BY, TZ = G::TZ, HZ = G::HZ;
+    static constexpr int W = TZ + 2 * HZ;               // smem row pitch of the u tile
+    static constexpr int H = BY + 2 * R;                // rows of the u tile
+    static constexpr int Q = 2 * R + 1;                 // register queue depth
+    static constexpr int UST = ((W * H * 4 + 127) / 128) * 128;   // u ring stage bytes
+    static constexpr int PL = TZ * BY * 4;              // one halo-free plane
+    static constexpr int NPL = 2 + (DAMP ? 1 : 0) + (MODE == SF_MODE_GRAD ? 2 : 0);
+    static constexpr int CST = NPL * PL;                // coefficient ring stage bytes
+    static constexpr int BUDGET = 225 * 1024;
+    // ring depths: the u ring must hold planes q..p (R + 1) plus the producer's lead;
+    // the coefficient ring gets what is left (up to 4; 1 only for r = 8 GRAD with damping)
+    static constexpr int DU_WANT = R + 5;
+    static constexpr int DU_FIT = (BUDGET - 2 * CST) / UST;
+    static constexpr int DU = DU_FIT >= DU_WANT ? DU_WANT : (DU_FIT >= R + 2 ? DU_FIT : R + 2);
+    static constexpr int DC_FIT = (BUDGET - DU * UST) / CST;
+    static constexpr int DC = DC_FIT >= 4 ? 4 : DC_FIT;
+    static constexpr int SMEM = DU * UST + DC * CST + 128;  // + alignment slack
+    static constexpr int THREADS = 32 * (NW + 1);       // NW consumer warps + 1 TMA producer warp
+    static_assert(DC >= 1, "coefficient ring does not fit shared memory");
+    static_assert(DU >= R + 2, "u ring does not fit shared memory");
+};
+
+// VZ consecutive floats <-> VZ/2 fp32x2 pair registers (LDS/STG .64 / .128)
 template <int VZ>
 __device__ __forceinline__ void ldp(const float *p, f2_t *v)
 {
@@ -144,124 +166,151 @@ __device__ __forceinline__ void stp(float *p, const f2_t *v)
     if (VZ == 4) *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(v[0], v[1]);
     else *reinterpret_cast<unsigned long long *>(p) = v[0];
 }
-
-// VZ consecutive floats <-> registers (LDS.64 / LDS.128, STG.64 / STG.128)
-template <int VZ>
-__device__ __forceinline__ void ldv(const float *p, float *v)
+__device__ __forceinline__ float lo2(f2_t v)
 {
-    if (VZ == 4) {
-        const float4 t = *reinterpret_cast<const float4 *>(p);
-        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    float a, b;
+    upk2(v, a, b);
+    return a;
+}
+__device__ __forceinline__ float hi2(f2_t v)
+{
+    float a, b;
+    upk2(v, a, b);
+    return b;
+}
+
+// Work split: per tile the planes [xa, xb) then [xa2, xb2) (PT in all), cut into `nchunk`
+// chunks of `chunk` planes; item it = (tile it % tiles, chunk it / tiles); CTA b takes items
+// b, b + G, b + 2G, ...  Consecutive CTAs work on y/z-neighbouring tiles of the same chunk at
+// the same time, so the tiles' shared halo rows are read from HBM once and hit in L2 for the
+// neighbour.  A chunk crossing from the first range into the second is two segments.
+struct Seg {
+    int tile;
+    int64_t qa, qb;
+};
+__device__ __forceinline__ Seg next_seg(int64_t w, int64_t end, int64_t P1, int64_t PT,
+                                        const SfStepArgs &a)
+{
+    Seg s;
+    s.tile = (int)(w / PT);
+    const int64_t pl = w - (int64_t)s.tile * PT;
+    int64_t lim;
+    if (pl < P1) {
+        s.qa = a.xa + pl;
+        lim = P1 - pl;
     } else {
-        const float2 t = *reinterpret_cast<const float2 *>(p);
-        v[0] = t.x; v[1] = t.y;
+        s.qa = a.xa2 + (pl - P1);
+        lim = PT - pl;
     }
-}
-template <int VZ>
-__device__ __forceinline__ void stv(float *p, const float *v)
-{
-    if (VZ == 4) *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
-    else *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+    s.qb = s.qa + min(lim, end - w);
+    return s;
 }
 
-// One CTA = BY consumer warps (one y row each, VZ consecutive z per lane) + 1 producer
-// warp whose elected lane issues every TMA load.  Per stage: `full` (TMA transaction
-// bytes) and `empty` (one arrive per consumer warp) mbarriers.
-template <int R, int BY, int VZ, bool DAMP, int MODE>
-__global__ void __launch_bounds__(32 * (BY + 1), (BY == 8 && R <= 4) ? 2 : 1)
+template <int R, int VY, bool DAMP, int MODE>
+__global__ void __launch_bounds__(Cfg<R, VY, DAMP, MODE>::THREADS, 1)
 k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_old,
         const __grid_constant__ CUtensorMap tm_c3, const __grid_constant__ CUtensorMap tm_beta,
         const __grid_constant__ CUtensorMap tm_snap, const __grid_constant__ CUtensorMap tm_grad,
-        const SfStepArgs a, const int snap_slot, const int chunk)
+        const SfStepArgs a, const int snap_slot, const int chunk, const int nchunk)
 {
-    using C = Cfg<R, BY, VZ, DAMP, MODE>;
-    constexpr int NJ = VZ / 2;  // fp32x2 pairs per lane
-    constexpr int Q = C::Q, TZ = C::TZ, HZ = C::HZ, W = C::W, S = C::S, PR = C::PRING;
+    using C = Cfg<R, VY, DAMP, MODE>;
+    constexpr int VZ = C::VZ, NJ = VZ / 2, NW = C::NW, BY = C::BY, TZ = C::TZ, HZ = C::HZ;
+    constexpr int Q = C::Q, W = C::W, DU = C::DU, DC = C::DC;
     const int PD = a.l2_prefetch;  // planes of L2 prefetch beyond the smem ring (0 = off)
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    // keep the address space visible to the compiler (LDS, not generic LD): align by
-    // offsetting the shared array itself
+    // keep the address space visible to the compiler (LDS, not generic LD)
     unsigned char *smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-    float *pring = reinterpret_cast<float *>(smem + S * C::STAGE_BYTES);
-    __shared__ __align__(8) uint64_t full[S];   // TMA bytes landed in stage s
-    __shared__ __align__(8) uint64_t empty[S];  // every consumer warp finished reading stage s
+    unsigned char *cring = smem + DU * C::UST;
+    __shared__ __align__(8) uint64_t bars[2 * DU + 2 * DC];
+    const uint32_t ufull = smem_u32(bars), uempty = ufull + 8 * DU;
+    const uint32_t cfull = uempty + 8 * DU, cempty = cfull + 8 * DC;
 
     const int lane = threadIdx.x, wy = threadIdx.y;
-    const int z0 = blockIdx.x * TZ, y0 = blockIdx.y * BY;
-    // chunk -> planes [qa, qb): chunks of the first range, then of the optional second
-    int64_t zc = blockIdx.z, ra = a.xa, rb = a.xb;
-    {
-        const int64_t nch1 = (a.xb - a.xa + chunk - 1) / chunk;
-        if (zc >= nch1) {
-            zc -= nch1;
-            ra = a.xa2;
-            rb = a.xb2;
-        }
-    }
-    const int64_t qa = ra + zc * chunk;
-    const int64_t qb = min(qa + (int64_t)chunk, rb);
-    if (qa >= qb) return;  // uniform over the CTA
-    const int NP = (int)(qb - qa) + 2 * R;
+    const int64_t P1 = a.xb - a.xa, PT = P1 + (a.xb2 - a.xa2);
+    const int ntz = (int)((a.n2 + TZ - 1) / TZ);
+    const int tiles = ntz * (int)((a.n1 + BY - 1) / BY);
+    const int items = tiles * nchunk;
+    if ((int)blockIdx.x >= items) return;  // uniform over the CTA
 
     if (wy == 0 && lane == 0) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], BY);
+#pragma unroll 1
+        for (int s = 0; s < DU; ++s) {
+            mbar_init(ufull + 8 * s, 1);
+            mbar_init(uempty + 8 * s, NW);
+        }
+#pragma unroll 1
+        for (int s = 0; s < DC; ++s) {
+            mbar_init(cfull + 8 * s, 1);
+            mbar_init(cempty + 8 * s, NW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
 
-    if (wy == BY) {
+    if (wy == NW) {
         // ------------------------------------------------ producer warp (TMA issue)
         if (lane == 0) {
             prefetch_tmap(&tm_cur);
             prefetch_tmap(&tm_old);
             prefetch_tmap(&tm_c3);
-            int st = 0;
-            uint32_t ph = 0;
-            for (int i = 0; i < NP; ++i) {
-                if (i >= S) mbar_wait(&empty[st], ph ^ 1u);
-                unsigned char *base = smem + st * C::STAGE_BYTES;
-                const int p = (int)(qa - R) + i;   // plane of u^n
-                const int q = p - R;               // output plane
-                const bool outp = (i >= 2 * R);
-                uint32_t bytes = W * C::H * 4;    // full box; out-of-bounds part zero-filled
-                if (outp) bytes += C::NPL * C::PL_BYTES;
-                mbar_expect_tx(&full[st], bytes);
-                tma_load3(base, &tm_cur, z0 - HZ, y0 - R, p, &full[st]);
-                if (outp) {
-                    unsigned char *pl = base + C::CUR_BYTES;
-                    tma_load3(pl, &tm_old, z0, y0, q, &full[st]);
-                    pl += C::PL_BYTES;
-                    tma_load3(pl, &tm_c3, z0, y0, q, &full[st]);
-                    pl += C::PL_BYTES;
-                    if (DAMP) {
-                        tma_load3(pl, &tm_beta, z0, y0, q, &full[st]);
-                        pl += C::PL_BYTES;
+            if (DAMP) prefetch_tmap(&tm_beta);
+            const uint32_t ubase = smem_u32(smem), cbase = smem_u32(cring);
+            int us = 0, cs = 0;
+            uint32_t uph = 0, cph = 0;
+            int64_t gu = 0, gc = 0;  // ring uses so far
+            for (int it = blockIdx.x; it < items; it += gridDim.x)
+            for (int64_t w = (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk,
+                         w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
+                const Seg sg = next_seg(w, w1, P1, PT, a);
+                w += sg.qb - sg.qa;
+                const int z0 = (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
+                const int NP = (int)(sg.qb - sg.qa) + 2 * R;
+                for (int i = 0; i < NP; ++i) {
+                    const int p = (int)(sg.qa - R) + i;   // plane of u^n
+                    const int q = p - R;                  // output plane
+                    if (gu >= DU) mbar_wait(uempty + 8 * us, uph ^ 1u);
+                    mbar_expect_tx(ufull + 8 * us, W * C::H * 4);  // full box, OOB zero-filled
+                    tma_load3(ubase + us * C::UST, &tm_cur, z0 - HZ, y0 - R, p, ufull + 8 * us);
+                    ++gu;
+                    if (++us == DU) {
+                        us = 0;
+                        uph ^= 1u;
                     }
-                    if (MODE == SF_MODE_GRAD) {
-                        tma_load4(pl, &tm_snap, z0, y0, q, snap_slot, &full[st]);
-                        pl += C::PL_BYTES;
-                        tma_load3(pl, &tm_grad, z0, y0, q, &full[st]);
+                    if (i >= 2 * R) {
+                        if (gc >= DC) mbar_wait(cempty + 8 * cs, cph ^ 1u);
+                        const uint32_t fb = cfull + 8 * cs;
+                        mbar_expect_tx(fb, C::CST);
+                        uint32_t pl = cbase + cs * C::CST;
+                        tma_load3(pl, &tm_old, z0, y0, q, fb);
+                        pl += C::PL;
+                        tma_load3(pl, &tm_c3, z0, y0, q, fb);
+                        pl += C::PL;
+                        if (DAMP) {
+                            tma_load3(pl, &tm_beta, z0, y0, q, fb);
+                            pl += C::PL;
+                        }
+                        if (MODE == SF_MODE_GRAD) {
+                            tma_load4(pl, &tm_snap, z0, y0, q, snap_slot, fb);
+                            pl += C::PL;
+                            tma_load3(pl, &tm_grad, z0, y0, q, fb);
+                        }
+                        ++gc;
+                        if (++cs == DC) {
+                            cs = 0;
+                            cph ^= 1u;
+                        }
                     }
-                }
-                // warm L2 PD planes ahead of the smem ring: the smem stages then fill from
-                // L2 and the ring depth no longer has to cover the full HBM latency
-                if (PD > 0 && i + PD < NP) {
-                    const int pp = p + PD, qq = q + PD;
-                    tma_prefetch3(&tm_cur, z0 - HZ, y0 - R, pp);
-                    if (i + PD >= 2 * R) {
-                        tma_prefetch3(&tm_old, z0, y0, qq);
-                        tma_prefetch3(&tm_c3, z0, y0, qq);
-                        if (DAMP) tma_prefetch3(&tm_beta, z0, y0, qq);
+                    // warm L2 PD planes ahead of the smem rings
+                    if (PD > 0 && i + PD < NP) {
+                        const int pp = p + PD, qq = q + PD;
+                        tma_prefetch3(&tm_cur, z0 - HZ, y0 - R, pp);
+                        if (i + PD >= 2 * R) {
+                            tma_prefetch3(&tm_old, z0, y0, qq);
+                            tma_prefetch3(&tm_c3, z0, y0, qq);
+                            if (DAMP) tma_prefetch3(&tm_beta, z0, y0, qq);
+                        }
                     }
-                }
-                if (++st == S) {
-                    st = 0;
-                    ph ^= 1u;
                 }
             }
         }
@@ -269,165 +318,268 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     }
 
     // ---------------------------------------------------- consumer warps
-    f2_t V[Q][NJ];  // u at planes (fp32 pairs), slot = iteration index mod Q
-    const int rown = R + wy;
-    const int zg = z0 + VZ * lane;
-    const int yg = y0 + wy;
-    const bool active = (zg < a.n2) && (yg < a.n1);
+    f2_t V[Q][VY][NJ];  // own u at planes (fp32 pairs), slot = iteration index mod Q
+    static_assert(Q <= 17, "slot switch covers r <= 8");
+    const int rown = R + VY * wy;       // first own row in the u tile
+    const float *ubase = reinterpret_cast<const float *>(smem);
+    const float *cbase = reinterpret_cast<const float *>(cring);
+    constexpr int UF = C::UST / 4, CF = C::CST / 4, PF = C::PL / 4;  // strides in floats
+    const int own_off = rown * W + HZ + VZ * lane;      // own values in a u tile
+    const int po = VY * wy * TZ + VZ * lane;            // own values (row 0) in a plane
+    int us = 0, uo = DU - R, cs = 0;                    // uo: u slot of plane q = p - R
+    uint32_t uph = 0, cph = 0;
     const int64_t plane = a.n1 * a.n2;
-    const int64_t rowoff = (int64_t)yg * a.n2 + zg;
-    const int po = wy * TZ + VZ * lane;  // this thread's VZ floats in a halo-free plane
-    float *myP = pring + po;            // private ring of in-plane partials (stride PL floats)
-    int st = 0, pw = 0;
-    uint32_t ph = 0;
-    // packed constants: weights {w_k, w_k}, -4, -2, -1, -gscale
+    // packed constants
     f2_t Wk[R + 1];
 #pragma unroll
     for (int k = 1; k <= R; ++k) Wk[k] = pk2(a.w.w[k], a.w.w[k]);
     Wk[0] = 0ull;
     const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f);
     const f2_t NG = pk2(-a.gscale, -a.gscale), ONE2 = pk2(1.f, 1.f);
-    // fused sparse work: this warp's cursors (warp-uniform), first entries at q >= qa
     constexpr int QINF = 0x7fffffff;
-    int ci = 0, ce = 0, cq = QINF;
-    {
-        const int wl = (blockIdx.y * gridDim.x + blockIdx.x) * BY + wy;
-        if (a.inj_beg) {
+
+    for (int it = blockIdx.x; it < items; it += gridDim.x)
+    for (int64_t w = (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk,
+                 w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
+        const Seg sg = next_seg(w, w1, P1, PT, a);
+        w += sg.qb - sg.qa;
+        const int z0 = (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
+        const int zg = z0 + VZ * lane;
+        const int yg = y0 + VY * wy;
+        const bool zact = zg < a.n2;
+        const int qa = (int)sg.qa, qb = (int)sg.qb;
+        const int NP = (qb - qa) + 2 * R;
+        float *optr = a.out + (int64_t)qa * plane + (int64_t)yg * a.n2 + zg;
+        float *sptr = (MODE == SF_MODE_SAVE) ? a.snap_out + (optr - a.out) : nullptr;
+        float *gptr = (MODE == SF_MODE_GRAD) ? a.grad + (optr - a.out) : nullptr;
+        // fused injection: this warp's cursor (warp-uniform), first entry at q >= qa
+        int ci = 0, ce = 0, cq = QINF;
+        if (MODE != SF_MODE_GRAD && a.inj_beg) {
+            const int wl = sg.tile * NW + wy;
             ci = a.inj_beg[wl];
             ce = a.inj_beg[wl + 1];
             while (ci < ce && a.inj_q[ci] < qa) ++ci;
             cq = ci < ce ? a.inj_q[ci] : QINF;
         }
-    }
 
-    for (int base = 0; base < NP; base += Q) {
+        // The x-direction register queue needs compile-time slots; only that small part
+        // (load plane p into its slot, x term of plane q) is replicated per slot through a
+        // switch -- everything else exists once, which keeps the loop in the instruction
+        // cache at r = 8 (a plane loop unrolled 2r+1 times thrashes it).
+        // For r <= 4 the whole loop body is unrolled 2r+1 times instead (slot = unrolled
+        // index, the switch folds away): small enough for the instruction cache, and the
+        // stage/slot bookkeeping becomes compile-time.
+        constexpr int UNR = (R <= 4) ? Q : 1;
+        int sl = 0;  // queue slot of plane p: iteration index mod Q
+#pragma unroll 1
+        for (int base = 0; base < NP; base += UNR)
 #pragma unroll
-        for (int s = 0; s < Q; ++s) {
-            const int i = base + s;
-            if (i < NP) {
-                mbar_wait(&full[st], ph);
-                const unsigned char *sb = smem + st * C::STAGE_BYTES;
-                const float *cs = reinterpret_cast<const float *>(sb);
-                // z row of this thread as aligned fp32 pairs: floats [VZ lane, VZ lane + 2 HZ + VZ)
-                constexpr int NZP = (2 * HZ + VZ) / 2;
-                f2_t zp[NZP];
+        for (int s2 = 0; s2 < UNR; ++s2) {
+                    const int i = base + s2;
+                    if (i >= NP) break;
+                    if (UNR == Q) sl = s2;
+                    const int p = qa - R + i;
+                    const bool outp = (i >= 2 * R);
+                    // ---- (1) in-plane partial of output plane q = p - R: its u tile is
+                    // resident (arrived R planes ago), so this overlaps the wait for plane p
+                    f2_t Pin[VY][NJ], Uq[VY][NJ];
+                    if (outp) {
+                        const float *uq = ubase + uo * UF;
+                        // y rows rown - R .. rown + VY - 1 + R (own rows included)
+                        f2_t Y[VY + 2 * R][NJ];
 #pragma unroll
-                for (int c = 0; c < (2 * HZ + VZ) / VZ; ++c) ldp<VZ>(cs + rown * W + VZ * lane + VZ * c, zp + NJ * c);
-                // odd-offset pairs (floats 2c+1, 2c+2), needed by odd radii
-                f2_t zo[NZP - 1];
+                        for (int t = 0; t < VY + 2 * R; ++t) ldp<VZ>(uq + own_off + (t - R) * W, Y[t]);
 #pragma unroll
-                for (int c = 0; c < NZP - 1; ++c) {
-                    float a0, a1, b0, b1;
-                    upk2(zp[c], a0, a1);
-                    upk2(zp[c + 1], b0, b1);
-                    zo[c] = pk2(a1, b0);
-                }
+                        for (int j = 0; j < VY; ++j)
 #pragma unroll
-                for (int jp = 0; jp < NJ; ++jp) V[s][jp] = zp[HZ / 2 + jp];
-                // in-plane partial P_p = sum_k w_k ((y-k + y+k) + (z-k + z+k) - 4u), fp32x2
-                f2_t pp2[NJ];
+                            for (int jp = 0; jp < NJ; ++jp) Uq[j][jp] = Y[R + j][jp];
+                        // z halos of the own rows: floats [-HZ, 0) and [VZ, VZ + HZ)
+                        f2_t ZL[VY][HZ / 2], ZR[VY][HZ / 2];
 #pragma unroll
-                for (int jp = 0; jp < NJ; ++jp) pp2[jp] = 0ull;
+                        for (int j = 0; j < VY; ++j) {
 #pragma unroll
-                for (int k = 1; k <= R; ++k) {
-                    f2_t ym2[NJ], yp2[NJ];
-                    ldp<VZ>(cs + (rown - k) * W + HZ + VZ * lane, ym2);
-                    ldp<VZ>(cs + (rown + k) * W + HZ + VZ * lane, yp2);
+                            for (int c = 0; c < HZ / VZ; ++c) {
+                                ldp<VZ>(uq + own_off + j * W - HZ + VZ * c, ZL[j] + NJ * c);
+                                ldp<VZ>(uq + own_off + j * W + VZ + VZ * c, ZR[j] + NJ * c);
+                            }
+                        }
 #pragma unroll
-                    for (int jp = 0; jp < NJ; ++jp) {
-                        const int fm = HZ + 2 * jp - k, fpp = HZ + 2 * jp + k;  // float index of the pair start
-                        const f2_t zm = (k & 1) ? zo[(fm - 1) / 2] : zp[fm / 2];
-                        const f2_t zq = (k & 1) ? zo[(fpp - 1) / 2] : zp[fpp / 2];
-                        const f2_t t = sf_inplane3_x2(ym2[jp], yp2[jp], zm, zq, V[s][jp], M4);
-                        pp2[jp] = fma2(Wk[k], t, pp2[jp]);
-                    }
-                }
-                const bool outp = (i >= 2 * R);
-                f2_t ov[NJ], cv[NJ], bv[NJ], sv[NJ], gv[NJ], pq[NJ];
-                if (!DAMP) {
+                        for (int j = 0; j < VY; ++j) {
+                            // float at z offset e (relative to the own first column) of row j
+                            auto F = [&](int e) -> float {
+                                if (e < 0) {
+                                    const int f = e + HZ;
+                                    return (f & 1) ? hi2(ZL[j][f >> 1]) : lo2(ZL[j][f >> 1]);
+                                }
+                                if (e >= VZ) {
+                                    const int f = e - VZ;
+                                    return (f & 1) ? hi2(ZR[j][f >> 1]) : lo2(ZR[j][f >> 1]);
+                                }
+                                return (e & 1) ? hi2(Uq[j][e >> 1]) : lo2(Uq[j][e >> 1]);
+                            };
+                            // aligned pair starting at even z offset e
+                            auto PZ = [&](int e) -> f2_t {
+                                if (e < 0) return ZL[j][(e + HZ) >> 1];
+                                if (e >= VZ) return ZR[j][(e - VZ) >> 1];
+                                return Uq[j][e >> 1];
+                            };
 #pragma unroll
-                    for (int jp = 0; jp < NJ; ++jp) bv[jp] = ONE2;
-                }
-                if (outp) {
-                    const float *pl = reinterpret_cast<const float *>(sb + C::CUR_BYTES);
-                    ldp<VZ>(pl + po, ov);
-                    ldp<VZ>(pl + TZ * BY + po, cv);
-                    int nxt = 2;
-                    if (DAMP) {
-                        ldp<VZ>(pl + 2 * TZ * BY + po, bv);
-                        nxt = 3;
-                    }
-                    if (MODE == SF_MODE_GRAD) {
-                        ldp<VZ>(pl + nxt * TZ * BY + po, sv);
-                        ldp<VZ>(pl + (nxt + 1) * TZ * BY + po, gv);
-                    }
-                }
-                // this warp is done with the stage: release it to the producer
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[st]);
-                if (++st == S) {
-                    st = 0;
-                    ph ^= 1u;
-                }
-                // P ring (thread-private slots, R deep): slot pw holds P_{p-R}; read it, then
-                // overwrite it with P_p (same thread, program order)
-                if (outp) ldp<VZ>(myP + pw * (TZ * BY), pq);
-                stp<VZ>(myP + pw * (TZ * BY), pp2);
-                if (++pw == PR) pw = 0;
-                // ---- finish output plane q = p - R from the register queue ----
-                if (outp) {
-                    const int sq = (s - R + Q) % Q;  // compile-time after unrolling
-                    const int64_t q = qa + (i - 2 * R);
-                    f2_t res2[NJ], gres2[NJ];
+                            for (int jp = 0; jp < NJ; ++jp) {
+                                const f2_t u = Uq[j][jp];
+                                // radius ascending (== sf_inplane3 per lane)
+                                f2_t P = 0ull;
 #pragma unroll
-                    for (int jp = 0; jp < NJ; ++jp) {
-                        const f2_t u = V[sq][jp];
-                        f2_t X = 0ull;
-#pragma unroll
-                        for (int k = 1; k <= R; ++k)
-                            X = fma2(Wk[k], sf_xterm_x2(V[(sq - k + Q) % Q][jp], V[(sq + k) % Q][jp], u, M2), X);
-                        const f2_t lap = add2(pq[jp], X);
-                        // out = u + beta (u - old) + c3 lap   (== sf_update per lane)
-                        const f2_t d = fma2(M1, ov[jp], u);
-                        res2[jp] = fma2(cv[jp], lap, fma2(bv[jp], d, u));
-                        if (MODE == SF_MODE_GRAD) {
-                            // S = (beta - 1) d + c3 lap ; g -= gscale * snap * S   (== sf_d2 / sf_grad)
-                            const f2_t S2 = fma2(add2(bv[jp], M1), d, mul2(cv[jp], lap));
-                            gres2[jp] = fma2(NG, mul2(sv[jp], S2), gv[jp]);
+                                for (int k = 1; k <= R; ++k) {
+                                    const f2_t ys = add2(Y[R + j - k][jp], Y[R + j + k][jp]);
+                                    const int em = 2 * jp - k, ep = 2 * jp + k;
+                                    f2_t zs;
+                                    if (k & 1)  // odd radius: unaligned pairs, two scalar adds
+                                        zs = pk2(__fadd_rn(F(em), F(ep)), __fadd_rn(F(em + 1), F(ep + 1)));
+                                    else
+                                        zs = add2(PZ(em), PZ(ep));
+                                    P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
+                                }
+                                Pin[j][jp] = P;
+                            }
                         }
                     }
-                    if (MODE != SF_MODE_GRAD && cq == (int)q) {  // GRAD steps inject standalone
-                        // fused injection, rare path: res[j] += sum_e coef_e vals[pt_e]
-                        // (the fp32 operations of k_inject, bitwise)
-                        float res[VZ];
+                    // ---- (2) plane p of u^n into queue slot sl; x term of plane q (slot sl - R)
+                    mbar_wait(ufull + 8 * us, uph);
+                    const float *ut = ubase + us * UF;
+                    f2_t X[VY][NJ];
+                    auto slot = [&](auto ic) {
+                        constexpr int S = decltype(ic)::value;
+                        constexpr int SQ = (S - R + Q) % Q;
 #pragma unroll
-                        for (int jp = 0; jp < NJ; ++jp) upk2(res2[jp], res[2 * jp], res[2 * jp + 1]);
-                        do {
-                            const int lj = a.inj_lj[ci];
-                            if ((lj >> 2) == lane) {
-                                const int t = a.inj_t[ci];
-                                float dd = 0.f;
-#pragma unroll 1
-                                for (int e = a.inj_rowptr[t]; e < a.inj_rowptr[t + 1]; ++e)
-                                    dd = __fmaf_rn(a.inj_coef[e], a.inj_vals[a.inj_pt[e]], dd);
-                                const int j = lj & 3;
+                        for (int j = 0; j < VY; ++j) ldp<VZ>(ut + own_off + j * W, V[S][j]);
+                        if (outp) {
 #pragma unroll
-                                for (int jj = 0; jj < VZ; ++jj) res[jj] = (j == jj) ? __fadd_rn(res[jj], dd) : res[jj];
+                            for (int j = 0; j < VY; ++j)
+#pragma unroll
+                                for (int jp = 0; jp < NJ; ++jp) {
+                                    f2_t x = 0ull;
+#pragma unroll
+                                    for (int k = 1; k <= R; ++k)
+                                        x = fma2(Wk[k], sf_xterm_x2(V[(SQ - k + Q) % Q][j][jp], V[(SQ + k) % Q][j][jp], V[SQ][j][jp], M2), x);
+                                    X[j][jp] = x;
+                                }
+                        }
+                    };
+                    switch (sl) {
+#define SF_SLOT(S_) \
+    case S_:        \
+        if constexpr (S_ < Q) slot(std::integral_constant<int, S_>{}); \
+        break;
+                        SF_SLOT(0) SF_SLOT(1) SF_SLOT(2) SF_SLOT(3) SF_SLOT(4) SF_SLOT(5) SF_SLOT(6)
+                        SF_SLOT(7) SF_SLOT(8) SF_SLOT(9) SF_SLOT(10) SF_SLOT(11) SF_SLOT(12) SF_SLOT(13)
+                        SF_SLOT(14) SF_SLOT(15) SF_SLOT(16)
+#undef SF_SLOT
+                    }
+                    if (UNR != Q && ++sl == Q) sl = 0;
+                    if (p < qa || p >= qb) {  // never an output plane: release the slot now
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(uempty + 8 * us);
+                    }
+                    if (outp) {
+                        // ---- (3) finish output plane q: update, store ----
+                        mbar_wait(cfull + 8 * cs, cph);
+                        const float *cp = cbase + cs * CF + po;
+                        f2_t ov[VY][NJ], cv[VY][NJ], bv[VY][NJ], sv[VY][NJ], gv[VY][NJ];
+#pragma unroll
+                        for (int j = 0; j < VY; ++j) {
+                            ldp<VZ>(cp + j * TZ, ov[j]);
+                            ldp<VZ>(cp + PF + j * TZ, cv[j]);
+                            int nxt = 2;
+                            if (DAMP) {
+                                ldp<VZ>(cp + 2 * PF + j * TZ, bv[j]);
+                                nxt = 3;
+                            } else {
+#pragma unroll
+                                for (int jp = 0; jp < NJ; ++jp) bv[j][jp] = ONE2;
                             }
-                            ++ci;
-                            cq = ci < ce ? a.inj_q[ci] : QINF;
-                        } while (cq == (int)q);
+                            if (MODE == SF_MODE_GRAD) {
+                                ldp<VZ>(cp + nxt * PF + j * TZ, sv[j]);
+                                ldp<VZ>(cp + (nxt + 1) * PF + j * TZ, gv[j]);
+                            }
+                        }
+                        // done with the u tile of plane q and the coefficient stage
+                        __syncwarp();
+                        if (lane == 0) {
+                            mbar_arrive(uempty + 8 * uo);
+                            mbar_arrive(cempty + 8 * cs);
+                        }
+                        if (++cs == DC) {
+                            cs = 0;
+                            cph ^= 1u;
+                        }
+                        const int q = p - R;
+                        f2_t res2[VY][NJ], gres2[VY][NJ];
 #pragma unroll
-                        for (int jp = 0; jp < NJ; ++jp) res2[jp] = pk2(res[2 * jp], res[2 * jp + 1]);
+                        for (int j = 0; j < VY; ++j) {
+#pragma unroll
+                            for (int jp = 0; jp < NJ; ++jp) {
+                                const f2_t u = Uq[j][jp];
+                                const f2_t lap = add2(Pin[j][jp], X[j][jp]);
+                                // out = u + beta (u - old) + c3 lap   (== sf_update per lane)
+                                const f2_t d = fma2(M1, ov[j][jp], u);
+                                res2[j][jp] = fma2(cv[j][jp], lap, fma2(bv[j][jp], d, u));
+                                if (MODE == SF_MODE_GRAD) {
+                                    // S = (beta - 1) d + c3 lap ; g -= gscale * snap * S
+                                    const f2_t S2 = fma2(add2(bv[j][jp], M1), d, mul2(cv[j][jp], lap));
+                                    gres2[j][jp] = fma2(NG, mul2(sv[j][jp], S2), gv[j][jp]);
+                                }
+                            }
+                        }
+                        if (MODE != SF_MODE_GRAD && cq == q) {
+                            // fused injection, rare path: res[t] += sum_e coef_e vals[pt_e]
+                            // (the fp32 operations of k_inject, bitwise); lj = ((jy 32 + lane) 4 + jz)
+                            float res[VY][VZ];
+#pragma unroll
+                            for (int j = 0; j < VY; ++j)
+#pragma unroll
+                                for (int jp = 0; jp < NJ; ++jp) upk2(res2[j][jp], res[j][2 * jp], res[j][2 * jp + 1]);
+                            do {
+                                const int lj = a.inj_lj[ci];
+                                if (((lj >> 2) & 31) == lane) {
+                                    const int t = a.inj_t[ci];
+                                    float dd = 0.f;
+#pragma unroll 1
+                                    for (int e = a.inj_rowptr[t]; e < a.inj_rowptr[t + 1]; ++e)
+                                        dd = __fmaf_rn(a.inj_coef[e], a.inj_vals[a.inj_pt[e]], dd);
+                                    const int jy = lj >> 7, jz = lj & 3;
+#pragma unroll
+                                    for (int j = 0; j < VY; ++j)
+#pragma unroll
+                                        for (int jj = 0; jj < VZ; ++jj)
+                                            res[j][jj] = (jy == j && jz == jj) ? __fadd_rn(res[j][jj], dd) : res[j][jj];
+                                }
+                                ++ci;
+                                cq = ci < ce ? a.inj_q[ci] : QINF;
+                            } while (cq == q);
+#pragma unroll
+                            for (int j = 0; j < VY; ++j)
+#pragma unroll
+                                for (int jp = 0; jp < NJ; ++jp) res2[j][jp] = pk2(res[j][2 * jp], res[j][2 * jp + 1]);
+                        }
+                        if (zact) {
+#pragma unroll
+                            for (int j = 0; j < VY; ++j) {
+                                if (yg + j < a.n1) {
+                                    stp<VZ>(optr + j * a.n2, res2[j]);
+                                    if (MODE == SF_MODE_SAVE) stp<VZ>(sptr + j * a.n2, res2[j]);
+                                    if (MODE == SF_MODE_GRAD) stp<VZ>(gptr + j * a.n2, gres2[j]);
+                                }
+                            }
+                        }
+                        optr += plane;
+                        if (MODE == SF_MODE_SAVE) sptr += plane;
+                        if (MODE == SF_MODE_GRAD) gptr += plane;
                     }
-                    if (active) {
-                        const int64_t off = q * plane + rowoff;
-                        stp<VZ>(a.out + off, res2);
-                        if (MODE == SF_MODE_SAVE) stp<VZ>(a.snap_out + off, res2);
-                        if (MODE == SF_MODE_GRAD) stp<VZ>(a.grad + off, gres2);
+                    if (++us == DU) {
+                        us = 0;
+                        uph ^= 1u;
                     }
-                }
-            }
+                    if (++uo == DU) uo = 0;
         }
     }
 }

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Sweep the stencil kernel's launch tuning (warps per CTA, x-chunks) on a BASELINE
+"""Sweep the stencil kernel's launch tuning (tile rows, persistent CTA count) on a BASELINE
 config and print the average stencil-launch time and GB/s (CUDA events around every
 stencil launch, recorded by libsf).  Usage: python scripts/tune.py [--config 1] [--nt 60]"""
 import argparse
@@ -21,8 +21,8 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--nt", type=int, default=60)
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--by", default="8,16")
-    ap.add_argument("--chunks", default="0,1,2,3,4,5,6,7,8,10,12,14")
+    ap.add_argument("--vy", default="2")
+    ap.add_argument("--ctas", default="0")
     ap.add_argument("--grad", action="store_true", help="time the adjoint with fused gradient")
     ap.add_argument("--random-init", action="store_true",
                     help="start from a random (incompressible) wavefield instead of zeros")
@@ -41,10 +41,10 @@ def main():
         k = p.save_every or 4
         _, _, snaps = prop.forward(wav, save_every=k)
         res = torch.randn((p.nt, p.rec_coords.shape[0]), device="cuda")
-    for by, ch in itertools.product([int(x) for x in args.by.split(",")],
-                                    [int(x) for x in args.chunks.split(",")]):
+    for vy, ch in itertools.product([int(x) for x in args.vy.split(",")],
+                                    [int(x) for x in args.ctas.split(",")]):
         try:
-            prop.set_tuning(2, by, ch)
+            prop.set_tuning(2, vy, ch)
         except sf.SfError:
             continue
         t = prop.tuning()
@@ -64,7 +64,7 @@ def main():
         ms = pr["stencil_ms"] / pr["stencil_launches"]
         extra = (4 + 12 / k) if args.grad else 0
         gbs = (bpp + extra) * N / (ms * 1e-3) / 1e9
-        row = {"by": t["by"], "chunks": t["chunks"], "req_chunks": ch, "launch_ms": round(ms, 5),
+        row = {"vy": t["vy"], "ctas": t["ctas"], "req_ctas": ch, "launch_ms": round(ms, 5),
                "interp_us": round(pr["interp_ms"] * 1e3 / max(pr["interp_launches"], 1), 2),
                "GBps": round(gbs, 1), "GPts": round(N / (ms * 1e-3) / 1e9, 2)}
         print(json.dumps(row), flush=True)

@@ -38,9 +38,9 @@ def make_prop(p, m=None, **kw):
                            rec_coords=p.rec_coords.astype(np.float64), **kw)
 
 
-def gpu_forward(p, variant=0, chunks=0, by=0, save_every=0, wavelet=None):
+def gpu_forward(p, variant=0, ctas=0, vy=0, save_every=0, wavelet=None):
     prop = make_prop(p)
-    prop.set_tuning(variant, by, chunks)
+    prop.set_tuning(variant, vy, ctas)
     rec, u, snaps = prop.forward(dev(p.wavelet if wavelet is None else wavelet), save_every=save_every)
     torch.cuda.synchronize()
     out = (rec.cpu().numpy(), u.cpu().numpy(), None if snaps is None else snaps.cpu().numpy())
@@ -57,26 +57,28 @@ def oracle_forward(p, save_every=0, wavelet=None):
 @pytest.mark.parametrize("so", [2, 4, 6, 8, 10, 12, 14, 16])
 def test_forward_3d_all_orders_both_variants(so):
     """3D, damping on, ragged tiles in every axis (n2 = 132: one full + one partial
-    128-column tile; n1 = 45; 37 planes split in 3 x-chunks)."""
+    128-column tile; n1 = 45: ragged 14- and 7-row tiles; 37 planes).  The persistent TMA
+    kernel runs with one CTA per SM and with 1, 3 and 7 CTAs, so that CTA runs start and
+    end mid-column and span several tile columns (segments)."""
     p = synth.random_problem(3, (37, 45, 132), so, 60, seed=so, nbl=6, nsrc=2, nrec=9)
     ro, uo, _ = oracle_forward(p)
     results = {}
-    for variant, chunks in ((1, 0), (2, 1), (2, 3)):
-        rg, ug, _ = gpu_forward(p, variant=variant, chunks=chunks)
-        assert rel(rg, ro) <= TOL, (variant, chunks, rel(rg, ro))
+    for variant, vy, ctas in ((1, 0, 0), (2, 2, 0), (2, 2, 1), (2, 2, 3), (2, 2, 7), (2, 1, 0), (2, 1, 5)):
+        rg, ug, _ = gpu_forward(p, variant=variant, vy=vy, ctas=ctas)
+        assert rel(rg, ro) <= TOL, (variant, vy, ctas, rel(rg, ro))
         assert rel(ug[1], uo[1]) <= TOL and rel(ug[0], uo[0]) <= TOL
-        results[(variant, chunks)] = (rg, ug)
+        results[(variant, vy, ctas)] = (rg, ug)
     # every variant evaluates the same per-point expression in the same order: identical bits
-    base = results[(1, 0)]
+    base = results[(1, 0, 0)]
     for k, v in results.items():
         assert np.array_equal(v[0], base[0]) and np.array_equal(v[1], base[1]), k
 
 
-@pytest.mark.parametrize("by", [8, 16])
-def test_forward_3d_tma_block_heights(by):
+@pytest.mark.parametrize("vy", [1, 2])
+def test_forward_3d_tma_rows_per_thread(vy):
     p = synth.random_problem(3, (30, 50, 64), 8, 40, seed=7, nbl=5)
     ro, uo, _ = oracle_forward(p)
-    rg, ug, _ = gpu_forward(p, variant=2, by=by, chunks=2)
+    rg, ug, _ = gpu_forward(p, variant=2, vy=vy, ctas=2)
     assert rel(rg, ro) <= TOL and rel(ug[1], uo[1]) <= TOL
 
 
