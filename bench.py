@@ -48,16 +48,20 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the stencil kernel from the committed ncu --set full
-    capture summary (profiles/r01_stencil_ncu_full.json, scripts/ncu_summary.py), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_stencil_ncu_full.json")
+NCU_ROUND = "r01"
+
+
+def ncu_traffic(cfg):
+    """Per-launch DRAM bytes (read + write) of the stencil kernel on this config from the
+    committed ncu --set full capture summary (profiles/<round>_stencil_ncu_c<cfg>.json,
+    written by scripts/ncu_summary.py), or None when that config was not captured."""
+    rel = os.path.join("profiles", f"{NCU_ROUND}_stencil_ncu_c{cfg}.json")
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, rel)) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d
+        return d.get("dram_bytes_per_launch"), rel
     except Exception:
-        return None, None
+        return None, rel
 
 
 class ClockSampler:
@@ -235,14 +239,17 @@ def run_ours(args):
 
     # roofline of the dominant kernel (stencil step): algorithmic bytes per launch
     bpp = 20 if eta_loc is not None else 16      # u^n, u^{n-1}, out, c3(+beta) fp32
-    # (gradient configs: the average over plain, save and fused-correlation launches is
-    # reported against the plain-step byte count; the extra save / correlation bytes are
-    # listed separately in per_update_us)
     launch_ms = prof["stencil_ms"] / max(prof["stencil_launches"], 1)
     alg_bytes = bpp * npts_local
+    if grad_mode:
+        # forward: nt-1 launches, (nt-1)//k of them also store a snapshot (+4 B/pt); adjoint:
+        # nt-1 launches, (nt-1)//k of them also read the snapshot and update the gradient
+        # (+12 B/pt) -- averaged over the 2 (nt-1) stencil launches of a gradient
+        nk = (p.nt - 1) // k
+        alg_bytes = int(round(npts_local * (bpp + (4 * nk + 12 * nk) / (2 * (p.nt - 1)))))
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
-    traffic, _ = ncu_traffic()
+    traffic, traffic_rel = ncu_traffic(cfg)
 
     result = None
     if rank == 0:
@@ -272,13 +279,14 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": None if traffic is None else int(traffic),
-                         "traffic_source": "profiles/r01_stencil_ncu_full.json (ncu --set full, dram "
-                                           "read+write per launch, random-init wavefield)",
+                         "traffic_source": (f"{traffic_rel} (ncu --set full, dram read+write per "
+                                            "launch, random-init wavefield)") if traffic is not None
+                                           else f"no ncu capture for this config ({traffic_rel})",
                          "peak_source": peak_src,
                          "kernel": "k_tma3d (stencil step)" if tuning["variant"] == 2 else
                                    ("k_generic3d" if len(gshape) == 3 else "k_generic2d"),
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "bytes_per_point": bpp, "avg_launch_ms": round(launch_ms, 5),
+                         "bytes_per_point": round(alg_bytes / npts_local, 3), "avg_launch_ms": round(launch_ms, 5),
                          "stencil_share_of_step": round(prof["stencil_ms"] / max(ms, 1e-9), 4),
                          "per_update_us": {k: round(prof[f"{k}_ms"] * 1e3 / (args.steps * (p.nt - 1)), 2)
                                            for k in ("stencil", "inject", "interp", "other")}},

@@ -31,7 +31,8 @@
  *   - `stream` is a cudaStream_t (NULL = legacy default stream); every call is
  *     ordered on it and returns without synchronising unless stated.
  *   - Ownership: the library never frees caller memory.  A handle owns its setup
- *     tables and its coefficient arrays (beta, c3: 1-2 x N floats), freed by sf_destroy.
+ *     tables and its coefficient arrays (beta, c3: 1-2 x N floats), allocated from the
+ *     device's stream-ordered memory pool (retained for reuse) and freed by sf_destroy.
  *   - Errors: every call validates before launching anything and returns an
  *     sf_status; nothing is thrown across the ABI.  sf_last_error() gives a message
  *     (thread-local).  A handle is not thread-safe.
@@ -89,6 +90,8 @@ SF_API sf_status sf_fd_weights(int space_order, double *w /* host [r+1] */);
 /* Validate (shape, order, CFL, domain), build interpolation / injection tables and the
  * hoisted coefficient arrays beta and c3 on the device.  Synchronises the device once. */
 SF_API sf_status sf_create(const sf_desc *d, sf_handle **out);
+/* Synchronises the device (work on any stream may still use the handle), then returns
+ * the handle's device memory to the pool.  NULL is a no-op. */
 SF_API void sf_destroy(sf_handle *h);
 
 /* Forward propagation.

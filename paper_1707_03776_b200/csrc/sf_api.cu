@@ -212,6 +212,32 @@ struct StepBufs {
     int64_t xa2 = 0, xb2 = 0;  // optional second range in the same launch
 };
 
+// Library-internal device allocations come from the device's stream-ordered memory pool
+// (kept, not released to the OS: release threshold = max), ordered on the legacy stream.
+// Creating and destroying handles then costs no device-wide synchronisation and no page
+// unmapping -- sf_forward_host builds a handle per call.
+static cudaError_t sf_dalloc(void **p, size_t bytes)
+{
+    static thread_local int pool_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (pool_dev != dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_dev = dev;
+    }
+    return cudaMallocAsync(p, bytes, 0);
+}
+static void sf_dfree(void *p)
+{
+    if (p) cudaFreeAsync(p, 0);
+}
+#define cudaMalloc(p, n) sf_dalloc((void **)(p), (n))
+#define cudaFree(p) sf_dfree((void *)(p))
+
 template <class T>
 static sf_status upload(T **dst, const std::vector<T> &v)
 {
@@ -271,6 +297,7 @@ static sf_status ensure_inj_tiles(sf_handle *h, SfSparse &sp, int by)
 {
     SfInjTiles &T = sp.tiles;
     if (T.by == by) return SF_OK;
+    if (T.by) cudaDeviceSynchronize();  // lists of another tile shape may still be in use
     free_inj(T);
     const int64_t nl = n_warp_lists(h, by);
     struct E {
@@ -618,6 +645,9 @@ static sf_status validate_desc(const sf_desc *d)
 extern "C" void sf_destroy(sf_handle *h)
 {
     if (!h) return;
+    // the pool frees below are ordered on the legacy stream: finish any work still using
+    // the handle's buffers on other (possibly non-blocking) streams first
+    cudaDeviceSynchronize();
     cudaFree(h->c3);
     cudaFree(h->beta);
     cudaFree(h->partial);
