@@ -11,7 +11,9 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsf.so")
+# SF_LIB_PATH: load another build of the same C-ABI (A/B timing of kernel variants only;
+# the tests, smoke() and bench.py use the in-tree build)
+LIB_PATH = os.environ.get("SF_LIB_PATH") or os.path.join(_HERE, "libsf.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 STATUS = {0: "SF_OK", 1: "SF_ERR_INVALID_ARG", 2: "SF_ERR_SHAPE", 3: "SF_ERR_ORDER",

@@ -166,6 +166,19 @@ __device__ __forceinline__ void stp(float *p, const f2_t *v)
     if (VZ == 4) *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(v[0], v[1]);
     else *reinterpret_cast<unsigned long long *>(p) = v[0];
 }
+// predicated 16-/8-byte global store (no divergent branch around edge tiles)
+template <int VZ>
+__device__ __forceinline__ void stp_if(float *p, const f2_t *v, bool pred)
+{
+    if (VZ == 4)
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+                     "@q st.global.v2.b64 [%0], {%1, %2};\n\t}" ::"l"(p), "l"(v[0]), "l"(v[1]), "r"((uint32_t)pred)
+                     : "memory");
+    else
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                     "@q st.global.b64 [%0], %1;\n\t}" ::"l"(p), "l"(v[0]), "r"((uint32_t)pred)
+                     : "memory");
+}
 __device__ __forceinline__ float lo2(f2_t v)
 {
     float a, b;
@@ -328,6 +341,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     const int po = VY * wy * TZ + VZ * lane;            // own values (row 0) in a plane
     int us = 0, uo = DU - R, cs = 0;                    // uo: u slot of plane q = p - R
     uint32_t uph = 0, cph = 0;
+    const int n2 = (int)a.n2;
     const int64_t plane = a.n1 * a.n2;
     // packed constants
     f2_t Wk[R + 1];
@@ -347,6 +361,9 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
         const int zg = z0 + VZ * lane;
         const int yg = y0 + VY * wy;
         const bool zact = zg < a.n2;
+        bool act[VY];
+#pragma unroll
+        for (int j = 0; j < VY; ++j) act[j] = zact && (yg + j < a.n1);
         const int qa = (int)sg.qa, qb = (int)sg.qb;
         const int NP = (qb - qa) + 2 * R;
         float *optr = a.out + (int64_t)qa * plane + (int64_t)yg * a.n2 + zg;
@@ -561,13 +578,26 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                                 for (int jp = 0; jp < NJ; ++jp) res2[j][jp] = pk2(res[j][2 * jp], res[j][2 * jp + 1]);
                         }
-                        if (zact) {
+                        if (UNR == 1) {
+                            // rolled loop (r >= 5): predicated stores, no divergent branches
+                            // (measured 5 % faster on configs[3])
 #pragma unroll
                             for (int j = 0; j < VY; ++j) {
-                                if (yg + j < a.n1) {
-                                    stp<VZ>(optr + j * a.n2, res2[j]);
-                                    if (MODE == SF_MODE_SAVE) stp<VZ>(sptr + j * a.n2, res2[j]);
-                                    if (MODE == SF_MODE_GRAD) stp<VZ>(gptr + j * a.n2, gres2[j]);
+                                stp_if<VZ>(optr + j * n2, res2[j], act[j]);
+                                if (MODE == SF_MODE_SAVE) stp_if<VZ>(sptr + j * n2, res2[j], act[j]);
+                                if (MODE == SF_MODE_GRAD) stp_if<VZ>(gptr + j * n2, gres2[j], act[j]);
+                            }
+                        } else {
+                            // unrolled loop (r <= 4): plain branchy stores -- the predicated
+                            // form measured 8 % slower here (scheduling of the unrolled body)
+                            if (zact) {
+#pragma unroll
+                                for (int j = 0; j < VY; ++j) {
+                                    if (yg + j < a.n1) {
+                                        stp<VZ>(optr + j * a.n2, res2[j]);
+                                        if (MODE == SF_MODE_SAVE) stp<VZ>(sptr + j * a.n2, res2[j]);
+                                        if (MODE == SF_MODE_GRAD) stp<VZ>(gptr + j * a.n2, gres2[j]);
+                                    }
                                 }
                             }
                         }
