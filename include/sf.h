@@ -159,6 +159,9 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   on one GPU it only reorders work: results are bitwise identical) */
 #define SF_OPT_FUSE_MAX 3      /* largest point set injected / interpolated inside the stencil
                                   kernel (default 256); larger sets use standalone kernels       */
+#define SF_OPT_COMM_SMS 4      /* split schedule: SMs the persistent interior launch leaves free
+                                  for the concurrent halo exchange (NCCL kernels) and the side-
+                                  stream records (default 8 in slab mode, 0 on one GPU; 0..64)   */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */

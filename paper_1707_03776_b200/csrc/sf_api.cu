@@ -210,6 +210,7 @@ struct StepBufs {
     float *itp_row;        // its record row for the new level ([npoint])
     int64_t xa = 0, xb = 0;  // planes to compute (xa == xb: the handle's full range)
     int64_t xa2 = 0, xb2 = 0;  // optional second range in the same launch
+    int ctas_cap = 0;          // > 0: at most this many persistent TMA CTAs (split interior)
 };
 
 // Library-internal device allocations come from the device's stream-ordered memory pool
@@ -365,6 +366,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     L.variant = resolve_variant(h);
     L.vy = resolve_vy(h);
     L.ctas = resolve_ctas(h);
+    if (b.ctas_cap > 0 && b.ctas_cap < L.ctas) L.ctas = b.ctas_cap;
     L.sms = h->sms;
     L.damp = h->beta != nullptr;
     L.mode = mode;
@@ -896,6 +898,10 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         if (value < 0) return sf_set_error(SF_ERR_INVALID_ARG, "fuse max %d", value);
         h->fuse_max = value;
         return SF_OK;
+    case SF_OPT_COMM_SMS:
+        if (value < 0 || value > 64) return sf_set_error(SF_ERR_INVALID_ARG, "comm SMs %d", value);
+        h->comm_sms = value;
+        return SF_OK;
     default:
         return sf_set_error(SF_ERR_INVALID_ARG, "unknown option %d", option);
     }
@@ -1037,6 +1043,10 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
     StepBufs bb = b, bi = b;
     bb.xa = xa, bb.xb = xa + r, bb.xa2 = xb - r, bb.xb2 = xb;
     bi.xa = xa + r, bi.xb = xb - r;
+    // the persistent interior launch would hold every SM until it ends: leave some free so
+    // the NCCL exchange kernels (and the side-stream records) run concurrently
+    const int reserve = h->comm_sms >= 0 ? h->comm_sms : (h->nranks > 1 ? 8 : 0);
+    if (reserve > 0) bi.ctas_cap = std::max(1, h->sms - reserve);
     SF_CUDA_TRY(cudaEventRecord(h->ev_pre, st));
     SF_CUDA_TRY(cudaStreamWaitEvent(h->hi_stream, h->ev_pre, 0));
     if ((s = launch_step(h, bb, mode, h->hi_stream, &fused, fused_itp))) return s;

@@ -99,6 +99,7 @@ struct sf_handle {
     cudaStream_t comm_stream = nullptr, hi_stream = nullptr;
     cudaEvent_t ev_pre = nullptr, ev_bnd = nullptr, ev_xch = nullptr;
     int fuse_max = 256;
+    int comm_sms = -1;              // SMs left free by the split interior launch (-1: auto)
 };
 
 // error reporting (thread-local message)

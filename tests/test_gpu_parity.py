@@ -375,7 +375,7 @@ def test_fused_sparse_epilogue_mixed_receivers():
 @pytest.mark.parametrize("variant", [1, 2])
 def test_split_boundary_launches_bitwise(variant):
     """SF_OPT_SPLIT (the slab-mode schedule: boundary planes + their injection first, then
-    the interior) reorders work only: forward records/state and adjoint+gradient are
+    the interior, optionally on fewer persistent CTAs, SF_OPT_COMM_SMS) reorders work only: forward records/state and adjoint+gradient are
     bitwise identical to the single launch (fused small-set and standalone large-set
     sparse paths, sources and receivers in the boundary planes)."""
     p = synth.random_problem(3, (26, 30, 64), 8, 50, seed=31, nbl=5, nsrc=3, nrec=300)
@@ -386,12 +386,14 @@ def test_split_boundary_launches_bitwise(variant):
     p.m_true = (p.m * 0.93).astype(np.float32)
     d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
     out = {}
-    for split in (0, 1):
+    for split in (0, 1, 2):
         for fuse in (256, 0):
             prop = make_prop(p)
             prop.set_tuning(variant, 0, 0)
-            prop.set_option(2, split)
+            prop.set_option(2, min(split, 1))
             prop.set_option(3, fuse)
+            if split == 2:
+                prop.set_option(4, 60)  # interior launch leaves 60 SMs free (SF_OPT_COMM_SMS)
             rec, u, _ = prop.forward(dev(p.wavelet))
             g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
             torch.cuda.synchronize()
