@@ -132,6 +132,43 @@ def test_config1_full_grid_short_run_bench_launch():
     assert rel(ug[1], uo[1]) <= TOL and rel(ug[0], uo[0]) <= TOL
 
 
+def test_config3_full_grid_restart_bench_launch():
+    """configs[3] at its FULL grid (1024 x 512 x 512, so16, no damping layer, 8-layer model)
+    in the launch configuration bench.py times (persistent TMA kernel), restarted from a
+    seeded random state so that every point of the grid -- tile edges, ragged 14-row tiles,
+    chunk boundaries, the zero halo on all six faces -- carries signal; nt = 6 so the fp64
+    oracle finishes.  Records and both final levels compared over the whole grid."""
+    p = synth.make_config(3, nt=6)
+    rng = np.random.default_rng(33)
+    u0 = rng.standard_normal((2,) + tuple(p.shape), dtype=np.float32) * np.float32(1e-3)
+    o = oracle.forward(p, u_state=u0)
+    prop = make_prop(p)
+    assert prop.tuning()["variant"] == 2
+    u = dev(u0)
+    rec, u, _ = prop.forward(dev(p.wavelet), u=u)
+    torch.cuda.synchronize()
+    rg, ug = rec.cpu().numpy(), u.cpu().numpy()
+    prop.close()
+    assert rel(rg, o["rec"]) <= TOL, rel(rg, o["rec"])
+    assert rel(ug[1], o["u_state"][1]) <= TOL and rel(ug[0], o["u_state"][0]) <= TOL
+
+
+def test_config4_full_grid_short_gradient():
+    """configs[4] (one shot) at its FULL grid (400^3, so12, no damping, layered model +
+    3 anomalies, 400 x 400 surface receivers incl. the clamped last node, save every 3) in
+    the bench launch configuration; short record nt = 12, observed data from a 15 %
+    perturbed model (well-conditioned residual)."""
+    p = synth.make_config(4, nt=12)
+    d_obs = oracle.forward(p, m=(p.m * 0.85).astype(np.float32))["rec"].astype(np.float32)
+    go = oracle.gradient(p, d_obs, save_every=3)
+    prop = make_prop(p)
+    g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+    torch.cuda.synchronize()
+    prop.close()
+    assert rel(g.cpu().numpy(), go["grad"]) <= TOL, rel(g.cpu().numpy(), go["grad"])
+    assert abs(J - go["J"]) <= 1e-4 * go["J"]
+
+
 def test_config3_shape_so16_no_damping_reduced():
     """configs[3] structure (so16, no damping layer, layered model) at scale 1/8."""
     p = synth.make_config(3, scale=0.125, nt=80)
