@@ -126,6 +126,7 @@ def build_problem(nt_override=None, rank=0, nranks=1, cfg=1):
     import synth as S
     vmax = 2500.0
     sig = S.damping_profile(gshape, p.nbl, p.h, vmax)   # only a 1D x-profile part differs
+    p.sigma = S.damping_profiles_1d(gshape, p.nbl, p.h, vmax)   # separable form (global grid)
     x0 = rank * n0
     lo, hi = x0 - r, x0 + n0 + r
     idx = np.clip(np.arange(lo, hi), 0, gshape[0] - 1)
@@ -177,10 +178,14 @@ def run_ours(args):
     p, m_loc, eta_loc, gshape = build_problem(args.nt, rank, world, cfg)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
     m_d = dev(m_loc)
-    eta_d = None if eta_loc is None else dev(eta_loc)
+    # damping: the eta array (hoisted beta streamed, 20 B/pt) unless --sep regenerates beta
+    # from the separable profiles (sf_desc.sigma, 16 B/pt; measured slower on B200: the
+    # kernel is latency-bound there)
+    sep = eta_loc is not None and p.sigma is not None and args.sep
+    eta_d = None if (eta_loc is None or sep) else dev(eta_loc)
     prop = sf.Propagator(m_d, eta_d, shape=gshape, h=p.h, space_order=p.space_order, nt=p.nt,
                          dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords,
-                         comm=comm, rank=rank, nranks=world)
+                         comm=comm, rank=rank, nranks=world, sigma=p.sigma if sep else None)
     if args.split:
         prop.set_option(2, 1)
     wav = dev(p.wavelet)
@@ -195,8 +200,9 @@ def run_ours(args):
     if grad_mode:
         k = p.save_every
         # observed data from the true model (input preparation, outside the timed region)
-        prop_true = sf.Propagator(dev(p.m_true), eta_d, shape=gshape, h=p.h, space_order=p.space_order,
-                                  nt=p.nt, dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords)
+        prop_true = sf.Propagator(dev(p.m_true), None if eta_loc is None else dev(eta_loc), shape=gshape,
+                                  h=p.h, space_order=p.space_order, nt=p.nt, dt=p.dt,
+                                  src_coords=p.src_coords, rec_coords=p.rec_coords)
         d_obs, _, _ = prop_true.forward(wav)
         torch.cuda.synchronize()
         prop_true.close()
@@ -238,7 +244,7 @@ def run_ours(args):
     value = updates / (ms_max * 1e-3) / 1e9
 
     # roofline of the dominant kernel (stencil step): algorithmic bytes per launch
-    bpp = 20 if eta_loc is not None else 16      # u^n, u^{n-1}, out, c3(+beta) fp32
+    bpp = 20 if eta_d is not None else 16      # u^n, u^{n-1}, out, c3 (+beta array) fp32
     launch_ms = prof["stencil_ms"] / max(prof["stencil_launches"], 1)
     split = args.split or world > 1
     if split:
@@ -260,7 +266,7 @@ def run_ours(args):
         # end to end through the public C-ABI with HOST buffers (pinned), N=1 form
         e2e = None
         if world == 1 and not args.no_e2e and cfg in (0, 1, 3):
-            e2e = run_e2e(p, args)
+            e2e = run_e2e(p, args, sep)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(p, args.cpu_seconds)
@@ -268,8 +274,8 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded configs[1] model: two layers, 40-pt quadratic damping layer, "
-                    "15 Hz Ricker; no dataset in the paper)",
+            "data": f"synthetic (seeded {p.name} model of BASELINE configs[{cfg}], readings of "
+                    "SURVEY 8.0; no dataset in the paper)",
             "config": {"workload": WORKLOADS[cfg] + (f" (weak-scaled: {'x'.join(map(str, gshape))} "
                                                      f"global, slab per GPU)" if world > 1 else ""),
                        "grid": list(gshape), "space_order": p.space_order, "nt": p.nt,
@@ -278,6 +284,8 @@ def run_ours(args):
                              "4-5 fields streamed per update)" if npts_local * 4 > 126e6 else
                              "grid smaller than L2 (configs[0]: launch-bound toy)",
                        "propagations_per_step": passes,
+                       "damping": ("separable profiles (sf_desc.sigma): beta regenerated in-kernel" if sep else
+                                   "eta array (hoisted beta streamed)" if eta_d is not None else "none"),
                        "schedule": "split (boundary planes, then interior)" if (args.split or world > 1) else "single launch per step",
                        "kernel_tuning": tuning},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -307,17 +315,18 @@ def run_ours(args):
     return result
 
 
-def run_e2e(p, args):
+def run_e2e(p, args, sep=False):
     import torch
 
     import paper_1707_03776_b200 as sf
     pin = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).pin_memory()
-    m_h, d_h, w_h = pin(p.m), pin(p.damp), pin(p.wavelet)
+    m_h, w_h = pin(p.m), pin(p.wavelet)
+    d_h = None if (sep or p.damp is None) else pin(p.damp)
     rec_h = torch.empty((p.nt, p.rec_coords.shape[0]), dtype=torch.float32).pin_memory()
-    call = lambda: sf.forward_host(m_h.numpy(), d_h.numpy(), h=p.h, space_order=p.space_order,
-                                   nt=p.nt, dt=p.dt, src_coords=p.src_coords,
+    call = lambda: sf.forward_host(m_h.numpy(), None if d_h is None else d_h.numpy(), h=p.h,
+                                   space_order=p.space_order, nt=p.nt, dt=p.dt, src_coords=p.src_coords,
                                    wavelet=w_h.numpy(), rec_coords=p.rec_coords,
-                                   rec_out=rec_h.numpy())
+                                   rec_out=rec_h.numpy(), sigma=p.sigma if sep else None)
     call()  # warm-up (allocates the library's device cache)
     torch.cuda.synchronize()
     n = max(1, min(args.steps, 3))
@@ -332,10 +341,11 @@ def run_e2e(p, args):
     ms = max(e0.elapsed_time(e1), wall * 1e3)
     N = int(np.prod(p.shape))
     return {"value": round(N * (p.nt - 1) * n / (ms * 1e-3) / 1e9, 3), "unit": UNIT,
-            "h2d_bytes_per_step": int(m_h.numel() * 4 + d_h.numel() * 4 + w_h.numel() * 4),
+            "h2d_bytes_per_step": int(m_h.numel() * 4 + (0 if d_h is None else d_h.numel() * 4) + w_h.numel() * 4
+                                      + (sum(len(a) for a in p.sigma) * 4 if sep else 0)),
             "d2h_bytes_per_step": int(rec_h.numel() * 4), "steps": n,
-            "includes": "H2D m/eta/wavelet, handle setup (coefficient hoist, tables, CFL), "
-                        "forward, D2H record"}
+            "includes": "H2D m/" + ("sigma profiles" if sep else "eta") + "/wavelet, handle setup "
+                        "(coefficient hoist, tables, CFL), forward, D2H record"}
 
 
 def cpu_baseline(p, seconds):
@@ -405,6 +415,9 @@ def main():
                     help="1 GPU: run the slab schedule (boundary planes first, interior second) "
                          "to measure its cost without communication")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sep", action="store_true",
+                    help="damped configs: regenerate beta in-kernel from the separable damping "
+                         "profiles (16 B/pt) instead of streaming the hoisted beta array (20 B/pt)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-steps-nt", type=int, default=6,
                     help="--impl reference: time samples per timed step of the oracle")

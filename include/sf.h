@@ -79,6 +79,14 @@ typedef struct {
     const double *src_coords; /* host [nsrc][ndim]                                            */
     int nrec;                 /* number of receivers                                          */
     const double *rec_coords; /* host [nrec][ndim]                                            */
+    const float *sigma[3];    /* optional SEPARABLE damping (reading C7: eta = m sigma with    */
+                              /* sigma = sum over axes of a 1D profile): host [shape[a]]      */
+                              /* profiles sigma_a >= 0 [1/s] of the GLOBAL grid, a < ndim, all */
+                              /* given or all NULL; with them `damp` must be NULL.  The kernel */
+                              /* then regenerates beta = (1 - s)/(1 + s), s = sigma dt/2, from */
+                              /* the profiles instead of streaming a beta array: 16 instead of */
+                              /* 20 bytes per point-update.  eta is evaluated once (at the m  */
+                              /* given); gradients are d J / d m at that fixed eta (C13).      */
 } sf_desc;
 
 typedef struct sf_handle sf_handle;

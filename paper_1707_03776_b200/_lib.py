@@ -43,7 +43,7 @@ class SfDesc(ctypes.Structure):
                 ("space_order", ctypes.c_int), ("nt", ctypes.c_int), ("dt", ctypes.c_double),
                 ("m", ctypes.c_void_p), ("damp", ctypes.c_void_p), ("nsrc", ctypes.c_int),
                 ("src_coords", ctypes.c_void_p), ("nrec", ctypes.c_int),
-                ("rec_coords", ctypes.c_void_p)]
+                ("rec_coords", ctypes.c_void_p), ("sigma", ctypes.c_void_p * 3)]
 
 
 def build(force: bool = False, jobs: int = 8) -> str:

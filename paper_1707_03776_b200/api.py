@@ -86,11 +86,13 @@ class Propagator:
     ``shape`` is the (global) computational grid.  In slab mode (``comm`` given,
     nranks > 1) ``m``/``damp`` are the rank's local arrays with r halo planes on
     axis 0 ([n0_loc + 2r][n1][n2]) and every wavefield array is local likewise.
+    ``sigma``: optional separable damping (sf_desc.sigma) -- one host 1D float32 array per
+    axis of the GLOBAL grid, eta = m * (sigma_x + sigma_y (+ sigma_z)); exclusive with damp.
     """
 
     def __init__(self, m: torch.Tensor, damp: Optional[torch.Tensor], *, shape, h: float,
                  space_order: int, nt: int, dt: float, src_coords=None, rec_coords=None,
-                 comm: Optional[int] = None, rank: int = 0, nranks: int = 1):
+                 comm: Optional[int] = None, rank: int = 0, nranks: int = 1, sigma=None):
         self.shape = tuple(int(s) for s in shape)
         self.ndim = len(self.shape)
         self.h, self.space_order, self.nt, self.dt = float(h), int(space_order), int(nt), float(dt)
@@ -121,6 +123,13 @@ class Propagator:
         d.src_coords = self._src.ctypes.data if self.nsrc else None
         d.nrec = self.nrec
         d.rec_coords = self._rec.ctypes.data if self.nrec else None
+        self._sigma = None
+        if sigma is not None:
+            self._sigma = [np.ascontiguousarray(np.asarray(sa, dtype=np.float32).reshape(-1)) for sa in sigma]
+            if len(self._sigma) != self.ndim or any(sa.size != n for sa, n in zip(self._sigma, self.shape)):
+                raise ValueError("sigma: one profile per axis of the global grid")
+            for a, sa in enumerate(self._sigma):
+                d.sigma[a] = sa.ctypes.data
         self._desc = d
         hnd = ctypes.c_void_p()
         torch.cuda.synchronize()
@@ -270,7 +279,7 @@ def allreduce_gradient(comm: int, grad: torch.Tensor, J: Optional[float] = None,
 
 def forward_host(m: np.ndarray, damp: Optional[np.ndarray], *, h: float, space_order: int, nt: int,
                  dt: float, src_coords, wavelet: np.ndarray, rec_coords, rec_out: Optional[np.ndarray] = None,
-                 u_out: Optional[np.ndarray] = None, stream=None) -> np.ndarray:
+                 u_out: Optional[np.ndarray] = None, stream=None, sigma=None) -> np.ndarray:
     """sf_forward_host: end-to-end forward with HOST (numpy / pinned) buffers."""
     shape = m.shape
     nd = len(shape)
@@ -288,6 +297,11 @@ def forward_host(m: np.ndarray, damp: Optional[np.ndarray], *, h: float, space_o
         d.damp = damp.ctypes.data
     d.nsrc, d.src_coords = src.shape[0], src.ctypes.data if src.shape[0] else None
     d.nrec, d.rec_coords = rec.shape[0], rec.ctypes.data if rec.shape[0] else None
+    sig = None
+    if sigma is not None:
+        sig = [np.ascontiguousarray(np.asarray(sa, dtype=np.float32).reshape(-1)) for sa in sigma]
+        for a, sa in enumerate(sig):
+            d.sigma[a] = sa.ctypes.data
     wav = np.ascontiguousarray(wavelet, dtype=np.float32)
     if rec_out is None:
         rec_out = np.empty((nt, rec.shape[0]), np.float32)

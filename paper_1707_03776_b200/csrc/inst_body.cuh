@@ -13,11 +13,11 @@
 
 namespace {
 
-template <int VY, bool DAMP, int MODE>
+template <int VY, int DM, int MODE>
 cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    using C = sftma::Cfg<SF_R, VY, DAMP, MODE>;
-    auto kern = sftma::k_tma3d<SF_R, VY, DAMP, MODE>;
+    using C = sftma::Cfg<SF_R, VY, DM, MODE>;
+    auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -66,31 +66,39 @@ cudaError_t launch_generic(const SfLaunch &L, const SfStepArgs &a, cudaStream_t 
     return cudaGetLastError();
 }
 
-template <int VY>
-cudaError_t launch_tma_vy(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
+template <int VY, int DM>
+cudaError_t launch_tma_dm(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    if (L.damp) {
-        switch (L.mode) {
-        case SF_MODE_PLAIN: return launch_tma<VY, true, SF_MODE_PLAIN>(L, a, st);
-        case SF_MODE_SAVE: return launch_tma<VY, true, SF_MODE_SAVE>(L, a, st);
-        default: return launch_tma<VY, true, SF_MODE_GRAD>(L, a, st);
-        }
-    }
     switch (L.mode) {
-    case SF_MODE_PLAIN: return launch_tma<VY, false, SF_MODE_PLAIN>(L, a, st);
-    case SF_MODE_SAVE: return launch_tma<VY, false, SF_MODE_SAVE>(L, a, st);
-    default: return launch_tma<VY, false, SF_MODE_GRAD>(L, a, st);
+    case SF_MODE_PLAIN: return launch_tma<VY, DM, SF_MODE_PLAIN>(L, a, st);
+    case SF_MODE_SAVE: return launch_tma<VY, DM, SF_MODE_SAVE>(L, a, st);
+    default: return launch_tma<VY, DM, SF_MODE_GRAD>(L, a, st);
     }
 }
 
-template <int VY, bool DAMP, int MODE>
-int smem_of() { return sftma::Cfg<SF_R, VY, DAMP, MODE>::SMEM; }
+template <int VY>
+cudaError_t launch_tma_vy(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
+{
+    if (L.damp == SF_DAMP_ARRAY) return launch_tma_dm<VY, SF_DAMP_ARRAY>(L, a, st);
+    if (L.damp == SF_DAMP_SEP) return launch_tma_dm<VY, SF_DAMP_SEP>(L, a, st);
+    return launch_tma_dm<VY, SF_DAMP_NONE>(L, a, st);
+}
+
+template <int VY, int DM, int MODE>
+int smem_of() { return sftma::Cfg<SF_R, VY, DM, MODE>::SMEM; }
+
+template <int VY, int DM>
+int smem_dm(int mode)
+{
+    return mode == 0 ? smem_of<VY, DM, 0>() : mode == 1 ? smem_of<VY, DM, 1>() : smem_of<VY, DM, 2>();
+}
 
 template <int VY>
 int smem_vy(int damp, int mode)
 {
-    if (damp) return mode == 0 ? smem_of<VY, true, 0>() : mode == 1 ? smem_of<VY, true, 1>() : smem_of<VY, true, 2>();
-    return mode == 0 ? smem_of<VY, false, 0>() : mode == 1 ? smem_of<VY, false, 1>() : smem_of<VY, false, 2>();
+    if (damp == SF_DAMP_ARRAY) return smem_dm<VY, SF_DAMP_ARRAY>(mode);
+    if (damp == SF_DAMP_SEP) return smem_dm<VY, SF_DAMP_SEP>(mode);
+    return smem_dm<VY, SF_DAMP_NONE>(mode);
 }
 
 }  // namespace

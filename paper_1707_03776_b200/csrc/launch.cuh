@@ -17,7 +17,7 @@ struct SfLaunch {
     int vy;           // TMA: rows per thread, 2 (14-row tiles) or 1 (7-row tiles)
     int ctas;         // TMA: persistent CTAs (0 = one per SM)
     int sms;          // multiprocessors of the device
-    int damp;         // beta array present
+    int damp;         // SfDampMode: none, beta array, separable profiles
     int mode;         // SfMode
     int snap_slot;    // GRAD: snapshot slot for the 4D snapshot tensor map
     const SfTmaMaps *maps;

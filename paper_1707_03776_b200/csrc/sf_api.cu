@@ -368,7 +368,11 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     L.ctas = resolve_ctas(h);
     if (b.ctas_cap > 0 && b.ctas_cap < L.ctas) L.ctas = b.ctas_cap;
     L.sms = h->sms;
-    L.damp = h->beta != nullptr;
+    L.damp = h->beta ? SF_DAMP_ARRAY : h->sep ? SF_DAMP_SEP : SF_DAMP_NONE;
+    a.sigx = h->sig[0];
+    a.sigy = h->sig[1];
+    a.sigz = h->sig[2];
+    a.hdt = (float)(0.5 * h->dt);
     L.mode = mode;
     L.snap_slot = b.snap_slot;
     SfTmaMaps maps;
@@ -641,6 +645,18 @@ static sf_status validate_desc(const sf_desc *d)
     if (!(d->dt > 0.0)) return sf_set_error(SF_ERR_INVALID_ARG, "dt = %g <= 0", d->dt);
     if (!(d->h > 0.0)) return sf_set_error(SF_ERR_INVALID_ARG, "h = %g <= 0", d->h);
     if (d->nsrc < 0 || d->nrec < 0) return sf_set_error(SF_ERR_INVALID_ARG, "negative point count");
+    if (d->sigma[0] || d->sigma[1] || d->sigma[2]) {
+        if (d->damp) return sf_set_error(SF_ERR_INVALID_ARG, "damp and sigma profiles are exclusive");
+        for (int a = 0; a < 3; ++a) {
+            if ((a < d->ndim) != (d->sigma[a] != nullptr))
+                return sf_set_error(SF_ERR_INVALID_ARG, "sigma[%d] must be %s", a, a < d->ndim ? "given" : "NULL");
+            if (a < d->ndim)
+                for (int64_t i = 0; i < d->shape[a]; ++i)
+                    if (!(d->sigma[a][i] >= 0.0f) || !std::isfinite(d->sigma[a][i]))
+                        return sf_set_error(SF_ERR_INVALID_ARG, "sigma[%d][%lld] = %g", a, (long long)i,
+                                            (double)d->sigma[a][i]);
+        }
+    }
     return SF_OK;
 }
 
@@ -652,6 +668,7 @@ extern "C" void sf_destroy(sf_handle *h)
     cudaDeviceSynchronize();
     cudaFree(h->c3);
     cudaFree(h->beta);
+    for (int a = 0; a < 3; ++a) cudaFree(h->sig[a]);
     cudaFree(h->partial);
     cudaFree(h->dJ);
     free_sparse(h->src);
@@ -690,8 +707,29 @@ static sf_status create_common(const sf_desc *d, sf_handle *h)
     // coefficient hoisting (same bytes as streaming m and eta)
     SF_CUDA_TRY(cudaMalloc(&h->c3, sizeof(float) * h->N));
     h->damp = d->damp != nullptr;
-    if (h->damp) SF_CUDA_TRY(cudaMalloc(&h->beta, sizeof(float) * h->N));
-    k_hoist<<<1184, 256>>>(d->m, d->damp, h->N, d->dt, h->c3, h->beta);
+    h->sep = d->sigma[0] != nullptr;
+    if (h->sep) {
+        // local profiles: x over the buffer planes (slab halo planes outside the global grid
+        // get 0: they are never computed), y and z whole
+        const int nd = d->ndim;
+        const int64_t off = h->x0 - (h->nranks > 1 ? h->r : 0);
+        std::vector<float> px((size_t)h->nb[0], 0.0f);
+        for (int64_t i = 0; i < h->nb[0]; ++i) {
+            const int64_t g = off + i;
+            if (g >= 0 && g < d->shape[0]) px[(size_t)i] = d->sigma[0][g];
+        }
+        sf_status s;
+        if ((s = upload(&h->sig[0], px))) return s;
+        for (int a = 1; a < nd; ++a) {
+            std::vector<float> pa(d->sigma[a], d->sigma[a] + d->shape[a]);
+            if ((s = upload(&h->sig[a == nd - 1 ? 2 : 1], pa))) return s;
+        }
+        const int64_t n1 = nd == 3 ? h->nb[1] : 1, n2 = nd == 3 ? h->nb[2] : h->nb[1];
+        k_hoist_sep<<<1184, 256>>>(d->m, h->N, n1, n2, d->dt, h->sig[0], h->sig[1], h->sig[2], h->c3);
+    } else {
+        if (h->damp) SF_CUDA_TRY(cudaMalloc(&h->beta, sizeof(float) * h->N));
+        k_hoist<<<1184, 256>>>(d->m, d->damp, h->N, d->dt, h->c3, h->beta);
+    }
     SF_CUDA_TRY(cudaGetLastError());
     // min m over the computed planes -> CFL (SF_ERR_CFL) and positivity (SF_ERR_INVALID_ARG)
     unsigned int *dmin = nullptr;

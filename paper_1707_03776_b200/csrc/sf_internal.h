@@ -71,7 +71,9 @@ struct sf_handle {
     SfWeights w{};
     float *c3 = nullptr;
     float *beta = nullptr;
-    bool damp = false;
+    bool damp = false;              // hoisted beta array (sf_desc.damp given)
+    bool sep = false;               // separable damping profiles (sf_desc.sigma given)
+    float *sig[3] = {nullptr, nullptr, nullptr};  // local profiles: buffer planes, y, z
     SfSparse src, rec;
     double *partial = nullptr;  // residual partial sums
     double *dJ = nullptr;

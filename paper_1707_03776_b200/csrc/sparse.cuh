@@ -157,6 +157,23 @@ __global__ void k_hoist(const float *__restrict__ m, const float *__restrict__ d
     }
 }
 
+// hoisted c3 with separable damping (sf_desc.sigma, reading C7): eta = m sigma,
+// sigma = sx[x] + sy[y] + sz[z] (fp64), A = m + eta dt/2, c3 = dt^2/A; beta is regenerated
+// in the stencil kernels (sf_beta_sep).  2D: n1 == 1 and sy == NULL.
+__global__ void k_hoist_sep(const float *__restrict__ m, int64_t n, int64_t n1, int64_t n2, double dt,
+                            const float *__restrict__ sx, const float *__restrict__ sy,
+                            const float *__restrict__ sz, float *__restrict__ c3)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = i / (n1 * n2), y = (i / n2) % n1, z = i % n2;
+        const double sig = (double)sx[x] + (sy ? (double)sy[y] : 0.0) + (double)sz[z];
+        const double mm = m[i];
+        const double A = mm + 0.5 * (mm * sig) * dt;
+        c3[i] = (float)(dt * dt / A);
+    }
+}
+
 // min over a float array (positive floats order like their bit patterns; non-positive
 // values and NaN are reported through the flag)
 __global__ void k_min_m(const float *__restrict__ m, int64_t n, unsigned int *__restrict__ minbits,

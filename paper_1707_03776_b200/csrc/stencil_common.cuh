@@ -25,6 +25,8 @@ struct SfWeights {
 };
 
 enum SfMode { SF_MODE_PLAIN = 0, SF_MODE_SAVE = 1, SF_MODE_GRAD = 2 };
+// damping representation: none (beta = 1), hoisted beta array, separable profiles
+enum SfDampMode { SF_DAMP_NONE = 0, SF_DAMP_ARRAY = 1, SF_DAMP_SEP = 2 };
 
 // in-plane term at radius k for 3D: ((ym + yp) + (zm + zp)) - 4u, as one fma
 __device__ __forceinline__ float sf_inplane3(float ym, float yp, float zm, float zp, float u)
@@ -110,12 +112,32 @@ __device__ __forceinline__ f2_t sf_xterm_x2(f2_t xm, f2_t xp, f2_t u, f2_t m2)
     return fma2(m2, u, add2(xm, xp));
 }
 
+// beta regenerated from separable damping profiles (sf_desc.sigma, reading C7):
+//   s = ((sx + sy) + sz) * (dt/2),  beta = (1 - s) * rcp(1 + s)
+// rcp.approx.ftz (one MUFU op, rel. error < 2^-22) instead of an IEEE division; every
+// variant uses this one function (or its lane-wise identical fp32x2 form), so they agree
+// bitwise.  The argument 1 + s lies in [1, 2) (s = sigma dt/2 < 1 for any stable damping),
+// so flush-to-zero never applies (the non-ftz form adds seven range-fixup instructions).
+__device__ __forceinline__ float sf_rcp(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sf_beta_sep(float sx, float sy, float sz, float hdt)
+{
+    const float s = __fmul_rn(__fadd_rn(__fadd_rn(sx, sy), sz), hdt);
+    return __fmul_rn(__fsub_rn(1.0f, s), sf_rcp(__fadd_rn(1.0f, s)));
+}
+
 // Kernel parameter block shared by all stencil variants.
 struct SfStepArgs {
     const float *cur;      // u^n (read, with neighbours)
     float *out;            // old level on input (u^{n-1}), new level on output (in place)
     const float *c3;       // hoisted dt^2 / A
-    const float *beta;     // hoisted (m - eta dt/2) / A, or NULL (== 1)
+    const float *beta;     // hoisted (m - eta dt/2) / A, or NULL (== 1, or separable below)
+    const float *sigx, *sigy, *sigz;  // separable damping profiles of the buffer (or NULL)
+    float hdt;             // dt / 2 (fp32) for sf_beta_sep
     float *snap_out;       // SAVE: snapshot slot to write (== out values), else NULL
     const float *snap_in;  // GRAD: u^n snapshot slot
     float *grad;           // GRAD: gradient accumulator

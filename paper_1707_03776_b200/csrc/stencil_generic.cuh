@@ -39,7 +39,9 @@ k_generic3d(SfStepArgs a)
     const float lap = __fadd_rn(P, X);
     const float old = a.out[idx];
     const float c3 = __ldg(a.c3 + idx);
-    const float beta = a.beta ? __ldg(a.beta + idx) : 1.0f;
+    const float beta = a.beta ? __ldg(a.beta + idx)
+                              : a.sigx ? sf_beta_sep(__ldg(a.sigx + x), __ldg(a.sigy + y), __ldg(a.sigz + z), a.hdt)
+                                       : 1.0f;
     const float o = sf_update(u, old, beta, c3, lap);
     if (MODE == SF_MODE_GRAD) {
         const float S = sf_d2(u, old, beta, c3, lap);
@@ -79,7 +81,10 @@ k_generic2d(SfStepArgs a)
     const float lap = __fadd_rn(P, X);
     const float old = a.out[idx];
     const float c3 = __ldg(a.c3 + idx);
-    const float beta = a.beta ? __ldg(a.beta + idx) : 1.0f;
+    // 2D separable damping: profiles of x and z (sigy unused: sy = 0 exactly)
+    const float beta = a.beta ? __ldg(a.beta + idx)
+                              : a.sigx ? sf_beta_sep(__ldg(a.sigx + x), 0.0f, __ldg(a.sigz + z), a.hdt)
+                                       : 1.0f;
     const float o = sf_update(u, old, beta, c3, lap);
     if (MODE == SF_MODE_GRAD) {
         const float S = sf_d2(u, old, beta, c3, lap);

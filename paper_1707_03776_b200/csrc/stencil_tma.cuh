@@ -9,7 +9,8 @@
 //       - u^n plane p with its (y, z) halo into a DU-deep u ring: box (TZ + 2 HZ) x (BY + 2R);
 //         the TMA out-of-bounds zero fill IS the zero ghost halo (reading C6);
 //       - old / c3 / beta (+ snapshot / gradient in GRAD mode) of output plane q = p - R
-//         into a DC-deep coefficient ring;
+//         into a DC-deep coefficient ring (with separable damping, DM = SF_DAMP_SEP, beta
+//         is regenerated from three 1D profiles instead: 16 B/pt instead of 20);
 //     completion via mbarrier transaction counts (full), slot reuse via one arrive per
 //     consumer warp (empty);
 //   * each consumer warp (VY rows, VZ consecutive z per lane) pushes its own u values of
@@ -123,8 +124,9 @@ struct Geo {
     static constexpr int HZ = ((R + 3) / 4) * 4;        // z halo rounded up to 16 B
 };
 
-template <int R, int VY, bool DAMP, int MODE>
+template <int R, int VY, int DM, int MODE>
 struct Cfg {
+    static constexpr bool DAMP = (DM == SF_DAMP_ARRAY);  // beta array streamed
     using G = Geo<R, VY>;
     static constexpr int VZ = G::VZ, NW = G::NW, BY = G::BY, TZ = G::TZ, HZ = G::HZ;
     static constexpr int W = TZ + 2 * HZ;               // smem row pitch of the u tile
@@ -192,6 +194,14 @@ __device__ __forceinline__ float hi2(f2_t v)
     return b;
 }
 
+// fp32x2 form of sf_beta_sep: sxy = sx + sy (both lanes), sz = the lanes' sigma_z
+__device__ __forceinline__ f2_t beta_sep2(f2_t sxy, f2_t sz, f2_t hdt2, f2_t one2, f2_t m1)
+{
+    const f2_t sh = mul2(add2(sxy, sz), hdt2);
+    const f2_t den = add2(one2, sh);
+    return mul2(fma2(m1, sh, one2), pk2(sf_rcp(lo2(den)), sf_rcp(hi2(den))));
+}
+
 // Work split: per tile the planes [xa, xb) then [xa2, xb2) (PT in all), cut into `nchunk`
 // chunks of `chunk` planes; item it = (tile it % tiles, chunk it / tiles); CTA b takes items
 // b, b + G, b + 2G, ...  Consecutive CTAs work on y/z-neighbouring tiles of the same chunk at
@@ -219,14 +229,15 @@ __device__ __forceinline__ Seg next_seg(int64_t w, int64_t end, int64_t P1, int6
     return s;
 }
 
-template <int R, int VY, bool DAMP, int MODE>
-__global__ void __launch_bounds__(Cfg<R, VY, DAMP, MODE>::THREADS, 1)
+template <int R, int VY, int DM, int MODE>
+__global__ void __launch_bounds__(Cfg<R, VY, DM, MODE>::THREADS, 1)
 k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_old,
         const __grid_constant__ CUtensorMap tm_c3, const __grid_constant__ CUtensorMap tm_beta,
         const __grid_constant__ CUtensorMap tm_snap, const __grid_constant__ CUtensorMap tm_grad,
         const SfStepArgs a, const int snap_slot, const int chunk, const int nchunk)
 {
-    using C = Cfg<R, VY, DAMP, MODE>;
+    using C = Cfg<R, VY, DM, MODE>;
+    constexpr bool DAMP = C::DAMP;
     constexpr int VZ = C::VZ, NJ = VZ / 2, NW = C::NW, BY = C::BY, TZ = C::TZ, HZ = C::HZ;
     constexpr int Q = C::Q, W = C::W, DU = C::DU, DC = C::DC;
     const int PD = a.l2_prefetch;  // planes of L2 prefetch beyond the smem ring (0 = off)
@@ -350,6 +361,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     Wk[0] = 0ull;
     const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f);
     const f2_t NG = pk2(-a.gscale, -a.gscale), ONE2 = pk2(1.f, 1.f);
+    const f2_t HDT2 = pk2(a.hdt, a.hdt);
     constexpr int QINF = 0x7fffffff;
 
     for (int it = blockIdx.x; it < items; it += gridDim.x)
@@ -361,6 +373,22 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
         const int zg = z0 + VZ * lane;
         const int yg = y0 + VY * wy;
         const bool zact = zg < a.n2;
+        // separable damping: profiles of the own rows / columns (clamped reads at ragged edges)
+        float SY[VY];
+        f2_t SZ[NJ], BYZ[VY][NJ];
+        if (DM == SF_DAMP_SEP) {
+#pragma unroll
+            for (int j = 0; j < VY; ++j) SY[j] = __ldg(a.sigy + min(yg + j, (int)a.n1 - 1));
+            const int zc = min(zg, (int)a.n2 - VZ);
+#pragma unroll
+            for (int jp = 0; jp < NJ; ++jp) SZ[jp] = pk2(__ldg(a.sigz + zc + 2 * jp), __ldg(a.sigz + zc + 2 * jp + 1));
+#pragma unroll
+            for (int j = 0; j < VY; ++j) {
+                const float s0 = __fadd_rn(0.0f, SY[j]);
+#pragma unroll
+                for (int jp = 0; jp < NJ; ++jp) BYZ[j][jp] = beta_sep2(pk2(s0, s0), SZ[jp], HDT2, ONE2, M1);
+            }
+        }
         bool act[VY];
 #pragma unroll
         for (int j = 0; j < VY; ++j) act[j] = zact && (yg + j < a.n1);
@@ -397,6 +425,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                     if (UNR == Q) sl = s2;
                     const int p = qa - R + i;
                     const bool outp = (i >= 2 * R);
+                    // separable damping: sigma_x of the output plane q = p - R (issued early)
+                    const float sxq = (DM == SF_DAMP_SEP && outp) ? __ldg(a.sigx + (p - R)) : 0.0f;
                     // ---- (1) in-plane partial of output plane q = p - R: its u tile is
                     // resident (arrived R planes ago), so this overlaps the wait for plane p
                     f2_t Pin[VY][NJ], Uq[VY][NJ];
@@ -510,6 +540,18 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             if (DAMP) {
                                 ldp<VZ>(cp + 2 * PF + j * TZ, bv[j]);
                                 nxt = 3;
+                            } else if (DM == SF_DAMP_SEP) {
+                                // beta regenerated from the separable profiles (== sf_beta_sep);
+                                // planes with sigma_x = 0 (warp-uniform) reuse the per-segment
+                                // beta(0, sigma_y, sigma_z) -- the same bits, as 0 + sy == sy
+                                if (sxq == 0.0f) {
+#pragma unroll
+                                    for (int jp = 0; jp < NJ; ++jp) bv[j][jp] = BYZ[j][jp];
+                                } else {
+                                    const f2_t sxy = pk2(__fadd_rn(sxq, SY[j]), __fadd_rn(sxq, SY[j]));
+#pragma unroll
+                                    for (int jp = 0; jp < NJ; ++jp) bv[j][jp] = beta_sep2(sxy, SZ[jp], HDT2, ONE2, M1);
+                                }
                             } else {
 #pragma unroll
                                 for (int jp = 0; jp < NJ; ++jp) bv[j][jp] = ONE2;

@@ -24,16 +24,18 @@ def main():
     ap.add_argument("--vy", default="2")
     ap.add_argument("--ctas", default="0")
     ap.add_argument("--grad", action="store_true", help="time the adjoint with fused gradient")
+    ap.add_argument("--sep", action="store_true", help="separable damping profiles (16 B/pt)")
     ap.add_argument("--random-init", action="store_true",
                     help="start from a random (incompressible) wavefield instead of zeros")
     args = ap.parse_args()
     p = synth.make_config(args.config, scale=args.scale, nt=args.nt)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
-    prop = sf.Propagator(dev(p.m), None if p.damp is None else dev(p.damp), shape=p.shape, h=p.h,
+    sep = args.sep and p.sigma is not None
+    prop = sf.Propagator(dev(p.m), None if (p.damp is None or sep) else dev(p.damp), shape=p.shape, h=p.h,
                          space_order=p.space_order, nt=p.nt, dt=p.dt, src_coords=p.src_coords,
-                         rec_coords=p.rec_coords)
+                         rec_coords=p.rec_coords, sigma=p.sigma if sep else None)
     N = int(np.prod(p.shape))
-    bpp = 20 if p.damp is not None else 16
+    bpp = 20 if (p.damp is not None and not sep) else 16
     wav = dev(p.wavelet)
     out = []
     snaps = None

@@ -28,7 +28,7 @@ from typing import Optional
 import numpy as np
 
 __all__ = [
-    "ricker", "damping_profile", "pad_edge", "Problem", "make_config",
+    "ricker", "damping_profile", "damping_profiles_1d", "pad_edge", "Problem", "make_config",
     "random_problem", "CONFIG_NAMES",
 ]
 
@@ -53,21 +53,30 @@ def pad_edge(v: np.ndarray, nbl: int, axes=None) -> np.ndarray:
     return np.pad(v, pw, mode="edge")
 
 
-def damping_profile(shape_comp, nbl: int, h: float, vmax: float) -> np.ndarray:
-    """sigma(x) = sum_axes sigma_max (d_a/nbl)^2, d_a = points beyond the physical
-    region on axis a (0 inside); sigma_max = 3 vmax ln(1e3) / (2 nbl h)  (reading C7).
-    Returns sigma in 1/s (eta = m * sigma is formed by the caller)."""
-    sig = np.zeros(shape_comp, dtype=np.float64)
-    if nbl == 0:
-        return sig
-    smax = 3.0 * vmax * math.log(1e3) / (2.0 * nbl * h)
-    for a, n in enumerate(shape_comp):
+def damping_profiles_1d(shape_comp, nbl: int, h: float, vmax: float) -> list:
+    """Per-axis damping profiles sigma_a(i) = sigma_max (d_a/nbl)^2 [1/s], d_a = points
+    beyond the physical region on axis a (0 inside), sigma_max = 3 vmax ln(1e3)/(2 nbl h)
+    (reading C7), rounded to fp32: the separable damping input (sf_desc.sigma)."""
+    out = []
+    for n in shape_comp:
+        if nbl == 0:
+            out.append(np.zeros(n, dtype=np.float32))
+            continue
+        smax = 3.0 * vmax * math.log(1e3) / (2.0 * nbl * h)
         i = np.arange(n, dtype=np.float64)
         d = np.maximum(np.maximum(nbl - i, i - (n - 1 - nbl)), 0.0)
-        prof = smax * (d / nbl) ** 2
+        out.append((smax * (d / nbl) ** 2).astype(np.float32))
+    return out
+
+
+def damping_profile(shape_comp, nbl: int, h: float, vmax: float) -> np.ndarray:
+    """sigma(x) = sum_axes sigma_a(x_a) (the fp32 1D profiles above, summed in fp64);
+    eta = m * sigma is formed by the caller.  Returns sigma in 1/s."""
+    sig = np.zeros(shape_comp, dtype=np.float64)
+    for a, prof in enumerate(damping_profiles_1d(shape_comp, nbl, h, vmax)):
         sh = [1] * len(shape_comp)
-        sh[a] = n
-        sig = sig + prof.reshape(sh)
+        sh[a] = len(prof)
+        sig = sig + prof.astype(np.float64).reshape(sh)
     return sig
 
 
@@ -90,6 +99,7 @@ class Problem:
     nbl: int = 0
     m_true: Optional[np.ndarray] = None  # gradient configs: model generating d_obs
     extra: dict = field(default_factory=dict)
+    sigma: Optional[list] = None       # separable form of damp: damp = m * sum_a sigma[a]
 
     @property
     def npoints(self) -> int:
@@ -135,9 +145,11 @@ def make_config(i: int, scale: float = 1.0, nt: Optional[int] = None, shot: int 
         rec = np.stack([np.arange(nrec) * h * (nphys - 1) / (nrec - 1) + nbl * h,
                         np.full(nrec, 20.0 + nbl * h)], axis=1)
         wav = ricker(ntt, dt, 10.0)[:, None]
-        return Problem("C1_2d_fwd", 2, shape, h, 4, ntt, dt, m.astype(np.float32),
-                       damp.astype(np.float32), src.astype(np.float32), wav,
-                       rec.astype(np.float32), 0, nbl)
+        p0 = Problem("C1_2d_fwd", 2, shape, h, 4, ntt, dt, m.astype(np.float32),
+                     damp.astype(np.float32), src.astype(np.float32), wav,
+                     rec.astype(np.float32), 0, nbl)
+        p0.sigma = damping_profiles_1d(shape, nbl, h, vmax)
+        return p0
     if i in (1, 2):
         nphys = _scaled(256, scale)
         nbl = _scaled(40, scale, lo=4)
@@ -177,6 +189,7 @@ def make_config(i: int, scale: float = 1.0, nt: Optional[int] = None, shot: int 
         p = Problem(CONFIG_NAMES[i], 3, shape, h, 8, ntt, dt, m.astype(np.float32),
                     damp.astype(np.float32), src.astype(np.float32), wav,
                     rec.astype(np.float32), 4 if i == 2 else 0, nbl)
+        p.sigma = damping_profiles_1d(shape, nbl, h, vmax)
         if i == 2:
             p.m_true = (1.0 / pad_edge(vtrue, nbl) ** 2).astype(np.float32)
         return p
@@ -269,7 +282,10 @@ def random_problem(ndim: int, shape, space_order: int, nt: int, *, seed: int = 0
         wav = rng.standard_normal((nt, nsrc)).astype(np.float32)
     else:
         wav = np.stack([ricker(nt, dt, f0) for _ in range(nsrc)], axis=1)
-    return Problem(f"rand{ndim}d", ndim, shape, h, space_order, nt, dt,
-                   m.astype(np.float32), None if eta is None else eta.astype(np.float32),
-                   src.astype(np.float32), wav.astype(np.float32), rec.astype(np.float32),
-                   0, nbl)
+    pr = Problem(f"rand{ndim}d", ndim, shape, h, space_order, nt, dt,
+                 m.astype(np.float32), None if eta is None else eta.astype(np.float32),
+                 src.astype(np.float32), wav.astype(np.float32), rec.astype(np.float32),
+                 0, nbl)
+    if eta is not None:
+        pr.sigma = damping_profiles_1d(shape, nbl, h, vmax)
+    return pr

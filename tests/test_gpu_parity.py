@@ -441,3 +441,77 @@ def test_split_boundary_launches_bitwise(variant):
         assert all(np.array_equal(a, b) for a, b in zip(v[:3], base[:3])) and v[3] == base[3], k
     go = oracle.gradient(p, d_obs, save_every=3)
     assert rel(base[2], go["grad"]) <= TOL
+
+
+# ------------------------------------------------------------ separable damping (16 B/pt)
+def make_prop_sep(p, m=None, **kw):
+    """Same problem, damping given as the separable profiles (sf_desc.sigma) instead of
+    the eta array: beta regenerated in-kernel, c3 hoisted from m and the profiles."""
+    m = p.m if m is None else m
+    return sf().Propagator(dev(m), None, shape=p.shape, h=p.h, space_order=p.space_order, nt=p.nt,
+                           dt=p.dt, src_coords=p.src_coords.astype(np.float64),
+                           rec_coords=p.rec_coords.astype(np.float64), sigma=p.sigma, **kw)
+
+
+@pytest.mark.parametrize("so", [4, 8, 16])
+def test_separable_damping_forward(so):
+    """Separable damping (reading C7 structure): both variants vs the oracle fed
+    the equivalent eta array; TMA and generic bitwise equal (one sf_beta_sep); close to
+    the beta-array path (the two differ only by fp32 rounding of eta and of beta)."""
+    p = synth.random_problem(3, (37, 45, 132), so, 60, seed=40 + so, nbl=6, nsrc=2, nrec=9)
+    ro, uo, _ = oracle_forward(p)
+    out = {}
+    for variant, vy, ctas in ((1, 0, 0), (2, 2, 0), (2, 2, 3), (2, 1, 0)):
+        prop = make_prop_sep(p)
+        prop.set_tuning(variant, vy, ctas)
+        rec, u, _ = prop.forward(dev(p.wavelet))
+        torch.cuda.synchronize()
+        out[(variant, vy, ctas)] = (rec.cpu().numpy(), u.cpu().numpy())
+        prop.close()
+        assert rel(out[(variant, vy, ctas)][0], ro) <= TOL
+        assert rel(out[(variant, vy, ctas)][1][1], uo[1]) <= TOL
+    base = out[(1, 0, 0)]
+    for k, v in out.items():
+        assert np.array_equal(v[0], base[0]) and np.array_equal(v[1], base[1]), k
+    ra, ua, _ = gpu_forward(p)
+    assert rel(base[0], ra) <= 1e-5 and rel(base[1][1], ua[1]) <= 1e-5
+
+
+def test_separable_damping_2d_and_gradient():
+    """2D (generic kernel, sigma_x and sigma_z) forward, and the 3D gradient (SAVE and
+    GRAD modes of the TMA kernel) with separable damping, vs the oracle."""
+    p2 = synth.random_problem(2, (90, 110), 8, 120, seed=5, nbl=10, nsrc=2, nrec=11)
+    ro, uo, _ = oracle_forward(p2)
+    prop = make_prop_sep(p2)
+    rec, u, _ = prop.forward(dev(p2.wavelet))
+    torch.cuda.synchronize()
+    assert rel(rec.cpu().numpy(), ro) <= TOL and rel(u.cpu().numpy()[1], uo[1]) <= TOL
+    prop.close()
+    p = synth.random_problem(3, (30, 34, 64), 8, 60, seed=6, nbl=5, nsrc=2, nrec=25)
+    p.m_true = (p.m * 0.9).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    go = oracle.gradient(p, d_obs, save_every=3)
+    for variant in (2, 1):
+        prop = make_prop_sep(p)
+        prop.set_tuning(variant, 0, 0)
+        g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+        torch.cuda.synchronize()
+        assert rel(g.cpu().numpy(), go["grad"]) <= TOL, (variant, rel(g.cpu().numpy(), go["grad"]))
+        assert abs(J - go["J"]) <= 1e-4 * go["J"]
+        prop.close()
+
+
+def test_separable_damping_errors():
+    p = synth.random_problem(3, (16, 16, 16), 4, 10, seed=0, nbl=3)
+    S = sf()
+    kw = dict(shape=p.shape, h=p.h, space_order=4, nt=10, dt=p.dt)
+    with pytest.raises(S.SfError) as e:      # damp and sigma are exclusive
+        S.Propagator(dev(p.m), dev(p.damp), sigma=p.sigma, **kw)
+    assert e.value.status == "SF_ERR_INVALID_ARG"
+    bad = [s.copy() for s in p.sigma]
+    bad[1][2] = -1.0
+    with pytest.raises(S.SfError) as e:      # negative profile value
+        S.Propagator(dev(p.m), None, sigma=bad, **kw)
+    assert e.value.status == "SF_ERR_INVALID_ARG"
+    with pytest.raises(ValueError):          # wrong number / length of profiles
+        S.Propagator(dev(p.m), None, sigma=p.sigma[:2], **kw)
