@@ -135,6 +135,19 @@ SF_API size_t sf_gradient_workspace_bytes(const sf_handle *h, int save_every);
 SF_API sf_status sf_gradient(sf_handle *h, const float *wavelet, const float *d_obs, float *grad,
                       double *J, void *ws, size_t ws_bytes, int save_every, void *stream);
 
+/* Memory-bounded form of sf_gradient: checkpoint-recompute.  The forward
+ * stores only the state pair (u^{b-1}, u^b) at every segment start b = 0, S, 2S, ...
+ * (segment = S time steps, a positive multiple of save_every); the backward sweep
+ * recomputes each segment's forward from its checkpoint, keeping that segment's
+ * snapshots only, and runs its adjoint steps.  Workspace ~ (2 ceil((nt-1)/S) + S/save_every
+ * + 5) N floats instead of ((nt-1)/save_every + 5) N; one extra forward propagation.
+ * The kernels are deterministic, so grad and *J are BITWISE equal to sf_gradient's.
+ * SF_ERR_INVALID_ARG if segment is not a positive multiple of save_every. */
+SF_API size_t sf_gradient_ckpt_workspace_bytes(const sf_handle *h, int save_every, int segment);
+SF_API sf_status sf_gradient_ckpt(sf_handle *h, const float *wavelet, const float *d_obs, float *grad,
+                                  double *J, void *ws, size_t ws_bytes, int save_every, int segment,
+                                  void *stream);
+
 /* Flat end-to-end form with HOST buffers (desc->m / desc->damp are HOST pointers here):
  * uploads m, damp and the wavelet, creates a handle, runs sf_forward from a zero state,
  * downloads rec [nt][nrec] and (optionally) u_final [2][N] = (u^{nt-2}, u^{nt-1}).

@@ -22,7 +22,8 @@ STATUS = {0: "SF_OK", 1: "SF_ERR_INVALID_ARG", 2: "SF_ERR_SHAPE", 3: "SF_ERR_ORD
 
 # every symbol include/sf.h declares
 EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint", "sf_residual",
-           "sf_gradient_workspace_bytes", "sf_gradient", "sf_forward_host", "sf_set_profiling",
+           "sf_gradient_workspace_bytes", "sf_gradient", "sf_gradient_ckpt_workspace_bytes",
+           "sf_gradient_ckpt", "sf_forward_host", "sf_set_profiling",
            "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_create_slab",
            "sf_allreduce_gradient", "sf_last_error", "sf_version"]
@@ -74,6 +75,7 @@ def lib():
             "sf_adjoint": [P, P, P, P, P, I, P, P],
             "sf_residual": [P, P, P, P, P, P],
             "sf_gradient": [P, P, P, P, P, P, Z, I, P],
+            "sf_gradient_ckpt": [P, P, P, P, P, P, Z, I, I, P],
             "sf_forward_host": [P, P, P, P, P],
             "sf_set_profiling": [P, I],
             "sf_get_profile": [P, P, P, P, I],
@@ -97,6 +99,8 @@ def lib():
         L.sf_destroy.argtypes = [P]
         L.sf_destroy.restype = None
         L.sf_gradient_workspace_bytes.argtypes = [P, I]
+        L.sf_gradient_ckpt_workspace_bytes.argtypes = [P, I, I]
+        L.sf_gradient_ckpt_workspace_bytes.restype = ctypes.c_size_t
         L.sf_gradient_workspace_bytes.restype = Z
         L.sf_last_error.argtypes = []
         L.sf_last_error.restype = ctypes.c_char_p

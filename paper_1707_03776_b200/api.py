@@ -262,6 +262,30 @@ class Propagator:
                                 int(save_every), _stream(stream)))
         return grad, J.value
 
+    def gradient_ckpt_workspace_bytes(self, save_every: int, segment: int) -> int:
+        return int(lib().sf_gradient_ckpt_workspace_bytes(self._h, int(save_every), int(segment)))
+
+    def gradient_ckpt(self, wavelet: torch.Tensor, d_obs: torch.Tensor, *, save_every: int = 1,
+                      segment: int, grad: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
+                      stream=None):
+        """sf_gradient_ckpt (checkpoint-recompute, `segment` steps per checkpoint): returns
+        (grad, J), bitwise equal to gradient()."""
+        _dev(d_obs, "d_obs", (self.nt, self.nrec))
+        if self.nsrc:
+            _dev(wavelet, "wavelet", (self.nt, self.nsrc))
+        nbytes = self.gradient_ckpt_workspace_bytes(save_every, segment)
+        if nbytes == 0:
+            raise ValueError("segment must be a positive multiple of save_every")
+        if ws is None or ws.numel() * ws.element_size() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        grad = torch.empty(self.local_shape, device=self.device) if grad is None else \
+            _dev(grad, "grad", self.local_shape)
+        J = ctypes.c_double()
+        check(lib().sf_gradient_ckpt(self._h, _ptr(wavelet) if self.nsrc else None, _ptr(d_obs), _ptr(grad),
+                                     ctypes.byref(J), ctypes.c_void_p(ws.data_ptr()), nbytes,
+                                     int(save_every), int(segment), _stream(stream)))
+        return grad, J.value
+
     def allreduce_gradient(self, comm: int, grad: torch.Tensor, J: Optional[float] = None, stream=None):
         return allreduce_gradient(comm, grad, J, handle=self, stream=stream)
 

@@ -1297,6 +1297,107 @@ extern "C" sf_status sf_gradient(sf_handle *h, const float *wavelet, const float
     return SF_OK;
 }
 
+// ------------------------------------------------------------------ checkpointed gradient
+// Time windows of the handle's loops: sf_forward / sf_adjoint run h->nt samples from the
+// state they are given, so a segment [b, b + L] is the same call with nt = L + 1 and the
+// sparse-series pointers offset by b rows (wavelet rows b.., residual rows b..).
+namespace {
+struct NtWindow {
+    sf_handle *h;
+    int saved;
+    NtWindow(sf_handle *h_, int nt) : h(h_), saved(h_->nt) { h->nt = nt; }
+    ~NtWindow() { h->nt = saved; }
+};
+}  // namespace
+
+extern "C" size_t sf_gradient_ckpt_workspace_bytes(const sf_handle *h, int save_every, int segment)
+{
+    if (!h || save_every < 1 || segment < save_every || segment % save_every) return 0;
+    const size_t N = (size_t)h->N;
+    const size_t nseg = (size_t)((h->nt - 1 + segment - 1) / segment);
+    const size_t nss = (size_t)(segment / save_every + 1);
+    const size_t nr = (size_t)std::max(h->rec.np, 1), ns = (size_t)std::max(h->src.np, 1);
+    return align256(sizeof(float) * 2 * N * nseg) + align256(sizeof(float) * N * nss) +
+           2 * align256(sizeof(float) * 2 * N) + align256(sizeof(float) * (size_t)h->nt * nr) +
+           align256(sizeof(float) * (size_t)h->nt * ns) + align256(sizeof(float) * (size_t)(segment + 1) * nr) +
+           align256(sizeof(float) * (size_t)(segment + 1) * ns);
+}
+
+extern "C" sf_status sf_gradient_ckpt(sf_handle *h, const float *wavelet, const float *d_obs, float *grad,
+                                      double *J, void *ws, size_t ws_bytes, int save_every, int segment,
+                                      void *stream)
+{
+    if (!h || !grad || !d_obs || !ws) return sf_set_error(SF_ERR_INVALID_ARG, "NULL argument");
+    if (save_every < 1 || segment < save_every || segment % save_every)
+        return sf_set_error(SF_ERR_INVALID_ARG, "segment %d is not a positive multiple of save_every %d",
+                            segment, save_every);
+    const size_t need = sf_gradient_ckpt_workspace_bytes(h, save_every, segment);
+    if (ws_bytes < need) return sf_set_error(SF_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+    cudaStream_t st = S(stream);
+    const size_t N = (size_t)h->N;
+    const int nt = h->nt, nrec = h->rec.np, nsrc = h->src.np;
+    const int nseg = (nt - 1 + segment - 1) / segment;
+    const size_t nr = (size_t)std::max(nrec, 1), ns = (size_t)std::max(nsrc, 1);
+    char *p = static_cast<char *>(ws);
+    float *ckpt = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * 2 * N * nseg);
+    float *snaps = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * N * (size_t)(segment / save_every + 1));
+    float *u = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * 2 * N);
+    float *v = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * 2 * N);
+    float *rec = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * (size_t)nt * nr);
+    float *srca = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * (size_t)nt * ns);
+    float *rec_seg = reinterpret_cast<float *>(p);
+    p += align256(sizeof(float) * (size_t)(segment + 1) * nr);
+    float *srca_seg = reinterpret_cast<float *>(p);
+    SF_CUDA_TRY(cudaMemsetAsync(u, 0, sizeof(float) * 2 * N, st));
+    SF_CUDA_TRY(cudaMemsetAsync(v, 0, sizeof(float) * 2 * N, st));
+    SF_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(float) * N, st));
+    sf_status s;
+    // pass 1: forward over the segments, checkpointing each segment's initial state pair
+    for (int k = 0; k < nseg; ++k) {
+        const int b = k * segment, len = std::min(segment, nt - 1 - b);
+        SF_CUDA_TRY(cudaMemcpyAsync(ckpt + 2 * N * k, u, sizeof(float) * 2 * N, cudaMemcpyDeviceToDevice, st));
+        {
+            NtWindow win(h, len + 1);
+            if ((s = sf_forward(h, wavelet ? wavelet + (size_t)b * nsrc : nullptr, nrec ? rec_seg : nullptr, u,
+                                nullptr, 0, st)))
+                return s;
+        }
+        if (nrec) {  // rows 1..len are levels b+1..b+len (row 0 = level b, already recorded)
+            const int r0 = k == 0 ? 0 : 1;
+            SF_CUDA_TRY(cudaMemcpyAsync(rec + (size_t)(b + r0) * nrec, rec_seg + (size_t)r0 * nrec,
+                                        sizeof(float) * (size_t)(len + 1 - r0) * nrec, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    if (h->nranks > 1 && nrec > 0) {  // every rank needs the full record (C18)
+        if ((s = sf_comm_allreduce_f32(h->comm, rec, (size_t)nt * nrec, st))) return s;
+    }
+    if ((s = sf_residual(h, rec, d_obs, rec, J, st))) return s;
+    // pass 2: backward over the segments: recompute the segment's forward from its
+    // checkpoint with snapshots every save_every, then its adjoint steps with correlation
+    for (int k = nseg - 1; k >= 0; --k) {
+        const int b = k * segment, len = std::min(segment, nt - 1 - b);
+        SF_CUDA_TRY(cudaMemcpyAsync(u, ckpt + 2 * N * k, sizeof(float) * 2 * N, cudaMemcpyDeviceToDevice, st));
+        NtWindow win(h, len + 1);
+        if ((s = sf_forward(h, wavelet ? wavelet + (size_t)b * nsrc : nullptr, nrec ? rec_seg : nullptr, u,
+                            snaps, save_every, st)))
+            return s;
+        if ((s = sf_adjoint(h, rec + (size_t)b * nrec, nsrc ? srca_seg : nullptr, v, snaps, save_every, grad, st)))
+            return s;
+        if (nsrc) {  // rows 0..len-1 are levels b..b+len-1 (row len = level b+len, from the later segment)
+            const int rows = len + (k == nseg - 1 ? 1 : 0);
+            SF_CUDA_TRY(cudaMemcpyAsync(srca + (size_t)b * nsrc, srca_seg, sizeof(float) * (size_t)rows * nsrc,
+                                        cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    return SF_OK;
+}
+
 // ------------------------------------------------------------------ end-to-end host form
 namespace {
 struct HostCache {

@@ -515,3 +515,27 @@ def test_separable_damping_errors():
     assert e.value.status == "SF_ERR_INVALID_ARG"
     with pytest.raises(ValueError):          # wrong number / length of profiles
         S.Propagator(dev(p.m), None, sigma=p.sigma[:2], **kw)
+
+
+# ------------------------------------------------------------ checkpointed gradient (f3)
+@pytest.mark.parametrize("ndim,k,segment", [(3, 3, 6), (3, 1, 7), (3, 4, 400), (2, 2, 10)])
+def test_gradient_checkpointed_bitwise(ndim, k, segment):
+    """sf_gradient_ckpt (checkpoint-recompute) == sf_gradient bit for bit (deterministic
+    kernels; the recomputed forward starts from the exact checkpointed state pair), for
+    segments that divide nt-1, leave a ragged last segment, or exceed the record."""
+    shape = (30, 34, 64) if ndim == 3 else (80, 96)
+    p = synth.random_problem(ndim, shape, 8, 61, seed=70 + k, nbl=5, nsrc=2, nrec=20)
+    p.m_true = (p.m * 0.9).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    prop = make_prop(p)
+    g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=k)
+    gc, Jc = prop.gradient_ckpt(dev(p.wavelet), dev(d_obs), save_every=k, segment=segment)
+    torch.cuda.synchronize()
+    assert np.array_equal(g.cpu().numpy(), gc.cpu().numpy()) and J == Jc
+    full = prop.gradient_workspace_bytes(k)
+    ck = prop.gradient_ckpt_workspace_bytes(k, segment)
+    if k == 1:   # every step saved: 9 checkpoints + 8 snapshots instead of 61 snapshots
+        assert ck < 0.6 * full
+    with pytest.raises(ValueError):
+        prop.gradient_ckpt(dev(p.wavelet), dev(d_obs), save_every=3, segment=4)
+    prop.close()
