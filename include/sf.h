@@ -212,18 +212,29 @@ SF_API sf_status sf_nccl_unique_id(char id_out[128]);
 SF_API sf_status sf_nccl_comm_init(const char id[128], int nranks, int rank, void **comm_out);
 SF_API sf_status sf_nccl_comm_destroy(void *comm);
 
+/* In-process transport (testing the slab path on ONE device): ranks are threads of one
+ * process, each with its own handle and stream; a group created here is passed as the
+ * `comm` of sf_create_slab / sf_allreduce_gradient instead of an NCCL communicator.  The
+ * exchange moves the same planes as the NCCL path with cudaMemcpyAsync, ordered by CUDA
+ * events and a host barrier per step (no kernel ever waits on another rank's kernel).
+ * Every rank of the group must call the same sequence of library calls. */
+SF_API sf_status sf_local_group_create(int nranks, void **group_out);
+SF_API sf_status sf_local_group_destroy(void *group);
+
 /* Slab handle: `global` holds the GLOBAL shape and sparse geometry; global->m/damp
  * point to the LOCAL slab arrays [n0_loc + 2r][n1][n2] (halo planes unused).  All
  * wavefield arrays passed to sf_forward/sf_adjoint are then local [n0_loc + 2r][n1][n2]
  * (u: [2][...]); records/srca are full [nt][npoint] arrays in which each rank writes the
  * rows of the points it owns (others are zeroed) -- sum them over ranks.  The halo of
- * r planes is exchanged every step with ncclSend/ncclRecv over NVLink. */
-SF_API sf_status sf_create_slab(const sf_desc *global, void *nccl_comm, int rank, int nranks,
+ * r planes is exchanged every step with ncclSend/ncclRecv over NVLink (`comm` from
+ * sf_nccl_comm_init), or with device copies when `comm` is a local group (above). */
+SF_API sf_status sf_create_slab(const sf_desc *global, void *comm, int rank, int nranks,
                          sf_handle **out);
 /* In-place fp32 sum of grad [Nloc] and fp64 sum of *J (host) over the communicator
- * (multi-shot FWI, one shot per GPU).  Synchronises `stream`. */
-SF_API sf_status sf_allreduce_gradient(sf_handle *h, void *nccl_comm, float *grad, size_t count,
-                                double *J, void *stream);
+ * (multi-shot FWI, one shot per GPU).  `rank` is the caller's rank in `comm` (used by the
+ * in-process transport; NCCL knows it).  Synchronises `stream`. */
+SF_API sf_status sf_allreduce_gradient(sf_handle *h, void *comm, float *grad, size_t count,
+                                       double *J, int rank, void *stream);
 
 SF_API const char *sf_last_error(void);
 SF_API int sf_version(void);

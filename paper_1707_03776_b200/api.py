@@ -18,7 +18,8 @@ import torch
 from ._lib import SfDesc, SfError, check, lib
 
 __all__ = ["Propagator", "fd_weights", "forward_host", "slab_plan", "slab_halo_plan", "sparse_owner", "SfError",
-           "nccl_unique_id", "nccl_comm_init", "nccl_comm_destroy", "allreduce_gradient"]
+           "nccl_unique_id", "nccl_comm_init", "nccl_comm_destroy", "allreduce_gradient",
+           "local_group_create", "local_group_destroy"]
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -286,19 +287,34 @@ class Propagator:
                                      int(save_every), int(segment), _stream(stream)))
         return grad, J.value
 
-    def allreduce_gradient(self, comm: int, grad: torch.Tensor, J: Optional[float] = None, stream=None):
-        return allreduce_gradient(comm, grad, J, handle=self, stream=stream)
+    def allreduce_gradient(self, comm: int, grad: torch.Tensor, J: Optional[float] = None, rank: int = 0,
+                           stream=None):
+        return allreduce_gradient(comm, grad, J, handle=self, rank=rank, stream=stream)
 
 
 def allreduce_gradient(comm: int, grad: torch.Tensor, J: Optional[float] = None, handle=None,
-                       stream=None):
-    """sf_allreduce_gradient: in-place sum of grad (and J) over the NCCL communicator."""
+                       rank: int = 0, stream=None):
+    """sf_allreduce_gradient: in-place sum of grad (and J) over the communicator (NCCL or
+    a local group; `rank` = the caller's rank, needed by the local group only)."""
     _dev(grad, "grad")
     Jc = ctypes.c_double(0.0 if J is None else J)
     check(lib().sf_allreduce_gradient(handle._h if handle is not None else None, ctypes.c_void_p(comm),
                                       _ptr(grad), grad.numel(),
-                                      ctypes.byref(Jc) if J is not None else None, _stream(stream)))
+                                      ctypes.byref(Jc) if J is not None else None, int(rank),
+                                      _stream(stream)))
     return grad, (Jc.value if J is not None else None)
+
+
+def local_group_create(nranks: int) -> int:
+    """sf_local_group_create: an in-process transport for `nranks` rank threads on one device
+    (testing the slab / multi-shot paths without NCCL); pass it as `comm`."""
+    g = ctypes.c_void_p()
+    check(lib().sf_local_group_create(int(nranks), ctypes.byref(g)))
+    return g.value
+
+
+def local_group_destroy(group: int):
+    check(lib().sf_local_group_destroy(ctypes.c_void_p(group)))
 
 
 def forward_host(m: np.ndarray, damp: Optional[np.ndarray], *, h: float, space_order: int, nt: int,

@@ -12,7 +12,10 @@
 // Global edges keep their zero halo (Dirichlet ghost, reading C6).
 #include <dlfcn.h>
 
+#include <condition_variable>
 #include <mutex>
+#include <set>
+#include <vector>
 
 #include <nccl.h>
 
@@ -111,8 +114,148 @@ extern "C" sf_status sf_nccl_comm_destroy(void *comm)
     return SF_OK;
 }
 
+// ------------------------------------------------------------ in-process transport
+namespace {
+struct LocalGroup {
+    int n = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int count = 0;
+    long long gen = 0;
+    std::vector<cudaEvent_t> ev, done;
+    std::vector<void *> ptr;
+    void barrier()
+    {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long g = gen;
+        if (++count == n) {
+            count = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+std::mutex g_groups_mu;
+std::set<void *> g_groups;
+
+LocalGroup *as_local(void *comm)
+{
+    std::lock_guard<std::mutex> lk(g_groups_mu);
+    return g_groups.count(comm) ? static_cast<LocalGroup *>(comm) : nullptr;
+}
+
+template <class T>
+__global__ void k_accumulate(T *__restrict__ dst, const T *__restrict__ src, size_t n)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] += src[i];
+}
+
+// sum over the group into every rank's buf: rank 0 accumulates ranks 1.. in rank order,
+// the others copy the sum back; events order the streams, barriers order the host calls
+template <class T>
+sf_status local_allreduce(LocalGroup *G, int rank, T *buf, size_t count, cudaStream_t st)
+{
+    G->ptr[rank] = buf;
+    SF_CUDA_TRY(cudaEventRecord(G->ev[rank], st));
+    G->barrier();
+    if (rank == 0) {
+        for (int q = 1; q < G->n; ++q) {
+            SF_CUDA_TRY(cudaStreamWaitEvent(st, G->ev[q], 0));
+            k_accumulate<T><<<592, 256, 0, st>>>(buf, static_cast<const T *>(G->ptr[q]), count);
+            SF_CUDA_TRY(cudaGetLastError());
+        }
+        SF_CUDA_TRY(cudaEventRecord(G->done[0], st));
+    }
+    G->barrier();
+    if (rank != 0) {
+        SF_CUDA_TRY(cudaStreamWaitEvent(st, G->done[0], 0));
+        SF_CUDA_TRY(cudaMemcpyAsync(buf, G->ptr[0], count * sizeof(T), cudaMemcpyDeviceToDevice, st));
+        SF_CUDA_TRY(cudaEventRecord(G->done[rank], st));
+    }
+    G->barrier();
+    if (rank == 0)  // rank 0's buffer was read by everyone: order its later writes
+        for (int q = 1; q < G->n; ++q) SF_CUDA_TRY(cudaStreamWaitEvent(st, G->done[q], 0));
+    G->barrier();
+    return SF_OK;
+}
+}  // namespace
+
+extern "C" sf_status sf_local_group_create(int nranks, void **group_out)
+{
+    if (nranks < 1 || !group_out) return sf_set_error(SF_ERR_INVALID_ARG, "bad local group (%d)", nranks);
+    LocalGroup *G = new LocalGroup();
+    G->n = nranks;
+    G->ev.resize(nranks);
+    G->done.resize(nranks);
+    G->ptr.assign(nranks, nullptr);
+    for (int q = 0; q < nranks; ++q) {
+        SF_CUDA_TRY(cudaEventCreateWithFlags(&G->ev[q], cudaEventDisableTiming));
+        SF_CUDA_TRY(cudaEventCreateWithFlags(&G->done[q], cudaEventDisableTiming));
+    }
+    std::lock_guard<std::mutex> lk(g_groups_mu);
+    g_groups.insert(G);
+    *group_out = G;
+    return SF_OK;
+}
+
+extern "C" sf_status sf_local_group_destroy(void *group)
+{
+    LocalGroup *G = as_local(group);
+    if (!G) return sf_set_error(SF_ERR_INVALID_ARG, "not a local group");
+    {
+        std::lock_guard<std::mutex> lk(g_groups_mu);
+        g_groups.erase(group);
+    }
+    cudaDeviceSynchronize();
+    for (int q = 0; q < G->n; ++q) {
+        cudaEventDestroy(G->ev[q]);
+        cudaEventDestroy(G->done[q]);
+    }
+    delete G;
+    return SF_OK;
+}
+
+bool sf_comm_is_local(void *comm) { return as_local(comm) != nullptr; }
+
+// the local form of the halo exchange below: the same planes, copied from the neighbours'
+// buffers after their step (event), the neighbours' next writes ordered after the copies
+static sf_status local_halo_exchange(sf_handle *h, LocalGroup *G, float *buf, cudaStream_t st)
+{
+    int64_t plan[7], qp[7];
+    sf_status s;
+    if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank, h->nranks, plan))) return s;
+    const int64_t plane = h->N / h->nb[0];
+    const size_t bytes = sizeof(float) * (size_t)plan[4] * (size_t)plane;
+    G->ptr[h->rank] = buf;
+    SF_CUDA_TRY(cudaEventRecord(G->ev[h->rank], st));
+    G->barrier();
+    if (plan[5]) {  // left halo <- left neighbour's planes it sends right
+        if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank - 1, h->nranks, qp))) return s;
+        SF_CUDA_TRY(cudaStreamWaitEvent(st, G->ev[h->rank - 1], 0));
+        SF_CUDA_TRY(cudaMemcpyAsync(buf + plan[1] * plane, static_cast<float *>(G->ptr[h->rank - 1]) + qp[2] * plane,
+                                    bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    if (plan[6]) {  // right halo <- right neighbour's planes it sends left
+        if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank + 1, h->nranks, qp))) return s;
+        SF_CUDA_TRY(cudaStreamWaitEvent(st, G->ev[h->rank + 1], 0));
+        SF_CUDA_TRY(cudaMemcpyAsync(buf + plan[3] * plane, static_cast<float *>(G->ptr[h->rank + 1]) + qp[0] * plane,
+                                    bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    SF_CUDA_TRY(cudaEventRecord(G->done[h->rank], st));
+    G->barrier();
+    if (plan[5]) SF_CUDA_TRY(cudaStreamWaitEvent(st, G->done[h->rank - 1], 0));
+    if (plan[6]) SF_CUDA_TRY(cudaStreamWaitEvent(st, G->done[h->rank + 1], 0));
+    h->n_all++;
+    h->n_kind[3]++;
+    return SF_OK;
+}
+
 sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st)
 {
+    if (LocalGroup *G = as_local(h->comm)) return local_halo_exchange(h, G, buf, st);
     sf_status s = need_nccl();
     if (s) return s;
     int64_t plan[7];
@@ -135,16 +278,18 @@ sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st)
     return SF_OK;
 }
 
-sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st)
+sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st, int rank)
 {
+    if (LocalGroup *G = as_local(comm)) return local_allreduce<float>(G, rank, buf, count, st);
     sf_status s = need_nccl();
     if (s) return s;
     SF_NCCL_TRY(api().AllReduce(buf, buf, count, ncclFloat, ncclSum, static_cast<ncclComm_t>(comm), st));
     return SF_OK;
 }
 
-sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st)
+sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st, int rank)
 {
+    if (LocalGroup *G = as_local(comm)) return local_allreduce<double>(G, rank, buf, count, st);
     sf_status s = need_nccl();
     if (s) return s;
     SF_NCCL_TRY(api().AllReduce(buf, buf, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm), st));
@@ -152,11 +297,11 @@ sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStrea
 }
 
 extern "C" sf_status sf_allreduce_gradient(sf_handle *h, void *comm, float *grad, size_t count,
-                                           double *J, void *stream)
+                                           double *J, int rank, void *stream)
 {
     if (!comm || !grad) return sf_set_error(SF_ERR_INVALID_ARG, "NULL argument");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    sf_status s = sf_comm_allreduce_f32(comm, grad, count, st);
+    sf_status s = sf_comm_allreduce_f32(comm, grad, count, st, rank);
     if (s) return s;
     if (J) {
         double *dJ = h ? h->dJ : nullptr;
@@ -166,7 +311,7 @@ extern "C" sf_status sf_allreduce_gradient(sf_handle *h, void *comm, float *grad
             own = true;
         }
         SF_CUDA_TRY(cudaMemcpyAsync(dJ, J, sizeof(double), cudaMemcpyHostToDevice, st));
-        if ((s = sf_comm_allreduce_f64(comm, dJ, 1, st))) return s;
+        if ((s = sf_comm_allreduce_f64(comm, dJ, 1, st, rank))) return s;
         SF_CUDA_TRY(cudaMemcpyAsync(J, dJ, sizeof(double), cudaMemcpyDeviceToHost, st));
         SF_CUDA_TRY(cudaStreamSynchronize(st));
         if (own) cudaFree(dJ);

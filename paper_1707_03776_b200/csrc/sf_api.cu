@@ -872,7 +872,7 @@ extern "C" sf_status sf_create_slab(const sf_desc *d, void *comm, int rank, int 
     *out = nullptr;
     sf_status s = validate_desc(d);
     if (s) return s;
-    if (nranks > 1 && !comm) return sf_set_error(SF_ERR_INVALID_ARG, "nccl comm is NULL");
+    if (nranks > 1 && !comm) return sf_set_error(SF_ERR_INVALID_ARG, "comm is NULL");
     int64_t x0, nl;
     if ((s = sf_slab_plan(d->shape[0], d->space_order, rank, nranks, &x0, &nl))) return s;
     sf_handle *h = new sf_handle();
@@ -1290,7 +1290,7 @@ extern "C" sf_status sf_gradient(sf_handle *h, const float *wavelet, const float
     sf_status s;
     if ((s = sf_forward(h, wavelet, rec, u, snaps, save_every, st))) return s;
     if (h->nranks > 1 && h->rec.np > 0) {  // every rank needs the full record (C18)
-        if ((s = sf_comm_allreduce_f32(h->comm, rec, (size_t)h->nt * h->rec.np, st))) return s;
+        if ((s = sf_comm_allreduce_f32(h->comm, rec, (size_t)h->nt * h->rec.np, st, h->rank))) return s;
     }
     if ((s = sf_residual(h, rec, d_obs, rec, J, st))) return s;
     if ((s = sf_adjoint(h, rec, h->src.np > 0 ? srca : nullptr, v, snaps, save_every, grad, st))) return s;
@@ -1375,7 +1375,7 @@ extern "C" sf_status sf_gradient_ckpt(sf_handle *h, const float *wavelet, const 
         }
     }
     if (h->nranks > 1 && nrec > 0) {  // every rank needs the full record (C18)
-        if ((s = sf_comm_allreduce_f32(h->comm, rec, (size_t)nt * nrec, st))) return s;
+        if ((s = sf_comm_allreduce_f32(h->comm, rec, (size_t)nt * nrec, st, h->rank))) return s;
     }
     if ((s = sf_residual(h, rec, d_obs, rec, J, st))) return s;
     // pass 2: backward over the segments: recompute the segment's forward from its

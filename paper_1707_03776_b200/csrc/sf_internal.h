@@ -116,5 +116,6 @@ sf_status sf_set_error(sf_status s, const char *fmt, ...);
 
 // comm.cu
 sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st);
-sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st);
-sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st);
+sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st, int rank);
+sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st, int rank);
+bool sf_comm_is_local(void *comm);

@@ -539,3 +539,138 @@ def test_gradient_checkpointed_bitwise(ndim, k, segment):
     with pytest.raises(ValueError):
         prop.gradient_ckpt(dev(p.wavelet), dev(d_obs), save_every=3, segment=4)
     prop.close()
+
+
+# ------------------------------------------------------------ slab path on one device
+def _run_ranks(nranks, fn):
+    """Run fn(rank) for every rank in its own thread (and CUDA stream); re-raise errors."""
+    import threading
+    out, err = [None] * nranks, []
+
+    def body(rank):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[rank] = fn(rank)
+                s.synchronize()
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+
+    ts = [threading.Thread(target=body, args=(q,)) for q in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not err, err
+    return out
+
+
+def _slab_inputs(p, rank, nranks):
+    S = sf()
+    r = p.space_order // 2
+    x0, nl = S.slab_plan(p.shape[0], p.space_order, rank, nranks)
+    g = np.arange(x0 - r, x0 + nl + r)
+    ok = (g >= 0) & (g < p.shape[0])
+    m = np.ones((nl + 2 * r,) + tuple(p.shape[1:]), np.float32)
+    m[ok] = p.m[g[ok]]
+    eta = None
+    if p.damp is not None:
+        eta = np.zeros_like(m)
+        eta[ok] = p.damp[g[ok]]
+    return x0, nl, m, eta
+
+
+@pytest.mark.parametrize("nranks,variant", [(2, 2), (3, 2), (3, 1)])
+def test_slab_decomposition_bitwise_local_transport(nranks, variant):
+    """The multi-GPU slab path (local [n0_loc + 2r] buffers, split boundary/interior
+    launches with the persistent-kernel SM reservation, per-step halo exchange, owner-only
+    injection and records, record all-reduce inside the gradient) run as rank threads on
+    ONE device through the in-process transport (same planes as the NCCL exchange): the
+    records, the owned planes of both final levels and of the gradient, and J are bitwise
+    those of the single-domain run (reading C18).  Sources and receivers straddle the slab
+    boundaries."""
+    S = sf()
+    p = synth.random_problem(3, (41, 30, 64), 8, 50, seed=91, nbl=5, nsrc=3, nrec=40)
+    h = p.h
+    p.src_coords[0, 0] = 13.5 * h          # on / across the rank boundaries (41 planes)
+    p.src_coords[1, 0] = 20.2 * h
+    p.rec_coords[:20, 0] = np.linspace(8 * h, 33 * h, 20)
+    p.m_true = (p.m * 0.92).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    prop = make_prop(p)
+    prop.set_tuning(variant, 0, 0)
+    rec1, u1, _ = prop.forward(dev(p.wavelet))
+    g1, J1 = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+    torch.cuda.synchronize()
+    rec1, u1, g1 = rec1.cpu().numpy(), u1.cpu().numpy(), g1.cpu().numpy()
+    prop.close()
+    group = S.local_group_create(nranks)
+    r = p.space_order // 2
+
+    def rank_fn(rank):
+        x0, nl, m, eta = _slab_inputs(p, rank, nranks)
+        pr = S.Propagator(dev(m), None if eta is None else dev(eta), shape=p.shape, h=p.h,
+                          space_order=p.space_order, nt=p.nt, dt=p.dt,
+                          src_coords=p.src_coords.astype(np.float64),
+                          rec_coords=p.rec_coords.astype(np.float64), comm=group, rank=rank, nranks=nranks)
+        pr.set_tuning(variant, 0, 0)
+        rec, u, _ = pr.forward(dev(p.wavelet))
+        g, J = pr.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+        torch.cuda.current_stream().synchronize()
+        res = (x0, nl, rec.cpu().numpy(), u.cpu().numpy()[:, r:r + nl], g.cpu().numpy()[r:r + nl], J)
+        pr.close()
+        return res
+
+    try:
+        outs = _run_ranks(nranks, rank_fn)
+    finally:
+        S.local_group_destroy(group)
+    rec_sum = sum(o[2] for o in outs)
+    assert np.array_equal(rec_sum, rec1)
+    for x0, nl, _, u, g, J in outs:
+        assert np.array_equal(u, u1[:, x0:x0 + nl]), (x0, nl)
+        assert np.array_equal(g, g1[x0:x0 + nl]), (x0, nl)
+        assert J == J1
+
+
+def test_multishot_allreduce_local_transport():
+    """Multi-shot FWI (one shot per rank) + sf_allreduce_gradient over the in-process
+    transport: the summed gradient and J equal the sequential sum of the shots'."""
+    S = sf()
+    shots = []
+    for s in range(2):
+        p = synth.random_problem(3, (26, 30, 64), 8, 40, seed=95 + s, nbl=5, nsrc=1, nrec=30)
+        p.m = shots[0].m if shots else p.m
+        p.damp = shots[0].damp if shots else p.damp
+        p.m_true = (p.m * 0.9).astype(np.float32)
+        shots.append(p)
+    gs, Js = [], []
+    for p in shots:
+        d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+        pr = make_prop(p)
+        g, J = pr.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
+        torch.cuda.synchronize()
+        gs.append(g.cpu().numpy())
+        Js.append(J)
+        p.d_obs = d_obs
+        pr.close()
+    group = S.local_group_create(2)
+
+    def rank_fn(rank):
+        p = shots[rank]
+        pr = make_prop(p)
+        g, J = pr.gradient(dev(p.wavelet), dev(p.d_obs), save_every=2)
+        g, J = pr.allreduce_gradient(group, g, J, rank=rank)
+        torch.cuda.current_stream().synchronize()
+        out = (g.cpu().numpy(), J)
+        pr.close()
+        return out
+
+    try:
+        outs = _run_ranks(2, rank_fn)
+    finally:
+        S.local_group_destroy(group)
+    gsum = (gs[0] + gs[1]).astype(np.float32)
+    for g, J in outs:
+        assert np.array_equal(g, gsum)
+        assert J == Js[0] + Js[1]
