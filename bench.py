@@ -125,14 +125,17 @@ def build_problem(nt_override=None, rank=0, nranks=1, cfg=1):
     gshape = (n0 * nranks,) + p.shape[1:]
     import synth as S
     vmax = 2500.0
-    sig = S.damping_profile(gshape, p.nbl, p.h, vmax)   # only a 1D x-profile part differs
-    p.sigma = S.damping_profiles_1d(gshape, p.nbl, p.h, vmax)   # separable form (global grid)
+    # damping of the global grid from its per-axis profiles (reading C7), evaluated on this
+    # rank's planes only (no global 3D array per rank)
+    p.sigma = S.damping_profiles_1d(gshape, p.nbl, p.h, vmax)
     x0 = rank * n0
     lo, hi = x0 - r, x0 + n0 + r
     idx = np.clip(np.arange(lo, hi), 0, gshape[0] - 1)
     m_col = p.m[0]  # every x-plane of the padded configs[1] model is identical
     m_loc = np.ascontiguousarray(np.broadcast_to(m_col, (hi - lo,) + p.shape[1:]), dtype=np.float32)
-    eta_loc = (m_loc.astype(np.float64) * sig[idx]).astype(np.float32)
+    sx, sy, sz = (a.astype(np.float64) for a in p.sigma)
+    sig_loc = sx[idx][:, None, None] + sy[None, :, None] + sz[None, None, :]
+    eta_loc = (m_loc.astype(np.float64) * sig_loc).astype(np.float32)
     src = p.src_coords.copy()
     src[:, 0] = gshape[0] * p.h / 2.0
     rec = p.rec_coords.copy()
