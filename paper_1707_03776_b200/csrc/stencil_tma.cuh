@@ -31,6 +31,9 @@
 #include <type_traits>
 #include "stencil_common.cuh"
 
+#ifndef SF_DC_MIN
+#define SF_DC_MIN 3
+#endif
 #ifndef SF_MBAR_SUSPEND_NS
 #define SF_MBAR_SUSPEND_NS 0x100000
 #endif
@@ -136,11 +139,14 @@ struct Cfg {
     static constexpr int PL = TZ * BY * 4;              // one halo-free plane
     static constexpr int NPL = 2 + (DAMP ? 1 : 0) + (MODE == SF_MODE_GRAD ? 2 : 0);
     static constexpr int CST = NPL * PL;                // coefficient ring stage bytes
-    static constexpr int BUDGET = 225 * 1024;
-    // ring depths: the u ring must hold planes q..p (R + 1) plus the producer's lead;
-    // the coefficient ring gets what is left (up to 4; 1 only for r = 8 GRAD with damping)
+    static constexpr int BUDGET = 226 * 1024;
+    // ring depths: the u ring must hold planes q..p (R + 1) plus the producer's lead, the
+    // coefficient ring DC output planes.  Leads are balanced: DU up to R + 5 while the
+    // coefficient ring keeps SF_DC_MIN stages, then the rest to the coefficients (up to 4;
+    // below SF_DC_MIN only when even DU = R + 2 leaves no more, e.g. r = 8 GRAD + damping)
+    static constexpr int DC_MIN = SF_DC_MIN;
     static constexpr int DU_WANT = R + 5;
-    static constexpr int DU_FIT = (BUDGET - 2 * CST) / UST;
+    static constexpr int DU_FIT = (BUDGET - DC_MIN * CST) / UST;
     static constexpr int DU = DU_FIT >= DU_WANT ? DU_WANT : (DU_FIT >= R + 2 ? DU_FIT : R + 2);
     static constexpr int DC_FIT = (BUDGET - DU * UST) / CST;
     static constexpr int DC = DC_FIT >= 4 ? 4 : DC_FIT;
