@@ -183,6 +183,12 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
 #define SF_OPT_COMM_SMS 4      /* split schedule: SMs the persistent interior launch leaves free
                                   for the concurrent halo exchange (NCCL kernels) and the side-
                                   stream records (default 8 in slab mode, 0 on one GPU; 0..64)   */
+#define SF_OPT_GRAPH 5         /* 1: replay whole sf_forward / sf_adjoint calls as CUDA graphs:
+                                  the second call with the same arguments (pointers, save_every,
+                                  stream, nt) is captured once and then replayed on an internal
+                                  stream ordered after / before `stream` by events -- for small,
+                                  launch-bound grids.  Off while profiling and in slab mode;
+                                  tuning or option changes drop the cached graphs. (default 0)  */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */

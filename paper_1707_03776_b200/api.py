@@ -167,7 +167,8 @@ class Propagator:
         check(lib().sf_set_tuning(self._h, variant, vy, ctas))
 
     def set_option(self, option: int, value: int):
-        """sf_set_option: 1 L2 prefetch distance, 2 split boundary launches, 3 fuse-max points."""
+        """sf_set_option: 1 L2 prefetch distance, 2 split boundary launches, 3 fuse-max points,
+        4 SMs left free by the split interior launch, 5 CUDA-graph replay of whole calls."""
         check(lib().sf_set_option(self._h, int(option), int(value)))
 
     def tuning(self):

@@ -239,6 +239,8 @@ static void sf_dfree(void *p)
 #define cudaMalloc(p, n) sf_dalloc((void **)(p), (n))
 #define cudaFree(p) sf_dfree((void *)(p))
 
+static void drop_graphs(sf_handle *h);
+
 template <class T>
 static sf_status upload(T **dst, const std::vector<T> &v)
 {
@@ -683,6 +685,10 @@ extern "C" void sf_destroy(sf_handle *h)
     if (h->ev_pre) cudaEventDestroy(h->ev_pre);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
     if (h->ev_xch) cudaEventDestroy(h->ev_xch);
+    drop_graphs(h);
+    if (h->gstream) cudaStreamDestroy(h->gstream);
+    if (h->ev_gin) cudaEventDestroy(h->ev_gin);
+    if (h->ev_gout) cudaEventDestroy(h->ev_gout);
     delete h;
 }
 
@@ -917,6 +923,7 @@ extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas)
     h->variant = variant;
     h->vy = vy;
     h->ctas = ctas;
+    drop_graphs(h);
     return SF_OK;
 }
 
@@ -927,18 +934,31 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
     case SF_OPT_L2_PREFETCH:
         if (value < 0 || value > 64) return sf_set_error(SF_ERR_INVALID_ARG, "prefetch distance %d", value);
         h->l2_prefetch = value;
+        drop_graphs(h);
         return SF_OK;
     case SF_OPT_SPLIT:
         if (h->nranks > 1 && !value) return sf_set_error(SF_ERR_INVALID_ARG, "slab mode always splits");
         h->split = value != 0;
+        drop_graphs(h);
         return SF_OK;
     case SF_OPT_FUSE_MAX:
         if (value < 0) return sf_set_error(SF_ERR_INVALID_ARG, "fuse max %d", value);
         h->fuse_max = value;
+        drop_graphs(h);
         return SF_OK;
     case SF_OPT_COMM_SMS:
         if (value < 0 || value > 64) return sf_set_error(SF_ERR_INVALID_ARG, "comm SMs %d", value);
         h->comm_sms = value;
+        drop_graphs(h);
+        return SF_OK;
+    case SF_OPT_GRAPH:
+        if (value && !h->gstream) {
+            SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+            SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_gin, cudaEventDisableTiming));
+            SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_gout, cudaEventDisableTiming));
+        }
+        h->use_graph = value != 0;
+        drop_graphs(h);
         return SF_OK;
     default:
         return sf_set_error(SF_ERR_INVALID_ARG, "unknown option %d", option);
@@ -1150,8 +1170,8 @@ static sf_status join_side(sf_handle *h, cudaStream_t st)
     return SF_OK;
 }
 
-extern "C" sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, float *u,
-                                float *snaps, int save_every, void *stream)
+static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, float *u, float *snaps,
+                              int save_every, void *stream)
 {
     if (!h || !u) return sf_set_error(SF_ERR_INVALID_ARG, "handle or u is NULL");
     if (h->src.np > 0 && !wavelet) return sf_set_error(SF_ERR_INVALID_ARG, "wavelet is NULL");
@@ -1186,8 +1206,8 @@ extern "C" sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, 
     return SF_OK;
 }
 
-extern "C" sf_status sf_adjoint(sf_handle *h, const float *res, float *srca, float *v,
-                                const float *snaps, int save_every, float *grad, void *stream)
+static sf_status adjoint_body(sf_handle *h, const float *res, float *srca, float *v, const float *snaps,
+                              int save_every, float *grad, void *stream)
 {
     if (!h || !v) return sf_set_error(SF_ERR_INVALID_ARG, "handle or v is NULL");
     if (h->rec.np > 0 && !res) return sf_set_error(SF_ERR_INVALID_ARG, "res is NULL");
@@ -1226,6 +1246,91 @@ extern "C" sf_status sf_adjoint(sf_handle *h, const float *res, float *srca, flo
     if ((s = join_side(h, st))) return s;
     if (h->nt % 2 == 0) return swap_halves(h, A, B, st);
     return SF_OK;
+}
+
+// ------------------------------------------------------------------ CUDA graphs (SF_OPT_GRAPH)
+static void drop_graphs(sf_handle *h)
+{
+    for (SfGraphCache *G : {&h->gfwd, &h->gadj}) {
+        if (G->exec) cudaGraphExecDestroy(G->exec);
+        *G = SfGraphCache{};
+    }
+}
+
+// Run `body(stream)` eagerly, or -- graphs on, same arguments as the previous call -- capture
+// it once on the handle's graph stream and replay it there, ordered after and before the
+// caller's stream by events (the legacy default stream cannot be captured).
+template <class F>
+static sf_status with_graph(sf_handle *h, SfGraphCache &G, const void *const k[6], const long long ik[3],
+                            cudaStream_t st, F body)
+{
+    if (!h->use_graph || h->prof || h->nranks > 1) return body(st);
+    auto same = [&](const void *const *a, const long long *ai) {
+        for (int i = 0; i < 6; ++i)
+            if (a[i] != k[i]) return false;
+        for (int i = 0; i < 3; ++i)
+            if (ai[i] != ik[i]) return false;
+        return true;
+    };
+    if (G.exec && same(G.key, G.ikey)) {
+        SF_CUDA_TRY(cudaEventRecord(h->ev_gin, st));
+        SF_CUDA_TRY(cudaStreamWaitEvent(h->gstream, h->ev_gin, 0));
+        SF_CUDA_TRY(cudaGraphLaunch(G.exec, h->gstream));
+        SF_CUDA_TRY(cudaEventRecord(h->ev_gout, h->gstream));
+        SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_gout, 0));
+        return SF_OK;
+    }
+    if (!same(G.seen, G.iseen)) {  // first call with these arguments: eager (builds tables)
+        for (int i = 0; i < 6; ++i) G.seen[i] = k[i];
+        for (int i = 0; i < 3; ++i) G.iseen[i] = ik[i];
+        return body(st);
+    }
+    // second call: capture the whole call on the graph stream, instantiate, replay
+    SF_CUDA_TRY(cudaEventRecord(h->ev_gin, st));
+    SF_CUDA_TRY(cudaStreamWaitEvent(h->gstream, h->ev_gin, 0));
+    SF_CUDA_TRY(cudaStreamBeginCapture(h->gstream, cudaStreamCaptureModeThreadLocal));
+    sf_status s = body(h->gstream);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(h->gstream, &g);
+    if (s) {
+        if (g) cudaGraphDestroy(g);
+        return s;
+    }
+    if (e != cudaSuccess) return sf_set_error(SF_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t e2 = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e2 != cudaSuccess) return sf_set_error(SF_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e2));
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    G.exec = ex;
+    for (int i = 0; i < 6; ++i) G.key[i] = k[i];
+    for (int i = 0; i < 3; ++i) G.ikey[i] = ik[i];
+    SF_CUDA_TRY(cudaGraphLaunch(G.exec, h->gstream));
+    SF_CUDA_TRY(cudaEventRecord(h->ev_gout, h->gstream));
+    SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_gout, 0));
+    return SF_OK;
+}
+
+extern "C" sf_status sf_forward(sf_handle *h, const float *wavelet, float *rec, float *u,
+                                float *snaps, int save_every, void *stream)
+{
+    if (!h || !u) return sf_set_error(SF_ERR_INVALID_ARG, "handle or u is NULL");
+    const void *k[6] = {wavelet, rec, u, snaps, stream, nullptr};
+    const long long ik[3] = {save_every, h->nt, 0};
+    return with_graph(h, h->gfwd, k, ik, S(stream), [&](cudaStream_t s2) {
+        return forward_body(h, wavelet, rec, u, snaps, save_every, s2);
+    });
+}
+
+extern "C" sf_status sf_adjoint(sf_handle *h, const float *res, float *srca, float *v,
+                                const float *snaps, int save_every, float *grad, void *stream)
+{
+    if (!h || !v) return sf_set_error(SF_ERR_INVALID_ARG, "handle or v is NULL");
+    const void *k[6] = {res, srca, v, snaps, grad, stream};
+    const long long ik[3] = {save_every, h->nt, 1};
+    return with_graph(h, h->gadj, k, ik, S(stream), [&](cudaStream_t s2) {
+        return adjoint_body(h, res, srca, v, snaps, save_every, grad, s2);
+    });
 }
 
 extern "C" sf_status sf_residual(sf_handle *h, const float *d_syn, const float *d_obs, float *res,

@@ -60,6 +60,18 @@ struct SfSparse {
     SfItpTiles itiles;
 };
 
+// One cached CUDA graph of a whole sf_forward / sf_adjoint call (SF_OPT_GRAPH): the
+// arguments it was captured with, and the arguments of the last eager call (a call is
+// captured the second time the same arguments come, after the first one has built every
+// lazily created table).
+struct SfGraphCache {
+    const void *key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    long long ikey[3] = {0, 0, 0};
+    const void *seen[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    long long iseen[3] = {-1, -1, -1};
+    cudaGraphExec_t exec = nullptr;
+};
+
 struct sf_handle {
     int ndim = 3;
     int64_t gshape[3] = {1, 1, 1};  // global computational grid
@@ -102,6 +114,11 @@ struct sf_handle {
     cudaEvent_t ev_pre = nullptr, ev_bnd = nullptr, ev_xch = nullptr;
     int fuse_max = 256;
     int comm_sms = -1;              // SMs left free by the split interior launch (-1: auto)
+    // CUDA graphs of whole time loops (SF_OPT_GRAPH), run on gstream between two events
+    bool use_graph = false;
+    SfGraphCache gfwd, gadj;
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t ev_gin = nullptr, ev_gout = nullptr;
 };
 
 // error reporting (thread-local message)

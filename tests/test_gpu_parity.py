@@ -674,3 +674,41 @@ def test_multishot_allreduce_local_transport():
     for g, J in outs:
         assert np.array_equal(g, gsum)
         assert J == Js[0] + Js[1]
+
+
+# ------------------------------------------------------------ CUDA graph replay
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_graph_replay_bitwise(cfg):
+    """SF_OPT_GRAPH: the first call runs eagerly, the second identical call is captured as
+    one CUDA graph (on the handle's stream, event-ordered after the caller's stream) and
+    replayed afterwards: records, states and gradients bitwise those of eager calls; a
+    tuning change drops the graph; a restart state (same buffers, new contents) is honoured."""
+    p = synth.make_config(cfg, scale=1.0 if cfg == 0 else 0.15, nt=60)
+    p.m_true = (p.m * 0.9).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    ref = make_prop(p)
+    r0, u0, _ = ref.forward(dev(p.wavelet))
+    g0, J0 = ref.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
+    torch.cuda.synchronize()
+    r0, u0, g0 = r0.cpu().numpy(), u0.cpu().numpy(), g0.cpu().numpy()
+    ref.close()
+    prop = make_prop(p)
+    prop.set_option(5, 1)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        wav, dob = dev(p.wavelet), dev(d_obs)
+        u = prop.zeros_state()
+        rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
+        ws = torch.empty(prop.gradient_workspace_bytes(2), dtype=torch.uint8, device="cuda")
+        grad = torch.empty(prop.local_shape, device="cuda")
+        for it in range(4):
+            if it == 3:
+                prop.set_tuning(0, 0, 0)   # drops the graphs: eager again
+            u.zero_()
+            prop.forward(wav, u=u, rec=rec)
+            s.synchronize()
+            assert np.array_equal(rec.cpu().numpy(), r0) and np.array_equal(u.cpu().numpy(), u0), it
+            g, J = prop.gradient(wav, dob, save_every=2, grad=grad, ws=ws)
+            s.synchronize()
+            assert np.array_equal(g.cpu().numpy(), g0) and J == J0, it
+    prop.close()
