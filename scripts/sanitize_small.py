@@ -32,7 +32,7 @@ def run(p, variant, fuse, split):
     return float(J)
 
 
-for so in (4, 8):
+for so in (4, 8, 16):
     p = synth.random_problem(3, (14, 18, 132), so, 8, seed=so, nbl=3, nsrc=2, nrec=20)
     for variant in (1, 2):
         for fuse in (0, 256):
@@ -41,3 +41,14 @@ for so in (4, 8):
 p = synth.random_problem(2, (20, 24), 4, 8, seed=1, nbl=3, nsrc=1, nrec=5)
 run(p, 1, 0, 0)
 print("sanitize run ok")
+
+
+# separable damping (in-kernel beta) and the checkpointed gradient, TMA variant
+p = synth.random_problem(3, (14, 18, 132), 8, 9, seed=5, nbl=3, nsrc=2, nrec=20)
+prop = sf.Propagator(dev(p.m), None, shape=p.shape, h=p.h, space_order=8, nt=p.nt, dt=p.dt,
+                     src_coords=p.src_coords, rec_coords=p.rec_coords, sigma=p.sigma)
+rec, u, _ = prop.forward(dev(p.wavelet))
+g, J = prop.gradient_ckpt(dev(p.wavelet), (rec * 0.9).contiguous(), save_every=2, segment=4)
+torch.cuda.synchronize()
+prop.close()
+print("sanitize run done")
