@@ -50,8 +50,11 @@ def _load():
         L.or_inject.argtypes = [i, P, d, i, P, P, P, d, P]
         L.or_forward.argtypes = [i, P, d, i, i, d, P, P, i, P, P, i, P, P, P, i, P]
         L.or_adjoint.argtypes = [i, P, d, i, i, d, P, P, i, P, P, i, P, P, P, i, P, P]
+        L.or_convection2d.argtypes = [P, d, d, d, d, i, P]
+        L.or_laplace2d.argtypes = [P, d, d, P, d, i, P, P, P]
         for f in (L.or_fd_weights, L.or_laplacian, L.or_point_stencil, L.or_interpolate,
-                  L.or_inject, L.or_forward, L.or_adjoint, L.or_num_threads):
+                  L.or_inject, L.or_forward, L.or_adjoint, L.or_num_threads, L.or_convection2d,
+                  L.or_laplace2d):
             f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -211,3 +214,28 @@ def gradient(prob, d_obs, m=None, save_every: int = 1):
     J = 0.5 * float(np.sum(res * res))
     ad = adjoint(prob, res=res, m=mm, save_every=save_every, snaps=fw["snaps"])
     return {"grad": ad["grad"], "J": J, "res": res, "d_syn": fw["rec"]}
+
+
+# ------------------------------------------------------------------ other paper workloads (f4)
+def convection2d(u0, *, c: float, dt: float, dx: float, dy: float, nt: int) -> np.ndarray:
+    """Linear 2D convection, Eq. 2, nt forward-Euler / upwind steps from u0
+    ([n0][n1]); edges keep their initial values (reading C21).  fp64."""
+    u = _f64(u0).copy()
+    n = _shape(u.shape)
+    _chk(_load().or_convection2d(_p(n), float(c), float(dt), float(dx), float(dy), int(nt), _p(u)),
+         "or_convection2d")
+    return u
+
+
+def laplace2d(p0, bc, *, dx: float, dy: float, tol: float = 1e-4, max_iter: int = 100000):
+    """Laplace equation by Jacobi sweeps, Eq. 4 with the boundary expressions of
+    P:411-414 and the l1 stopping rule of P:433-447 (reading C22).  Returns (p, iterations,
+    last l1).  fp64."""
+    p = _f64(p0).copy()
+    n = _shape(p.shape)
+    b = _f64(bc)
+    it = ctypes.c_int()
+    l1 = ctypes.c_double()
+    _chk(_load().or_laplace2d(_p(n), float(dx), float(dy), _p(b), float(tol), int(max_iter), _p(p),
+                              ctypes.byref(it), ctypes.byref(l1)), "or_laplace2d")
+    return p, it.value, l1.value

@@ -35,6 +35,20 @@
  *                    "g += v * u_tt", readings C13/C14):
  *                      g -= k * u^n * (v^{n+1} - 2 v^n + v^{n-1}) / dt^2  for n % k == 0, n >= 1.
  *
+ * The paper's two other example workloads (readings C21/C22 in DESIGN.md):
+ *   or_convection2d : linear 2D convection, forward Euler in time, backward (upwind) in
+ *                     space, Eq. 2:
+ *                       u^{n+1}_ij = u^n_ij - c dt/dx (u^n_ij - u^n_{i-1,j}) - c dt/dy (u^n_ij - u^n_{i,j-1})
+ *                     on the interior 1 <= i < n0-1, 1 <= j < n1-1; edge points keep their
+ *                     initial values (Dirichlet, C21).
+ *   or_laplace2d    : Laplace equation by Jacobi sweeps, Eq. 4:
+ *                       p_ij = (dy^2 (pn_{i+1,j} + pn_{i-1,j}) + dx^2 (pn_{i,j+1} + pn_{i,j-1}))
+ *                              / (2 (dx^2 + dy^2))
+ *                     on the interior, then the boundary expressions in the listing's order
+ *                     (P:411-414): p[x,0] = 0; p[x,n1-1] = bc[x]; p[0,y] = p[1,y];
+ *                     p[n0-1,y] = p[n0-2,y]; buffers swap every sweep; after each sweep
+ *                     l1 = sum(|p| - |pn|) / sum(|pn|); stop when l1 <= tol (C22).
+ *
  * Layout: row-major [n0][n1][n2] (2D: [n0][n1]), last axis fastest.  Sparse data are
  * time-major [nt][npoint] (reading C12).  Coordinates in metres from index 0.
  * Return codes: 0 ok, 1 invalid argument, 5 sparse point out of domain.
@@ -357,6 +371,68 @@ int or_adjoint(int ndim, const int64_t *n, double h, int so, int nt, double dt,
 done:
     free(vp1); free(v0); free(vm1); free(rv);
     return e;
+}
+
+/* ---------------------------------------------------------------------------------
+ * Linear convection (Eq. 2; reading C21).  u: [n0][n1] in/out (fp64).
+ * ------------------------------------------------------------------------------- */
+int or_convection2d(const int64_t *n, double c, double dt, double dx, double dy, int nt, double *u)
+{
+    if (!n || !u || n[0] < 2 || n[1] < 2 || nt < 0 || !(dx > 0.0) || !(dy > 0.0)) return 1;
+    const int64_t n0 = n[0], n1 = n[1];
+    double *un = (double *)malloc(sizeof(double) * (size_t)(n0 * n1));
+    if (!un) return 1;
+    const double ax = c * dt / dx, ay = c * dt / dy;
+    for (int t = 0; t < nt; ++t) {
+        memcpy(un, u, sizeof(double) * (size_t)(n0 * n1));
+        for (int64_t i = 1; i < n0 - 1; ++i)
+            for (int64_t j = 1; j < n1 - 1; ++j) {
+                const double uij = un[i * n1 + j];
+                u[i * n1 + j] = uij - ax * (uij - un[(i - 1) * n1 + j]) - ay * (uij - un[i * n1 + j - 1]);
+            }
+    }
+    free(un);
+    return 0;
+}
+
+/* ---------------------------------------------------------------------------------
+ * Laplace / Jacobi (Eq. 4; boundary listing P:411-414; loop P:433-447;
+ * reading C22).  p: [n0][n1] in = the initial buffer pn, out = the last computed p;
+ * bc: [n0] the prescribed boundary row.  Stops after the first sweep with l1 <= tol or
+ * after max_iter sweeps; *iters = sweeps done, *l1 = the last l1.
+ * ------------------------------------------------------------------------------- */
+int or_laplace2d(const int64_t *n, double dx, double dy, const double *bc, double tol, int max_iter,
+                 double *p, int *iters, double *l1)
+{
+    if (!n || !p || !bc || n[0] < 3 || n[1] < 3 || max_iter < 0 || !(dx > 0.0) || !(dy > 0.0)) return 1;
+    const int64_t n0 = n[0], n1 = n[1], N = n0 * n1;
+    double *pn = (double *)malloc(sizeof(double) * (size_t)N);
+    if (!pn) return 1;
+    const double dx2 = dx * dx, dy2 = dy * dy;
+    double l1v = 1.0;
+    int it = 0;
+    while (it < max_iter && l1v > tol) {
+        memcpy(pn, p, sizeof(double) * (size_t)N);
+        for (int64_t i = 1; i < n0 - 1; ++i)
+            for (int64_t j = 1; j < n1 - 1; ++j)
+                p[i * n1 + j] = (dy2 * (pn[(i + 1) * n1 + j] + pn[(i - 1) * n1 + j]) +
+                                 dx2 * (pn[i * n1 + j + 1] + pn[i * n1 + j - 1])) / (2.0 * (dx2 + dy2));
+        for (int64_t i = 0; i < n0; ++i) p[i * n1 + 0] = 0.0;
+        for (int64_t i = 0; i < n0; ++i) p[i * n1 + n1 - 1] = bc[i];
+        for (int64_t j = 0; j < n1; ++j) p[0 * n1 + j] = p[1 * n1 + j];
+        for (int64_t j = 0; j < n1; ++j) p[(n0 - 1) * n1 + j] = p[(n0 - 2) * n1 + j];
+        double num = 0.0, den = 0.0;
+        for (int64_t k = 0; k < N; ++k) {
+            num += fabs(p[k]) - fabs(pn[k]);
+            den += fabs(pn[k]);
+        }
+        l1v = num / den;
+        ++it;
+    }
+    free(pn);
+    if (iters) *iters = it;
+    if (l1) *l1 = l1v;
+    return 0;
 }
 
 int or_num_threads(void)

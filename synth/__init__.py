@@ -28,7 +28,8 @@ from typing import Optional
 import numpy as np
 
 __all__ = [
-    "ricker", "damping_profile", "damping_profiles_1d", "pad_edge", "Problem", "make_config",
+    "ricker", "damping_profile", "damping_profiles_1d", "pad_edge", "convection_problem",
+    "laplace_problem", "Problem", "make_config",
     "random_problem", "CONFIG_NAMES",
 ]
 
@@ -289,3 +290,32 @@ def random_problem(ndim: int, shape, space_order: int, nt: int, *, seed: int = 0
     if eta is not None:
         pr.sigma = damping_profiles_1d(shape, nbl, h, vmax)
     return pr
+
+
+# ------------------------------------------------------------------ other paper workloads (f4)
+def convection_problem(nx: int = 81, ny: int = 81, nt: int = 100, sigma: float = 0.2, c: float = 1.0):
+    """Linear convection example (the CFD tutorial's step 5 it reproduces):
+    domain [0, 2]^2, u = 2 on [0.5, 1]^2 and 1 elsewhere, dt = sigma dx.  Returns a dict
+    (u0 [nx][ny] float32, c, dt, dx, dy, nt)."""
+    dx = 2.0 / (nx - 1)
+    dy = 2.0 / (ny - 1)
+    x = np.arange(nx) * dx
+    y = np.arange(ny) * dy
+    u0 = np.ones((nx, ny), dtype=np.float32)
+    u0[np.ix_((x >= 0.5) & (x <= 1.0), (y >= 0.5) & (y <= 1.0))] = 2.0
+    return {"u0": u0, "c": c, "dt": sigma * dx, "dx": dx, "dy": dy, "nt": nt}
+
+
+def laplace_problem(nx: int = 31, ny: int = 31):
+    """Laplace example (the CFD tutorial's step 9): domain [0, 2] x [0, 1],
+    bc = linspace(0, 1, nx), initial p = 0 with the listing's boundary expressions
+    applied (figure 'initial condition of pn.data').  Returns a dict (p0, bc, dx, dy)."""
+    dx = 2.0 / (nx - 1)
+    dy = 1.0 / (ny - 1)
+    bc = np.linspace(0.0, 1.0, nx).astype(np.float32)
+    p0 = np.zeros((nx, ny), dtype=np.float32)
+    p0[:, 0] = 0.0
+    p0[:, ny - 1] = bc
+    p0[0, :] = p0[1, :]
+    p0[nx - 1, :] = p0[nx - 2, :]
+    return {"p0": p0, "bc": bc, "dx": dx, "dy": dy}

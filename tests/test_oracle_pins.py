@@ -398,3 +398,121 @@ def test_damping_term_closed_form():
     np.testing.assert_allclose(core, A + B * lam ** (nt - 1), rtol=1e-13)
     prev = out["u_state"][0][k:-k, k:-k, k:-k]
     np.testing.assert_allclose(prev, A + B * lam ** (nt - 2), rtol=1e-13)
+
+
+# ------------------------------------------------------------------ f4: convection, Laplace
+def test_convection_constant_and_edges():
+    """A constant field is a fixed point bit for bit; the edge points keep their values
+    (reading C21)."""
+    u0 = np.full((12, 15), 1.7)
+    u = oracle.convection2d(u0, c=1.0, dt=0.013, dx=0.05, dy=0.04, nt=9)
+    assert np.array_equal(u, u0)
+    rng = np.random.default_rng(2)
+    u0 = rng.uniform(1, 2, (12, 15))
+    u = oracle.convection2d(u0, c=1.0, dt=0.013, dx=0.05, dy=0.04, nt=9)
+    for sl in (np.s_[0, :], np.s_[-1, :], np.s_[:, 0], np.s_[:, -1]):
+        assert np.array_equal(u[sl], u0[sl])
+
+
+def test_convection_multinomial_closed_form():
+    """Eq. 2 is u^{n+1}_ij = (1-a-b) u_ij + a u_{i-1,j} + b u_{i,j-1}; n steps of it are the
+    multinomial sum_{p+q+s=n} n!/(p! q! s!) (1-a-b)^p a^q b^s u0_{i-q, j-s} wherever the
+    backward cone stays off the fixed edges -- brute force on random data, two (a, b) pairs,
+    including a = b = 1/2 (the binomial average)."""
+    from math import factorial
+    rng = np.random.default_rng(3)
+    u0 = rng.uniform(-1, 1, (18, 17))
+    for c, dt, dx, dy in ((1.0, 0.5, 1.0, 1.0), (0.7, 0.3, 0.9, 1.3)):
+        a, b = c * dt / dx, c * dt / dy
+        n = 5
+        u = oracle.convection2d(u0, c=c, dt=dt, dx=dx, dy=dy, nt=n)
+        for i in range(n + 1, 17):
+            for j in range(n + 1, 16):
+                ref = 0.0
+                for q in range(n + 1):
+                    for s_ in range(n + 1 - q):
+                        p_ = n - q - s_
+                        coef = factorial(n) / (factorial(p_) * factorial(q) * factorial(s_))
+                        ref += coef * (1 - a - b) ** p_ * a ** q * b ** s_ * u0[i - q, j - s_]
+                assert abs(u[i, j] - ref) < 1e-12, (i, j)
+
+
+def test_convection_monotone_and_transport_speed():
+    """a + b <= 1: each step is a convex combination -> min/max principle (upwind).  Away
+    from the edges the upwind scheme moves the perturbation's mass and centroid exactly
+    (its modified equation has no first-moment error): mass conserved, centroid advected
+    by c t along both axes (the physics of Eq. 1 at the discrete level)."""
+    p = synth.convection_problem(81, 81, nt=60)
+    u = oracle.convection2d(p["u0"], c=p["c"], dt=p["dt"], dx=p["dx"], dy=p["dy"], nt=p["nt"])
+    assert u.min() >= 1.0 - 1e-15 and u.max() <= 2.0 + 1e-15 and u.max() < 2.0
+    d0, d = p["u0"].astype(np.float64) - 1.0, u - 1.0
+    assert abs(d.sum() - d0.sum()) < 1e-9 * d0.sum()
+    x = np.arange(81) * p["dx"]
+    t = p["nt"] * p["dt"]
+    for ax in (0, 1):
+        c0 = (d0.sum(axis=1 - ax) * x).sum() / d0.sum()
+        c1 = (d.sum(axis=1 - ax) * x).sum() / d.sum()
+        assert abs((c1 - c0) - p["c"] * t) < 1e-9
+
+
+def _laplace_direct(bc, nx, ny, dx, dy):
+    """The fixed point of the Jacobi sweep with the boundary expressions of P:411-414,
+    as one dense linear solve over the interior unknowns (brute force)."""
+    idx = {}
+    for i in range(1, nx - 1):
+        for j in range(1, ny - 1):
+            idx[(i, j)] = len(idx)
+    A = np.zeros((len(idx), len(idx)))
+    rhs = np.zeros(len(idx))
+    cx, cy = dy * dy, dx * dx
+
+    def add(row, i, j, w):
+        i = 1 if i == 0 else (nx - 2 if i == nx - 1 else i)      # Neumann copies
+        if j == 0:
+            return                                               # p = 0
+        if j == ny - 1:
+            rhs[row] += w * bc[i]
+            return
+        A[row, idx[(i, j)]] -= w
+    for (i, j), row in idx.items():
+        A[row, row] += 2 * (cx + cy)
+        add(row, i + 1, j, cx)
+        add(row, i - 1, j, cx)
+        add(row, i, j + 1, cy)
+        add(row, i, j - 1, cy)
+    x = np.linalg.solve(A, rhs)
+    p = np.zeros((nx, ny))
+    for (i, j), row in idx.items():
+        p[i, j] = x[row]
+    p[:, ny - 1] = bc
+    p[0, :] = p[1, :]
+    p[-1, :] = p[-2, :]
+    return p
+
+
+def test_laplace_fixed_point_equals_direct_solve():
+    """Run to the fixed point (tol < 0: max_iter sweeps) on a small grid: the interior equals
+    the dense solve of the same discrete system (Eq. 4 + the P:411-414 boundary rows)."""
+    q = synth.laplace_problem(12, 10)
+    p, it, l1 = oracle.laplace2d(q["p0"], q["bc"], dx=q["dx"], dy=q["dy"], tol=-1.0, max_iter=20000)
+    assert it == 20000 and abs(l1) < 1e-14
+    ref = _laplace_direct(q["bc"].astype(np.float64), 12, 10, q["dx"], q["dy"])
+    assert np.abs(p[1:-1, 1:-1] - ref[1:-1, 1:-1]).max() < 1e-10
+
+
+def test_laplace_linear_solution_and_stopping_rule():
+    """Constant top boundary C: the fixed point is x-independent and linear in y,
+    p_ij = C j / (n1 - 1) (closed form).  The l1 rule stops at the first sweep
+    with l1 <= tol: one sweep fewer leaves l1 > tol."""
+    nx, ny = 9, 13
+    bc = np.full(nx, 0.8)
+    p0 = np.zeros((nx, ny))
+    p0[:, -1] = bc
+    p, it, l1 = oracle.laplace2d(p0, bc, dx=0.25, dy=0.1, tol=-1.0, max_iter=8000)
+    ref = np.broadcast_to(0.8 * np.arange(ny) / (ny - 1), (nx, ny))
+    assert np.abs(p - ref).max() < 1e-10
+    q = synth.laplace_problem(31, 31)
+    p, it, l1 = oracle.laplace2d(q["p0"], q["bc"], dx=q["dx"], dy=q["dy"], tol=1e-4)
+    assert 0 < it < 100000 and l1 <= 1e-4
+    _, it2, l12 = oracle.laplace2d(q["p0"], q["bc"], dx=q["dx"], dy=q["dy"], tol=1e-4, max_iter=it - 1)
+    assert it2 == it - 1 and l12 > 1e-4
