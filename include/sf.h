@@ -242,6 +242,28 @@ SF_API sf_status sf_create_slab(const sf_desc *global, void *comm, int rank, int
 SF_API sf_status sf_allreduce_gradient(sf_handle *h, void *comm, float *grad, size_t count,
                                        double *J, int rank, void *stream);
 
+/* ---- the paper's other example workloads, 2D fp32, layout [n0][n1] ---- */
+
+/* Linear convection, Eq. 2: nt steps of
+ *   u_ij <- u_ij - c dt/dx (u_ij - u_{i-1,j}) - c dt/dy (u_ij - u_{i,j-1})
+ * on the interior; edge points keep their values (reading C21).  u: device [n0][n1],
+ * in = initial, out = final.  Grids up to 25 600 points run in one CTA (both levels in
+ * shared memory, no launch per step; work may be NULL); larger grids need `work`
+ * (device [n0][n1] scratch) and launch one kernel per step.  Asynchronous on `stream`. */
+SF_API sf_status sf_convection2d(float *u, float *work, int64_t n0, int64_t n1, double c, double dt,
+                                 double dx, double dy, int nt, void *stream);
+
+/* Laplace equation by Jacobi sweeps, Eq. 4, boundary rows as in the listing
+ * (p[x,0]=0, p[x,n1-1]=bc[x], p[0,y]=p[1,y], p[n0-1,y]=p[n0-2,y]), l1 rule of
+ * P:433-447 (reading C22): sweeps until l1 = sum(|p|-|pn|)/sum(|pn|) <= tol or max_iter.
+ * p: device [n0][n1], in = initial buffer, out = the last computed p; bc: device [n0];
+ * work: device [n0][n1] scratch (may be NULL for grids up to 4 096 points, which run in
+ * one CTA; larger grids run one cooperative kernel over all SMs).  The l1 test never
+ * leaves the device.  *iters / *l1 (host) receive the sweep count and the last l1.
+ * Synchronises `stream`. */
+SF_API sf_status sf_laplace2d(float *p, float *work, const float *bc, int64_t n0, int64_t n1, double dx,
+                              double dy, double tol, int max_iter, int *iters, double *l1, void *stream);
+
 SF_API const char *sf_last_error(void);
 SF_API int sf_version(void);
 

@@ -12,6 +12,6 @@ This package never imports ``oracle`` (the fp64 CPU reference used by the tests)
 from ._lib import EXPORTS, LIB_PATH, SfError, build, lib  # noqa: F401
 from .api import (Propagator, allreduce_gradient, fd_weights, forward_host,  # noqa: F401
                   nccl_comm_destroy, nccl_comm_init, nccl_unique_id, slab_halo_plan, slab_plan,
-                  local_group_create, local_group_destroy, sparse_owner)
+                  local_group_create, local_group_destroy, sparse_owner, convection2d, laplace2d)
 
 __version__ = "0.1.0"

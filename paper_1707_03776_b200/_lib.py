@@ -27,7 +27,7 @@ EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint
            "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_create_slab",
            "sf_allreduce_gradient", "sf_local_group_create", "sf_local_group_destroy",
-           "sf_last_error", "sf_version"]
+           "sf_convection2d", "sf_laplace2d", "sf_last_error", "sf_version"]
 
 
 SF_OPT_L2_PREFETCH, SF_OPT_SPLIT, SF_OPT_FUSE_MAX, SF_OPT_COMM_SMS, SF_OPT_GRAPH = 1, 2, 3, 4, 5
@@ -93,6 +93,8 @@ def lib():
             "sf_create_slab": [P, P, I, I, P],
             "sf_allreduce_gradient": [P, P, P, Z, P, I, P],
             "sf_local_group_create": [I, P],
+            "sf_convection2d": [P, P, I64, I64, D, D, D, D, I, P],
+            "sf_laplace2d": [P, P, P, I64, I64, D, D, D, I, P, P, P],
             "sf_local_group_destroy": [P],
         }
         for name, at in sig.items():

@@ -19,7 +19,7 @@ from ._lib import SfDesc, SfError, check, lib
 
 __all__ = ["Propagator", "fd_weights", "forward_host", "slab_plan", "slab_halo_plan", "sparse_owner", "SfError",
            "nccl_unique_id", "nccl_comm_init", "nccl_comm_destroy", "allreduce_gradient",
-           "local_group_create", "local_group_destroy"]
+           "local_group_create", "local_group_destroy", "convection2d", "laplace2d"]
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -351,3 +351,28 @@ def forward_host(m: np.ndarray, damp: Optional[np.ndarray], *, h: float, space_o
                                 None if u_out is None else u_out.ctypes.data_as(ctypes.c_void_p),
                                 _stream(stream)))
     return rec_out
+
+
+# ------------------------------------------------------------------ other paper workloads (f4)
+def convection2d(u: torch.Tensor, *, c: float, dt: float, dx: float, dy: float, nt: int, stream=None):
+    """sf_convection2d: nt steps of Eq. 2 on the device [n0][n1] tensor u, in place."""
+    _dev(u, "u")
+    if u.dim() != 2:
+        raise ValueError("u: expected a 2D [n0][n1] tensor")
+    work = None if u.numel() <= 25600 else torch.empty_like(u)
+    check(lib().sf_convection2d(_ptr(u), _ptr(work), u.shape[0], u.shape[1], float(c), float(dt), float(dx),
+                                float(dy), int(nt), _stream(stream)))
+    return u
+
+
+def laplace2d(p: torch.Tensor, bc: torch.Tensor, *, dx: float, dy: float, tol: float = 1e-4,
+              max_iter: int = 100000, stream=None):
+    """sf_laplace2d: Jacobi sweeps of Eq. 4 with the P:411-414 boundary rows until the l1 rule
+    of P:433-447 holds; p (device [n0][n1]) in place.  Returns (p, sweeps, last l1)."""
+    _dev(p, "p")
+    _dev(bc, "bc", (p.shape[0],))
+    work = None if p.numel() <= 4096 else torch.empty_like(p)
+    it, l1 = ctypes.c_int(), ctypes.c_double()
+    check(lib().sf_laplace2d(_ptr(p), _ptr(work), _ptr(bc), p.shape[0], p.shape[1], float(dx), float(dy),
+                             float(tol), int(max_iter), ctypes.byref(it), ctypes.byref(l1), _stream(stream)))
+    return p, it.value, l1.value
