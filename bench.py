@@ -193,6 +193,8 @@ def run_ours(args):
         prop.set_option(2, 1)
     if args.graph:
         prop.set_option(5, 1)
+    if args.snap_half:
+        prop.set_option(7, 1)
     wav = dev(p.wavelet)
     u = prop.zeros_state()
     rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
@@ -272,7 +274,8 @@ def run_ours(args):
         # nt-1 launches, (nt-1)//k of them also read the snapshot and update the gradient
         # (+12 B/pt) -- averaged over the 2 (nt-1) stencil launches of a gradient
         nk = (p.nt - 1) // k
-        alg_bytes = int(round(npts_local * (bpp + (4 * nk + 12 * nk) / (2 * (p.nt - 1)))))
+        se = 2 if args.snap_half else 4   # snapshot bytes: written on save steps, read on correlation steps
+        alg_bytes = int(round(npts_local * (bpp + (se * nk + (se + 8) * nk) / (2 * (p.nt - 1)))))
     achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     traffic, traffic_rel = ncu_traffic(cfg)
@@ -300,6 +303,7 @@ def run_ours(args):
                              "4-5 fields streamed per update)" if npts_local * 4 > 126e6 else
                              "grid smaller than L2 (configs[0]: launch-bound toy)",
                        "propagations_per_step": passes,
+                       "snapshots": ("fp16" if args.snap_half else "fp32") if grad_mode else None,
                        "damping": ("separable profiles (sf_desc.sigma): beta regenerated in-kernel" if sep else
                                    "eta array (hoisted beta streamed)" if eta_d is not None else "none"),
                        "schedule": ("split (boundary planes, then interior)" if (args.split or world > 1) else
@@ -433,6 +437,8 @@ def main():
                          "to measure its cost without communication")
     ap.add_argument("--graph", action="store_true",
                     help="replay each step as a CUDA graph (SF_OPT_GRAPH; for launch-bound grids)")
+    ap.add_argument("--snap-half", action="store_true",
+                    help="gradient configs: fp16 snapshots (SF_OPT_SNAP_HALF, reading C23)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sep", action="store_true",
                     help="damped configs: regenerate beta in-kernel from the separable damping "

@@ -189,6 +189,13 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   stream ordered after / before `stream` by events -- for small,
                                   launch-bound grids.  Off while profiling and in slab mode;
                                   tuning or option changes drop the cached graphs. (default 0)  */
+#define SF_OPT_SNAP_HALF 7     /* 1: every snapshot array (sf_forward / sf_adjoint `snaps`, the
+                                  gradient workspaces) holds IEEE fp16 values, 2 bytes each:
+                                  u^n rounded to nearest even when saved, widened exactly when
+                                  correlated (reading C23; relative error <= 2^-11 per value in
+                                  the normal range, values beyond 65504 overflow).  Half the
+                                  snapshot memory and bytes.  The TMA kernel then needs
+                                  n2 % 8 == 0 (else the generic kernel runs).  (default 0)       */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */

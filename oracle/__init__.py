@@ -204,15 +204,22 @@ def adjoint(prob=None, *, res=None, m=None, damp=None, shape=None, h=None, space
     return {"srca": srca[:, :nsrc], "v_state": st, "grad": g}
 
 
-def gradient(prob, d_obs, m=None, save_every: int = 1):
+def gradient(prob, d_obs, m=None, save_every: int = 1, snap_dtype=None):
     """FWI gradient at model m (default prob.m): forward with snapshots, residual
     res = d_syn - d_obs, J = 1/2 sum res^2, adjoint with correlation (C13/C14).
-    Returns dict(grad, J, res, d_syn)."""
+    snap_dtype='float16': the snapshots are stored in IEEE half precision before the
+    correlation (reading C23: u^n -> fp32 -> fp16, round to nearest even at both steps,
+    numpy's conversions; widened exactly).  Returns dict(grad, J, res, d_syn)."""
     mm = prob.m if m is None else m
     fw = forward(prob, m=mm, save_every=save_every)
     res = fw["rec"] - _f64(d_obs)
     J = 0.5 * float(np.sum(res * res))
-    ad = adjoint(prob, res=res, m=mm, save_every=save_every, snaps=fw["snaps"])
+    snaps = fw["snaps"]
+    if snap_dtype == "float16":
+        snaps = snaps.astype(np.float32).astype(np.float16).astype(np.float64)
+    elif snap_dtype is not None:
+        raise ValueError(f"snap_dtype {snap_dtype!r}")
+    ad = adjoint(prob, res=res, m=mm, save_every=save_every, snaps=snaps)
     return {"grad": ad["grad"], "J": J, "res": res, "d_syn": fw["rec"]}
 
 

@@ -141,6 +141,7 @@ class Propagator:
             check(lib().sf_create(ctypes.byref(d), ctypes.byref(hnd)))
         self._h = hnd
         self.device = m.device
+        self.snap_dtype = torch.float32
 
     # -------------------------------------------------------------- lifetime
     def close(self):
@@ -158,6 +159,12 @@ class Propagator:
     def nsnap(self, save_every: int) -> int:
         return (self.nt - 1) // save_every + 1
 
+    def _check_snaps(self, snaps: torch.Tensor, save_every: int):
+        shape = (self.nsnap(save_every),) + self.local_shape
+        if not (isinstance(snaps, torch.Tensor) and snaps.is_cuda and snaps.dtype == self.snap_dtype
+                and snaps.is_contiguous() and tuple(snaps.shape) == shape):
+            raise TypeError(f"snaps: expected a contiguous {self.snap_dtype} CUDA tensor of shape {shape}")
+
     def zeros_state(self):
         return torch.zeros((2,) + self.local_shape, device=self.device, dtype=torch.float32)
 
@@ -168,8 +175,11 @@ class Propagator:
 
     def set_option(self, option: int, value: int):
         """sf_set_option: 1 L2 prefetch distance, 2 split boundary launches, 3 fuse-max points,
-        4 SMs left free by the split interior launch, 5 CUDA-graph replay of whole calls."""
+        4 SMs left free by the split interior launch, 5 CUDA-graph replay of whole calls,
+        7 fp16 snapshots."""
         check(lib().sf_set_option(self._h, int(option), int(value)))
+        if int(option) == 7:
+            self.snap_dtype = torch.float16 if value else torch.float32
 
     def tuning(self):
         v, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
@@ -205,9 +215,10 @@ class Propagator:
         else:
             rec = None
         if save_every > 0 and snaps is None:
-            snaps = torch.empty((self.nsnap(save_every),) + self.local_shape, device=self.device)
+            snaps = torch.empty((self.nsnap(save_every),) + self.local_shape, device=self.device,
+                                dtype=self.snap_dtype)
         if snaps is not None:
-            _dev(snaps, "snaps", (self.nsnap(save_every),) + self.local_shape)
+            self._check_snaps(snaps, save_every)
         check(lib().sf_forward(self._h, _ptr(wavelet) if self.nsrc else None, _ptr(rec), _ptr(u),
                                _ptr(snaps), int(save_every), _stream(stream)))
         return rec, u, snaps
@@ -225,7 +236,7 @@ class Propagator:
         else:
             srca = None
         if snaps is not None:
-            _dev(snaps, "snaps", (self.nsnap(save_every),) + self.local_shape)
+            self._check_snaps(snaps, save_every)
             if grad is None:
                 grad = torch.zeros(self.local_shape, device=self.device)
         if grad is not None:

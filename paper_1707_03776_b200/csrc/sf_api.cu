@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "sf_internal.h"
@@ -81,13 +82,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder()
 
 // fp32 tensor [dims[rank-1]]...[dims[0]] (dims[0] fastest), dense strides, box `box`.
 static sf_status make_map(CUtensorMap *m, const void *base, int rank, const int64_t *dims,
-                          const uint32_t *box)
+                          const uint32_t *box, bool half = false)
 {
     auto enc = tmap_encoder();
     if (!enc) return sf_set_error(SF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t gd[5], gs[4];
     cuuint32_t bx[5], es[5];
-    uint64_t stride = 4;
+    uint64_t stride = half ? 2 : 4;
     for (int i = 0; i < rank; ++i) {
         gd[i] = (cuuint64_t)dims[i];
         bx[i] = box[i];
@@ -95,7 +96,8 @@ static sf_status make_map(CUtensorMap *m, const void *base, int rank, const int6
         if (i > 0) gs[i - 1] = stride;
         stride *= (uint64_t)dims[i];
     }
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void *>(base),
+    CUresult r = enc(m, half ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     (cuuint32_t)rank, const_cast<void *>(base),
                      gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return sf_set_error(SF_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -135,8 +137,18 @@ int sf_tma_smem_bytes(int r, int vy, int damp, int mode)
 
 static bool tma_ok(const sf_handle *h)
 {
-    return h->ndim == 3 && (h->nb[2] % 4) == 0 && h->nb[2] >= 4 && h->nb[1] >= 1 &&
+    // 16-byte global strides for TMA: n2 % 4 (fp32 fields), n2 % 8 with fp16 snapshots
+    return h->ndim == 3 && (h->nb[2] % (h->snap_half ? 8 : 4)) == 0 && h->nb[2] >= 4 && h->nb[1] >= 1 &&
            h->N < (int64_t(1) << 40) && h->nb[0] < (int64_t(1) << 31);
+}
+
+// bytes per snapshot element (fp32, or fp16 with SF_OPT_SNAP_HALF)
+static size_t snap_es(const sf_handle *h) { return h->snap_half ? 2 : 4; }
+template <class T>
+static T *snap_slot(T *base, const sf_handle *h, int64_t slot)
+{
+    using B = typename std::conditional<std::is_const<T>::value, const char, char>::type;
+    return reinterpret_cast<T *>(reinterpret_cast<B *>(base) + (size_t)slot * (size_t)h->N * snap_es(h));
 }
 
 static int resolve_variant(const sf_handle *h)
@@ -344,7 +356,8 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     a.c3 = h->c3;
     a.beta = h->beta;
     a.snap_out = b.snap_out;
-    a.snap_in = b.snaps ? b.snaps + (int64_t)b.snap_slot * h->N : nullptr;
+    a.snap_in = b.snaps ? snap_slot(b.snaps, h, b.snap_slot) : nullptr;
+    a.snap_half = h->snap_half ? 1 : 0;
     a.grad = b.grad;
     a.gscale = b.gscale;
     if (h->ndim == 3) {
@@ -393,7 +406,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         if (mode == SF_MODE_GRAD) {
             const int64_t d4[4] = {h->nb[2], h->nb[1], h->nb[0], b.nsnap};
             const uint32_t b4[4] = {(uint32_t)TZ, (uint32_t)BY, 1, 1};
-            if ((s = make_map(&maps.snap, b.snaps, 4, d4, b4))) return s;
+            if ((s = make_map(&maps.snap, b.snaps, 4, d4, b4, h->snap_half))) return s;
             if ((s = make_map(&maps.grad, b.grad, 3, d3, bpl))) return s;
         }
     }
@@ -455,10 +468,12 @@ static sf_status launch_inject(sf_handle *h, const SfSparse &sp, float *u, const
     ProfScope ps(h, PK_INJECT, st);
     if (sp.jk > 0)
         k_inject_ell<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.jk, sp.ej_pt, sp.ej_coef, sp.ntgt,
-                                                             vals, snap_patch, grad_snap, grad, gscale);
+                                                             vals, snap_patch, grad_snap, grad, gscale,
+                                                             h->snap_half ? 1 : 0);
     else
         k_inject<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.j_rowptr, sp.j_pt, sp.j_coef,
-                                                         sp.ntgt, vals, snap_patch, grad_snap, grad, gscale);
+                                                         sp.ntgt, vals, snap_patch, grad_snap, grad, gscale,
+                                                         h->snap_half ? 1 : 0);
     SF_CUDA_TRY(cudaGetLastError());
     return SF_OK;
 }
@@ -951,6 +966,10 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         h->comm_sms = value;
         drop_graphs(h);
         return SF_OK;
+    case SF_OPT_SNAP_HALF:
+        h->snap_half = value != 0;
+        drop_graphs(h);
+        return SF_OK;
     case SF_OPT_GRAPH:
         if (value && !h->gstream) {
             SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
@@ -1069,7 +1088,8 @@ static sf_status launch_inject_list(sf_handle *h, const SfSparse &sp, float *u, 
     ProfScope ps(h, PK_INJECT, st);
     if (sp.jk > 0) {
         k_inject_ell_list<<<(nl + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.jk, sp.ej_pt, sp.ej_coef, sp.ntgt,
-                                                            list, nl, vals, snap_patch, grad_snap, grad, gscale);
+                                                            list, nl, vals, snap_patch, grad_snap, grad, gscale,
+                                                            h->snap_half ? 1 : 0);
     } else {
         return sf_set_error(SF_ERR_INVALID_ARG, "split injection needs <= 8 contributions per target");
     }
@@ -1186,12 +1206,17 @@ static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, fl
         if ((s = post_step_exchange(h, B, st))) return s;
     }
     if ((s = side_interp(h, h->rec, false, B, rec, 0, st))) return s;
-    if (snaps) SF_CUDA_TRY(cudaMemcpyAsync(snaps, B, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
+    if (snaps && h->snap_half) {
+        k_f32_to_f16<<<592, 256, 0, st>>>(reinterpret_cast<__half *>(snaps), B, N);
+        SF_CUDA_TRY(cudaGetLastError());
+    } else if (snaps) {
+        SF_CUDA_TRY(cudaMemcpyAsync(snaps, B, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
+    }
     for (int n = 0; n <= h->nt - 2; ++n) {
         float *cur = (n % 2 == 0) ? B : A;
         float *out = (n % 2 == 0) ? A : B;   // holds u^{n-1}, becomes u^{n+1}
         const bool save = snaps && ((n + 1) % save_every == 0);
-        float *slot = save ? snaps + (int64_t)((n + 1) / save_every) * N : nullptr;
+        float *slot = save ? snap_slot(snaps, h, (n + 1) / save_every) : nullptr;
         const float *wrow = wavelet ? wavelet + (int64_t)n * h->src.np : nullptr;
         float *rrow = rec ? rec + (int64_t)(n + 1) * h->rec.np : nullptr;
         if ((s = wait_interp(h, n - 1, st))) return s;
@@ -1239,7 +1264,7 @@ static sf_status adjoint_body(sf_handle *h, const float *res, float *srca, float
                    g ? grad : nullptr, gscale, &h->rec, rrow, &h->src, srow};
         bool fused_itp = false;
         if ((s = do_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, nullptr,
-                         g ? snaps + (int64_t)(n / save_every) * N : nullptr, st, &fused_itp)))
+                         g ? snap_slot(snaps, h, n / save_every) : nullptr, st, &fused_itp)))
             return s;
         if ((s = side_interp(h, h->src, fused_itp, out, srow, j + 1, st))) return s;
     }
@@ -1363,7 +1388,7 @@ extern "C" size_t sf_gradient_workspace_bytes(const sf_handle *h, int save_every
     if (!h || save_every < 1) return 0;
     const size_t N = (size_t)h->N;
     const size_t nsnap = (size_t)((h->nt - 1) / save_every + 1);
-    return align256(sizeof(float) * N * nsnap) + 2 * align256(sizeof(float) * 2 * N) +
+    return align256(snap_es(h) * N * nsnap) + 2 * align256(sizeof(float) * 2 * N) +
            align256(sizeof(float) * (size_t)h->nt * std::max(h->rec.np, 1)) +
            align256(sizeof(float) * (size_t)h->nt * std::max(h->src.np, 1));
 }
@@ -1381,7 +1406,7 @@ extern "C" sf_status sf_gradient(sf_handle *h, const float *wavelet, const float
     const size_t nsnap = (size_t)((h->nt - 1) / save_every + 1);
     char *p = static_cast<char *>(ws);
     float *snaps = reinterpret_cast<float *>(p);
-    p += align256(sizeof(float) * N * nsnap);
+    p += align256(snap_es(h) * N * nsnap);
     float *u = reinterpret_cast<float *>(p);
     p += align256(sizeof(float) * 2 * N);
     float *v = reinterpret_cast<float *>(p);
@@ -1422,7 +1447,7 @@ extern "C" size_t sf_gradient_ckpt_workspace_bytes(const sf_handle *h, int save_
     const size_t nseg = (size_t)((h->nt - 1 + segment - 1) / segment);
     const size_t nss = (size_t)(segment / save_every + 1);
     const size_t nr = (size_t)std::max(h->rec.np, 1), ns = (size_t)std::max(h->src.np, 1);
-    return align256(sizeof(float) * 2 * N * nseg) + align256(sizeof(float) * N * nss) +
+    return align256(sizeof(float) * 2 * N * nseg) + align256(snap_es(h) * N * nss) +
            2 * align256(sizeof(float) * 2 * N) + align256(sizeof(float) * (size_t)h->nt * nr) +
            align256(sizeof(float) * (size_t)h->nt * ns) + align256(sizeof(float) * (size_t)(segment + 1) * nr) +
            align256(sizeof(float) * (size_t)(segment + 1) * ns);
@@ -1447,7 +1472,7 @@ extern "C" sf_status sf_gradient_ckpt(sf_handle *h, const float *wavelet, const 
     float *ckpt = reinterpret_cast<float *>(p);
     p += align256(sizeof(float) * 2 * N * nseg);
     float *snaps = reinterpret_cast<float *>(p);
-    p += align256(sizeof(float) * N * (size_t)(segment / save_every + 1));
+    p += align256(snap_es(h) * N * (size_t)(segment / save_every + 1));
     float *u = reinterpret_cast<float *>(p);
     p += align256(sizeof(float) * 2 * N);
     float *v = reinterpret_cast<float *>(p);

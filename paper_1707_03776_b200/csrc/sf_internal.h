@@ -116,6 +116,7 @@ struct sf_handle {
     int comm_sms = -1;              // SMs left free by the split interior launch (-1: auto)
     // CUDA graphs of whole time loops (SF_OPT_GRAPH), run on gstream between two events
     bool use_graph = false;
+    bool snap_half = false;         // snapshots stored as fp16 (SF_OPT_SNAP_HALF, reading C23)
     SfGraphCache gfwd, gadj;
     cudaStream_t gstream = nullptr;
     cudaEvent_t ev_gin = nullptr, ev_gout = nullptr;

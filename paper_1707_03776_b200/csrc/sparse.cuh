@@ -13,7 +13,20 @@
 //   residual (BASELINE configs[2]): res = d_syn - d_obs, J = 1/2 sum res^2 (fp64, fixed order)
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
+
+// snapshot element access: fp32, or fp16 (SF_OPT_SNAP_HALF, reading C23: round to nearest
+// even on store, exact widening on load)
+__device__ __forceinline__ float snap_ld(const void *s, int64_t i, int half)
+{
+    return half ? __half2float(static_cast<const __half *>(s)[i]) : static_cast<const float *>(s)[i];
+}
+__device__ __forceinline__ void snap_st(void *s, int64_t i, float v, int half)
+{
+    if (half) static_cast<__half *>(s)[i] = __float2half_rn(v);
+    else static_cast<float *>(s)[i] = v;
+}
 
 __global__ void k_interp(const float *__restrict__ u, const int64_t *__restrict__ idx,
                          const float *__restrict__ W, const int *__restrict__ owned, int np, int nc,
@@ -50,8 +63,9 @@ __global__ void k_interp_ell(const float *__restrict__ u, const int64_t *__restr
 // to k_inject (same terms, same order).
 __global__ void k_inject_ell(float *__restrict__ u, const int64_t *__restrict__ tgt, int K,
                              const int *__restrict__ ept, const float *__restrict__ ecoef, int ntgt,
-                             const float *__restrict__ vals, float *__restrict__ snap_patch,
-                             const float *__restrict__ grad_snap, float *__restrict__ grad, float gscale)
+                             const float *__restrict__ vals, void *__restrict__ snap_patch,
+                             const void *__restrict__ grad_snap, float *__restrict__ grad, float gscale,
+                             int snap_half)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntgt) return;
@@ -61,17 +75,19 @@ __global__ void k_inject_ell(float *__restrict__ u, const int64_t *__restrict__ 
         const float cf = ecoef[(int64_t)c * ntgt + t];
         if (cf != 0.0f) d = __fmaf_rn(cf, vals[ept[(int64_t)c * ntgt + t]], d);
     }
-    u[g] = __fadd_rn(u[g], d);
-    if (snap_patch) snap_patch[g] = __fadd_rn(snap_patch[g], d);
-    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(grad_snap[g], d), grad[g]);
+    const float un = __fadd_rn(u[g], d);
+    u[g] = un;
+    // save step: the snapshot holds the new level after injection (== snap + d in fp32)
+    if (snap_patch) snap_st(snap_patch, g, un, snap_half);
+    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(snap_ld(grad_snap, g, snap_half), d), grad[g]);
 }
 
 // k_inject_ell restricted to a list of target rows (split boundary / interior launches)
 __global__ void k_inject_ell_list(float *__restrict__ u, const int64_t *__restrict__ tgt, int K,
                                   const int *__restrict__ ept, const float *__restrict__ ecoef, int ntgt,
                                   const int *__restrict__ list, int nl, const float *__restrict__ vals,
-                                  float *__restrict__ snap_patch, const float *__restrict__ grad_snap,
-                                  float *__restrict__ grad, float gscale)
+                                  void *__restrict__ snap_patch, const void *__restrict__ grad_snap,
+                                  float *__restrict__ grad, float gscale, int snap_half)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nl) return;
@@ -82,9 +98,11 @@ __global__ void k_inject_ell_list(float *__restrict__ u, const int64_t *__restri
         const float cf = ecoef[(int64_t)c * ntgt + t];
         if (cf != 0.0f) d = __fmaf_rn(cf, vals[ept[(int64_t)c * ntgt + t]], d);
     }
-    u[g] = __fadd_rn(u[g], d);
-    if (snap_patch) snap_patch[g] = __fadd_rn(snap_patch[g], d);
-    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(grad_snap[g], d), grad[g]);
+    const float un = __fadd_rn(u[g], d);
+    u[g] = un;
+    // save step: the snapshot holds the new level after injection (== snap + d in fp32)
+    if (snap_patch) snap_st(snap_patch, g, un, snap_half);
+    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(snap_ld(grad_snap, g, snap_half), d), grad[g]);
 }
 
 // CSR -> ELL (slot-major) for the injection tables
@@ -120,17 +138,20 @@ __global__ void k_interp_list(const float *__restrict__ u, const int *__restrict
 __global__ void k_inject(float *__restrict__ u, const int64_t *__restrict__ tgt,
                          const int *__restrict__ rowptr, const int *__restrict__ ent_pt,
                          const float *__restrict__ ent_coef, int ntgt,
-                         const float *__restrict__ vals, float *__restrict__ snap_patch,
-                         const float *__restrict__ grad_snap, float *__restrict__ grad, float gscale)
+                         const float *__restrict__ vals, void *__restrict__ snap_patch,
+                         const void *__restrict__ grad_snap, float *__restrict__ grad, float gscale,
+                         int snap_half)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntgt) return;
     float d = 0.0f;
     for (int e = rowptr[t]; e < rowptr[t + 1]; ++e) d = __fmaf_rn(ent_coef[e], vals[ent_pt[e]], d);
     const int64_t g = tgt[t];
-    u[g] = __fadd_rn(u[g], d);
-    if (snap_patch) snap_patch[g] = __fadd_rn(snap_patch[g], d);
-    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(grad_snap[g], d), grad[g]);
+    const float un = __fadd_rn(u[g], d);
+    u[g] = un;
+    // save step: the snapshot holds the new level after injection (== snap + d in fp32)
+    if (snap_patch) snap_st(snap_patch, g, un, snap_half);
+    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(snap_ld(grad_snap, g, snap_half), d), grad[g]);
 }
 
 // coef_e = W_e * dt^2 / m[t_e], computed in fp64, rounded once
@@ -155,6 +176,13 @@ __global__ void k_hoist(const float *__restrict__ m, const float *__restrict__ d
         c3[i] = (float)(dt * dt / A);
         if (beta) beta[i] = (float)((mm - 0.5 * e * dt) / A);
     }
+}
+
+// fp32 level -> fp16 snapshot slot (slot 0 of a forward with SF_OPT_SNAP_HALF)
+__global__ void k_f32_to_f16(__half *__restrict__ dst, const float *__restrict__ src, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = __float2half_rn(src[i]);
 }
 
 // hoisted c3 with separable damping (sf_desc.sigma, reading C7): eta = m sigma,

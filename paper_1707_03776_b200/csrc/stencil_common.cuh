@@ -16,6 +16,7 @@
 //   S = out - 2u + old (before injection) = (beta - 1)(u - old) + c3 * Lap
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #define SF_MAXR 8
@@ -140,6 +141,8 @@ struct SfStepArgs {
     float hdt;             // dt / 2 (fp32) for sf_beta_sep
     float *snap_out;       // SAVE: snapshot slot to write (== out values), else NULL
     const float *snap_in;  // GRAD: u^n snapshot slot
+    int snap_half;         // snapshots stored as fp16 (SF_OPT_SNAP_HALF): snap_out / snap_in
+                           // then point to __half data (element offsets unchanged)
     float *grad;           // GRAD: gradient accumulator
     float gscale;          // GRAD: k / dt^2
     int64_t n0b, n1, n2;   // buffer extents (n0b includes slab halo planes)

@@ -45,10 +45,15 @@ k_generic3d(SfStepArgs a)
     const float o = sf_update(u, old, beta, c3, lap);
     if (MODE == SF_MODE_GRAD) {
         const float S = sf_d2(u, old, beta, c3, lap);
-        a.grad[idx] = sf_grad(a.grad[idx], a.gscale, __ldg(a.snap_in + idx), S);
+        const float sn = a.snap_half ? __half2float(reinterpret_cast<const __half *>(a.snap_in)[idx])
+                                     : __ldg(a.snap_in + idx);
+        a.grad[idx] = sf_grad(a.grad[idx], a.gscale, sn, S);
     }
     a.out[idx] = o;
-    if (MODE == SF_MODE_SAVE) a.snap_out[idx] = o;
+    if (MODE == SF_MODE_SAVE) {
+        if (a.snap_half) reinterpret_cast<__half *>(a.snap_out)[idx] = __float2half_rn(o);
+        else a.snap_out[idx] = o;
+    }
 }
 
 // 2D, layout [x][z] (n1 == 1 is not used: n1 holds the z extent here).
@@ -88,8 +93,13 @@ k_generic2d(SfStepArgs a)
     const float o = sf_update(u, old, beta, c3, lap);
     if (MODE == SF_MODE_GRAD) {
         const float S = sf_d2(u, old, beta, c3, lap);
-        a.grad[idx] = sf_grad(a.grad[idx], a.gscale, __ldg(a.snap_in + idx), S);
+        const float sn = a.snap_half ? __half2float(reinterpret_cast<const __half *>(a.snap_in)[idx])
+                                     : __ldg(a.snap_in + idx);
+        a.grad[idx] = sf_grad(a.grad[idx], a.gscale, sn, S);
     }
     a.out[idx] = o;
-    if (MODE == SF_MODE_SAVE) a.snap_out[idx] = o;
+    if (MODE == SF_MODE_SAVE) {
+        if (a.snap_half) reinterpret_cast<__half *>(a.snap_out)[idx] = __float2half_rn(o);
+        else a.snap_out[idx] = o;
+    }
 }

@@ -28,6 +28,7 @@
 // z halo 2 HZ/VZ x 4 B, coefficients 4 B each, + the TMA fills -- no partial-sum ring.
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <type_traits>
 #include "stencil_common.cuh"
 
@@ -187,6 +188,20 @@ __device__ __forceinline__ void stp_if(float *p, const f2_t *v, bool pred)
                      "@q st.global.b64 [%0], %1;\n\t}" ::"l"(p), "l"(v[0]), "r"((uint32_t)pred)
                      : "memory");
 }
+// fp16 snapshot store (SF_OPT_SNAP_HALF): p = (float*)snap_out + e addresses element e; the
+// VZ values go to element e of the __half array at snap_out (round to nearest even)
+template <int VZ>
+__device__ __forceinline__ void stsnap_half(float *snap_out, float *p, const f2_t *v)
+{
+    __half2 *hp = reinterpret_cast<__half2 *>(reinterpret_cast<__half *>(snap_out) + (p - snap_out));
+#pragma unroll
+    for (int jp = 0; jp < VZ / 2; ++jp) {
+        float x, y;
+        upk2(v[jp], x, y);
+        hp[jp] = __floats2half2_rn(x, y);
+    }
+}
+
 __device__ __forceinline__ float lo2(f2_t v)
 {
     float a, b;
@@ -310,7 +325,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                     if (i >= 2 * R) {
                         if (gc >= DC) mbar_wait(cempty + 8 * cs, cph ^ 1u);
                         const uint32_t fb = cfull + 8 * cs;
-                        mbar_expect_tx(fb, C::CST);
+                        // fp16 snapshots: that plane of the stage carries half the bytes
+                        mbar_expect_tx(fb, C::CST - ((MODE == SF_MODE_GRAD && a.snap_half) ? C::PL / 2 : 0));
                         uint32_t pl = cbase + cs * C::CST;
                         tma_load3(pl, &tm_old, z0, y0, q, fb);
                         pl += C::PL;
@@ -401,6 +417,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
         const int qa = (int)sg.qa, qb = (int)sg.qb;
         const int NP = (qb - qa) + 2 * R;
         float *optr = a.out + (int64_t)qa * plane + (int64_t)yg * a.n2 + zg;
+        // snapshot row pointer (element offsets as the output; with fp16 snapshots it only
+        // carries the element index, stsnap_half rebases it onto the __half array)
         float *sptr = (MODE == SF_MODE_SAVE) ? a.snap_out + (optr - a.out) : nullptr;
         float *gptr = (MODE == SF_MODE_GRAD) ? a.grad + (optr - a.out) : nullptr;
         // fused injection: this warp's cursor (warp-uniform), first entry at q >= qa
@@ -563,7 +581,17 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                 for (int jp = 0; jp < NJ; ++jp) bv[j][jp] = ONE2;
                             }
                             if (MODE == SF_MODE_GRAD) {
-                                ldp<VZ>(cp + nxt * PF + j * TZ, sv[j]);
+                                if (a.snap_half) {  // fp16 plane: VZ halves per lane, widened exactly
+                                    const __half2 *hp = reinterpret_cast<const __half2 *>(
+                                        reinterpret_cast<const __half *>(cp - po + nxt * PF) + (po + j * TZ));
+#pragma unroll
+                                    for (int jp = 0; jp < NJ; ++jp) {
+                                        const float2 f = __half22float2(hp[jp]);
+                                        sv[j][jp] = pk2(f.x, f.y);
+                                    }
+                                } else {
+                                    ldp<VZ>(cp + nxt * PF + j * TZ, sv[j]);
+                                }
                                 ldp<VZ>(cp + (nxt + 1) * PF + j * TZ, gv[j]);
                             }
                         }
@@ -632,7 +660,13 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                             for (int j = 0; j < VY; ++j) {
                                 stp_if<VZ>(optr + j * n2, res2[j], act[j]);
-                                if (MODE == SF_MODE_SAVE) stp_if<VZ>(sptr + j * n2, res2[j], act[j]);
+                                if (MODE == SF_MODE_SAVE) {
+                                    if (a.snap_half) {
+                                        if (act[j]) stsnap_half<VZ>(a.snap_out, sptr + j * n2, res2[j]);
+                                    } else {
+                                        stp_if<VZ>(sptr + j * n2, res2[j], act[j]);
+                                    }
+                                }
                                 if (MODE == SF_MODE_GRAD) stp_if<VZ>(gptr + j * n2, gres2[j], act[j]);
                             }
                         } else {
@@ -643,7 +677,10 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                 for (int j = 0; j < VY; ++j) {
                                     if (yg + j < a.n1) {
                                         stp<VZ>(optr + j * a.n2, res2[j]);
-                                        if (MODE == SF_MODE_SAVE) stp<VZ>(sptr + j * a.n2, res2[j]);
+                                        if (MODE == SF_MODE_SAVE) {
+                                            if (a.snap_half) stsnap_half<VZ>(a.snap_out, sptr + j * a.n2, res2[j]);
+                                            else stp<VZ>(sptr + j * a.n2, res2[j]);
+                                        }
                                         if (MODE == SF_MODE_GRAD) stp<VZ>(gptr + j * a.n2, gres2[j]);
                                     }
                                 }

@@ -749,3 +749,36 @@ def test_laplace2d_parity(shape):
         assert abs(it - ito) <= 1 and l1 <= 1e-4
         ref, _, _ = oracle.laplace2d(q["p0"], q["bc"], tol=-1.0, max_iter=it, **kw)
         assert rel(p.cpu().numpy(), ref) <= 1e-5
+
+
+# ------------------------------------------------------------ fp16 snapshots (C23)
+def test_fp16_snapshots_forward_and_gradient():
+    """SF_OPT_SNAP_HALF: saved snapshots are exactly the fp32 snapshots rounded to fp16
+    (bitwise vs torch's conversion); the gradient (TMA and generic, full and checkpointed)
+    matches the oracle with fp16 snapshots (rel. L2 <= 1e-4); TMA == generic == checkpointed
+    bitwise; within the quantisation bound of the fp32-snapshot gradient."""
+    p = synth.random_problem(3, (26, 30, 64), 8, 61, seed=33, nbl=5, nsrc=2, nrec=30)
+    p.m_true = (p.m * 0.9).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    go16 = oracle.gradient(p, d_obs, save_every=3, snap_dtype="float16")
+    prop = make_prop(p)
+    _, _, s32 = prop.forward(dev(p.wavelet), save_every=3)
+    g32, _ = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+    prop.set_option(7, 1)
+    _, _, s16 = prop.forward(dev(p.wavelet), save_every=3)
+    torch.cuda.synchronize()
+    assert s16.dtype == torch.float16 and torch.equal(s16, s32.half())
+    out = []
+    for variant in (2, 1):
+        prop.set_tuning(variant, 0, 0)
+        g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+        gc, Jc = prop.gradient_ckpt(dev(p.wavelet), dev(d_obs), save_every=3, segment=9)
+        torch.cuda.synchronize()
+        out.append(g.cpu().numpy())
+        assert np.array_equal(g.cpu().numpy(), gc.cpu().numpy()) and J == Jc
+        assert rel(g.cpu().numpy(), go16["grad"]) <= TOL, rel(g.cpu().numpy(), go16["grad"])
+        assert abs(J - go16["J"]) <= 1e-4 * go16["J"]
+    assert np.array_equal(out[0], out[1])
+    assert rel(out[0], g32.cpu().numpy()) < 2.0 ** -11 * 4
+    assert prop.gradient_workspace_bytes(3) < make_prop(p).gradient_workspace_bytes(3)
+    prop.close()

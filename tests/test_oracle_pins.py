@@ -516,3 +516,17 @@ def test_laplace_linear_solution_and_stopping_rule():
     assert 0 < it < 100000 and l1 <= 1e-4
     _, it2, l12 = oracle.laplace2d(q["p0"], q["bc"], dx=q["dx"], dy=q["dy"], tol=1e-4, max_iter=it - 1)
     assert it2 == it - 1 and l12 > 1e-4
+
+
+def test_gradient_fp16_snapshots_error_bound():
+    """Reading C23: the oracle's fp16-snapshot gradient uses IEEE round-to-nearest-even
+    (numpy; ties go to even: 1 + 2^-11 -> 1, 1 + 3 2^-11 -> 1 + 2^-9) and stays within the
+    quantisation bound of the exact gradient: |g16 - g| / |g| <= 2^-11 sum|u D2v| / |g|."""
+    t = np.array([1 + 2.0 ** -11, 1 + 3 * 2.0 ** -11, 65504.0, 2.0 ** -24], dtype=np.float32)
+    assert list(t.astype(np.float16).astype(np.float64)) == [1.0, 1 + 2.0 ** -9, 65504.0, 2.0 ** -24]
+    p = synth.random_problem(3, (18, 20, 22), 4, 50, seed=12, nbl=3, nsrc=1, nrec=16)
+    d_obs = oracle.forward(p, m=(p.m * 0.9).astype(np.float32))["rec"]
+    g = oracle.gradient(p, d_obs, save_every=2)["grad"]
+    g16 = oracle.gradient(p, d_obs, save_every=2, snap_dtype="float16")["grad"]
+    e = np.linalg.norm(g16 - g) / np.linalg.norm(g)
+    assert 0 < e < 2.0 ** -11 * 4
