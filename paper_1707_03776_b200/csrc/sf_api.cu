@@ -1534,6 +1534,8 @@ struct HostCache {
     std::mutex mu;
     float *m = nullptr, *damp = nullptr, *wav = nullptr, *rec = nullptr, *u = nullptr;
     size_t nm = 0, nd = 0, nw = 0, nr = 0, nu = 0;
+    cudaStream_t copy = nullptr;  // record downloads overlapping the next time window
+    cudaEvent_t ev = nullptr;
 };
 HostCache g_hc;
 
@@ -1576,9 +1578,39 @@ extern "C" sf_status sf_forward_host(const sf_desc *hd, const float *wavelet_hos
     dd.damp = hd->damp ? g_hc.damp : nullptr;
     sf_handle *h = nullptr;
     if ((s = sf_create(&dd, &h))) return s;
-    s = sf_forward(h, nw ? g_hc.wav : nullptr, nr ? g_hc.rec : nullptr, g_hc.u, nullptr, 0, st);
+    // the forward in a few time windows (the same loop: sf_forward from the state it is
+    // given, wavelet / record rows offset): each window's finished record rows go to the
+    // host on a copy stream while the next window computes -- only the last window's
+    // download stays exposed
+    if (!g_hc.copy) {
+        SF_CUDA_TRY(cudaStreamCreateWithFlags(&g_hc.copy, cudaStreamNonBlocking));
+        SF_CUDA_TRY(cudaEventCreateWithFlags(&g_hc.ev, cudaEventDisableTiming));
+    }
+    const int nwin = (nr && rec_host && hd->nt > 64) ? 4 : 1;
+    const int steps = hd->nt - 1;
+    int64_t row0 = 0;  // first record row not yet downloaded
+    for (int w = 0, b = 0; w < nwin && !s; ++w) {
+        const int len = (w == nwin - 1) ? steps - b : steps / nwin;
+        {
+            NtWindow win(h, len + 1);
+            s = sf_forward(h, nw ? g_hc.wav + (size_t)b * hd->nsrc : nullptr,
+                           nr ? g_hc.rec + (size_t)b * hd->nrec : nullptr, g_hc.u, nullptr, 0, st);
+        }
+        if (s) break;
+        b += len;
+        if (nr && rec_host) {  // rows [row0, b) are final (row b is rewritten, identically, next window)
+            const int64_t row1 = (w == nwin - 1) ? hd->nt : b;
+            SF_CUDA_TRY(cudaEventRecord(g_hc.ev, st));
+            SF_CUDA_TRY(cudaStreamWaitEvent(g_hc.copy, g_hc.ev, 0));
+            cudaError_t e = cudaMemcpyAsync(rec_host + row0 * hd->nrec, g_hc.rec + row0 * hd->nrec,
+                                            sizeof(float) * (size_t)(row1 - row0) * hd->nrec,
+                                            cudaMemcpyDeviceToHost, g_hc.copy);
+            if (e != cudaSuccess) s = sf_set_error(SF_ERR_CUDA, "rec download: %s", cudaGetErrorString(e));
+            row0 = row1;
+        }
+    }
     if (!s && nr && rec_host) {
-        cudaError_t e = cudaMemcpyAsync(rec_host, g_hc.rec, nr * sizeof(float), cudaMemcpyDeviceToHost, st);
+        cudaError_t e = cudaStreamSynchronize(g_hc.copy);
         if (e != cudaSuccess) s = sf_set_error(SF_ERR_CUDA, "rec download: %s", cudaGetErrorString(e));
     }
     if (!s && u_final_host) {
