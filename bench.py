@@ -237,13 +237,17 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
-    for _ in range(args.steps):
+    marks[0].record(stream)
+    for i in range(args.steps):
         step()
+        marks[i + 1].record(stream)
     e1.record(stream)
     barrier()
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     if args.graph:
         prop.set_profiling(True)
         prop.profile(reset=True)
@@ -292,6 +296,8 @@ def run_ours(args):
         result = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+            "step_ms": {"median": round(statistics.median(step_ms), 3), "best": round(min(step_ms), 3),
+                        "rank0_all": [round(x, 3) for x in step_ms]},
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": f"synthetic (seeded {p.name} model of BASELINE configs[{cfg}], readings of "
                     "SURVEY 8.0; no dataset in the paper)",
@@ -311,6 +317,7 @@ def run_ours(args):
                        "kernel_tuning": tuning},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
+                         "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
                          "traffic": None if traffic is None else int(traffic),
                          "traffic_source": (f"{traffic_rel} (ncu --set full, dram read+write per "
                                             "launch, random-init wavefield)") if traffic is not None
