@@ -1,4 +1,4 @@
-# round-1 evidence refresh (final kernels): GPU tests, smoke, bench lines configs[1..4] +
+# evidence refresh (run under gpurun): GPU tests, smoke, bench lines configs[1..4] +
 # reference arm, ncu launch list of the default bench command, full captures on configs[1]/[3]
 set -x
 mkdir -p gpurun_out
