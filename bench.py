@@ -12,7 +12,9 @@ max-over-ranks device time  [GPts/s = 1e9 grid-point updates per second].
 
 N > 1 (torchrun, one rank per GPU): weak scaling -- the grid is slab-decomposed along x
 with 336 planes per rank (global 336N x 336 x 336) and r=4 halo planes exchanged every
-step with NCCL send/recv.  --impl reference runs the fp64 CPU oracle (the only
+step with NCCL send/recv.  With --config 4 (multi-shot FWI gradient) each rank instead
+runs its own shot on the full 400^3 model and every step ends with the NCCL all-reduce
+of the gradient (sf_allreduce_gradient) -- weak scaling by shots.  --impl reference runs the fp64 CPU oracle (the only
 "reference" this paper-only build has) on a bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -113,11 +115,17 @@ class ClockSampler:
 # ---------------------------------------------------------------------------- workload
 def build_problem(nt_override=None, rank=0, nranks=1, cfg=1):
     import synth
+    if cfg == 4:
+        # multi-shot FWI gradient (BASELINE configs[4]): one shot per rank on the
+        # full 400^3 model, gradients summed by sf_allreduce_gradient -- weak scaling by shots
+        p = synth.make_config(cfg, nt=nt_override, shot=rank)
+        return p, p.m, p.damp, p.shape
     p = synth.make_config(cfg, nt=nt_override)
     if nranks == 1:
         return p, p.m, p.damp, p.shape
     if cfg != 1:
-        raise SystemExit("multi-GPU bench runs configs[1] weak-scaled (slab decomposition)")
+        raise SystemExit("multi-GPU bench runs configs[1] weak-scaled (slab decomposition) "
+                         "or configs[4] (one shot per GPU + gradient all-reduce)")
     # weak scaling: global grid (336 N) x 336 x 336 = the configs[1] model tiled along x
     # (its physical part is x-invariant); the absorbing layer stays at the global x edges.
     r = p.space_order // 2
@@ -186,9 +194,11 @@ def run_ours(args):
     # kernel is latency-bound there)
     sep = eta_loc is not None and p.sigma is not None and args.sep
     eta_d = None if (eta_loc is None or sep) else dev(eta_loc)
+    slab = world > 1 and cfg != 4           # configs[4] shards shots, not the grid
     prop = sf.Propagator(m_d, eta_d, shape=gshape, h=p.h, space_order=p.space_order, nt=p.nt,
                          dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords,
-                         comm=comm, rank=rank, nranks=world, sigma=p.sigma if sep else None)
+                         comm=comm if slab else None, rank=rank if slab else 0,
+                         nranks=world if slab else 1, sigma=p.sigma if sep else None)
     if args.split:
         prop.set_option(2, 1)
     if args.graph:
@@ -198,7 +208,7 @@ def run_ours(args):
     wav = dev(p.wavelet)
     u = prop.zeros_state()
     rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
-    npts_local = int(np.prod(prop.local_shape)) if world == 1 else prop.n0_loc * int(np.prod(gshape[1:]))
+    npts_local = int(np.prod(prop.local_shape)) if not slab else prop.n0_loc * int(np.prod(gshape[1:]))
     tuning = prop.tuning()
     log(f"[bench] rank {rank}/{world} grid {gshape} local {prop.local_shape} nt {p.nt} tuning {tuning}")
 
@@ -220,6 +230,9 @@ def run_ours(args):
     def step():
         if grad_mode:
             prop.gradient(wav, d_obs, save_every=k, grad=grad, ws=ws)
+            if world > 1:
+                # multi-shot: sum the per-shot gradients over the GPUs (NCCL, in-stream)
+                prop.allreduce_gradient(comm, grad, rank=rank)
         else:
             u.zero_()
             prop.forward(wav, u=u, rec=rec)
@@ -268,7 +281,7 @@ def run_ours(args):
     # roofline of the dominant kernel (stencil step): algorithmic bytes per launch
     bpp = 20 if eta_d is not None else 16      # u^n, u^{n-1}, out, c3 (+beta array) fp32
     launch_ms = prof["stencil_ms"] / max(prof["stencil_launches"], 1)
-    split = args.split or world > 1
+    split = args.split or slab
     if split:
         # boundary and interior launches overlap: time the stencil by the wall time per update
         launch_ms = ms_max / (args.steps * (p.nt - 1) * passes)
@@ -302,9 +315,11 @@ def run_ours(args):
             "data": f"synthetic (seeded {p.name} model of BASELINE configs[{cfg}], readings of "
                     "SURVEY 8.0; no dataset in the paper)",
             "config": {"workload": WORKLOADS[cfg] + (f" (weak-scaled: {'x'.join(map(str, gshape))} "
-                                                     f"global, slab per GPU)" if world > 1 else ""),
+                                                     f"global, slab per GPU)" if slab else
+                                                     f" (weak-scaled: {world} shots, one per GPU, gradient "
+                                                     f"all-reduce in every step)" if world > 1 else ""),
                        "grid": list(gshape), "space_order": p.space_order, "nt": p.nt,
-                       "points_per_rank": npts_local, "parallelism": f"slab{world}" if world > 1 else "1gpu",
+                       "points_per_rank": npts_local, "parallelism": f"slab{world}" if slab else f"shots{world}" if world > 1 else "1gpu",
                        "l2": "inputs larger than L2 (each fp32 field >= 152 MB > 126 MB L2; "
                              "4-5 fields streamed per update)" if npts_local * 4 > 126e6 else
                              "grid smaller than L2 (configs[0]: launch-bound toy)",
@@ -312,7 +327,7 @@ def run_ours(args):
                        "snapshots": ("fp16" if args.snap_half else "fp32") if grad_mode else None,
                        "damping": ("separable profiles (sf_desc.sigma): beta regenerated in-kernel" if sep else
                                    "eta array (hoisted beta streamed)" if eta_d is not None else "none"),
-                       "schedule": ("split (boundary planes, then interior)" if (args.split or world > 1) else
+                       "schedule": ("split (boundary planes, then interior)" if split else
                                     "single launch per step") + (", CUDA graph replay" if args.graph else ""),
                        "kernel_tuning": tuning},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
