@@ -376,6 +376,41 @@ def test_gradient_subsampled_consistent():
     assert cos > 0.999
 
 
+def test_gradient_identity_from_stored_levels():
+    """Gradient identity (SURVEY 8(c) pins; north_star "g += v u_tt"): the oracle's fused
+    correlation (in-register S plus the injection patch, C13) equals the plain definitions
+    written out on stored levels,
+        g = -sum_{n=1}^{nt-1} u^n (v^{n+1} - 2 v^n + v^{n-1}) / dt^2
+          = -sum_{n=0}^{nt-1} v^n (u^{n+1} - 2 u^n + u^{n-1}) / dt^2   (summation by parts,
+    u^{-1} = u^0 = 0, v^{nt} = v^{nt-1} = 0), to <= 1e-13 relative.  u^n comes from the
+    forward's every-step snapshots; v^s from adjoint runs restarted on the time-shifted
+    residual (nt' = nt - s, res'[n'] = res[n' + s] ends at (v^{s+1}, v^s))."""
+    base, m0, mt, eta = _taylor_problem()
+    nt = 60
+    base = dict(base, nt=nt, wavelet=base["wavelet"][:nt])
+    dt = base["dt"]
+    d_obs = oracle.forward(m=mt, damp=eta, **base)["rec"]
+    fw = oracle.forward(m=m0, damp=eta, save_every=1, **base)
+    res = fw["rec"] - d_obs
+    nosrc = {k: v for k, v in base.items() if k not in ("wavelet", "nt")}
+    g = oracle.adjoint(m=m0, damp=eta, res=res, save_every=1, snaps=fw["snaps"], nt=nt,
+                       **nosrc)["grad"]
+    u = fw["snaps"]                                   # u^0 .. u^{nt-1}
+    v = np.zeros((nt + 1,) + u.shape[1:])             # v^0 .. v^{nt}
+    for s in range(nt - 1):
+        st = oracle.adjoint(m=m0, damp=eta, res=res[s:], nt=nt - s, **nosrc)["v_state"]
+        v[s + 1], v[s] = st[0], st[1]
+    g_uv = -sum(u[n] * (v[n + 1] - 2 * v[n] + v[n - 1]) for n in range(1, nt)) / dt ** 2
+    up = np.concatenate([np.zeros((1,) + u.shape[1:]), u, np.zeros((1,) + u.shape[1:])])
+    # up[n + 1] = u^n; u^{nt} only multiplies v^{nt-1} = 0
+    g_vu = -sum(v[n] * (up[n + 2] - 2 * up[n + 1] + up[n]) for n in range(0, nt - 1)) / dt ** 2
+    scale = np.linalg.norm(g)
+    assert scale > 0
+    assert np.all(v[nt] == 0) and np.all(v[nt - 1] == 0)
+    assert np.linalg.norm(g - g_uv) <= 1e-13 * scale
+    assert np.linalg.norm(g - g_vu) <= 1e-13 * scale
+
+
 def test_damping_term_closed_form():
     """Uniform m and eta, zero Laplacian in the interior: the leapfrog of
     m u_tt + eta u_t = 0 (centred u_t, reading C1) has the closed-form solution
