@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--nt", type=int, default=40)
     ap.add_argument("--damp", action="store_true")
     ap.add_argument("--vy", type=int, default=2)
+    ap.add_argument("--variant", type=int, default=2, help="1 generic, 2 TMA")
     ap.add_argument("--ctas", default="0", help="comma list of persistent CTA counts (0 = auto)")
     ap.add_argument("--shapes", default="336x336x336,336x336x384,336x336x320,336x336x256,336x392x336")
     args = ap.parse_args()
@@ -34,7 +35,7 @@ def main():
         g = torch.Generator(device="cuda").manual_seed(0)
         u0 = torch.randn((2,) + shape, device="cuda", generator=g) * 1e-3
         for ctas in [int(c) for c in args.ctas.split(",")]:
-            prop.set_tuning(2, args.vy, ctas)
+            prop.set_tuning(args.variant, args.vy if args.variant == 2 else 0, ctas)
             best = None
             for rep in range(3):
                 prop.set_profiling(True)
