@@ -196,6 +196,17 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   the normal range, values beyond 65504 overflow).  Half the
                                   snapshot memory and bytes.  The TMA kernel then needs
                                   n2 % 8 == 0 (else the generic kernel runs).  (default 0)       */
+#define SF_OPT_P2P 8           /* slab handles: 1 replaces the per-step NCCL send/recv with
+                                  peer stores -- the boundary-plane kernel (and the injection
+                                  there) writes each owned boundary plane straight into the
+                                  neighbour's halo of the same level, then bumps a counter in the
+                                  neighbour's memory with a stream-ordered write; each rank's
+                                  stream waits on its counters (cuStreamWaitValue32) before the
+                                  halo is read.  Buffers are exchanged per call: local groups
+                                  share pointers, NCCL ranks CUDA IPC handles (all-gathered over
+                                  NCCL; the state buffer `u`/`v` must come from cudaMalloc, e.g.
+                                  torch's caching allocator).  Every rank must own > 2r planes
+                                  (SF_ERR_SHAPE).  Bitwise equal to the NCCL exchange. (default 0) */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */

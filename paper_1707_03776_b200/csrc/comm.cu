@@ -10,6 +10,7 @@
 //   send owned planes [n0_loc, n0_loc + r) -> right neighbour's left halo [0, r)
 // Each face is one contiguous r * n1 * n2 block (x is the outermost axis): no packing.
 // Global edges keep their zero halo (Dirichlet ghost, reading C6).
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 
 #include <condition_variable>
@@ -32,6 +33,7 @@ struct NcclApi {
     decltype(&ncclGroupStart) GroupStart = nullptr;
     decltype(&ncclGroupEnd) GroupEnd = nullptr;
     decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
     decltype(&ncclGetErrorString) GetErrorString = nullptr;
     bool ok = false;
 };
@@ -56,10 +58,11 @@ NcclApi &api()
         SF_SYM(GroupStart);
         SF_SYM(GroupEnd);
         SF_SYM(AllReduce);
+        SF_SYM(AllGather);
         SF_SYM(GetErrorString);
 #undef SF_SYM
         a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv &&
-               a.GroupStart && a.GroupEnd && a.AllReduce && a.GetErrorString;
+               a.GroupStart && a.GroupEnd && a.AllReduce && a.AllGather && a.GetErrorString;
     });
     return a;
 }
@@ -124,6 +127,7 @@ struct LocalGroup {
     long long gen = 0;
     std::vector<cudaEvent_t> ev, done;
     std::vector<void *> ptr;
+    std::vector<void *> p2p;  // [rank][3]: state buffers A, B and the P2P counters
     void barrier()
     {
         std::unique_lock<std::mutex> lk(mu);
@@ -191,6 +195,7 @@ extern "C" sf_status sf_local_group_create(int nranks, void **group_out)
     G->ev.resize(nranks);
     G->done.resize(nranks);
     G->ptr.assign(nranks, nullptr);
+    G->p2p.assign(3 * (size_t)nranks, nullptr);
     for (int q = 0; q < nranks; ++q) {
         SF_CUDA_TRY(cudaEventCreateWithFlags(&G->ev[q], cudaEventDisableTiming));
         SF_CUDA_TRY(cudaEventCreateWithFlags(&G->done[q], cudaEventDisableTiming));
@@ -319,4 +324,105 @@ extern "C" sf_status sf_allreduce_gradient(sf_handle *h, void *comm, float *grad
         SF_CUDA_TRY(cudaStreamSynchronize(st));
     }
     return SF_OK;
+}
+
+// ------------------------------------------------------------ peer-store halo exchange
+// (SF_OPT_P2P).  Every call publishes the rank's state buffers (A, B: the two
+// time levels it ping-pongs) and its counters; the neighbours' copies become the mirror
+// targets of the boundary-plane stencil / injection and of the counter writes.
+static sf_status ipc_open(sf_handle *h, const cudaIpcMemHandle_t &hd, void **out)
+{
+    const std::string key(reinterpret_cast<const char *>(&hd), sizeof hd);
+    for (auto &e : h->ipc_open)
+        if (e.first == key) {
+            *out = e.second;
+            return SF_OK;
+        }
+    void *p = nullptr;
+    SF_CUDA_TRY(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_open.emplace_back(key, p);
+    *out = p;
+    return SF_OK;
+}
+
+sf_status sf_comm_p2p_setup(sf_handle *h, float *A, float *B, cudaStream_t st)
+{
+    h->p2p_own[0] = A;
+    h->p2p_own[1] = B;
+    void *mine[3] = {A, B, h->p2p_flags};
+    const int nb[2] = {h->rank - 1, h->rank + 1};
+    void *theirs[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    if (LocalGroup *G = as_local(h->comm)) {
+        for (int k = 0; k < 3; ++k) G->p2p[3 * (size_t)h->rank + k] = mine[k];
+        SF_CUDA_TRY(cudaEventRecord(G->ev[h->rank], st));
+        G->barrier();
+        for (int side = 0; side < 2; ++side) {
+            const int q = nb[side];
+            if (q < 0 || q >= h->nranks) continue;
+            for (int k = 0; k < 3; ++k) theirs[side][k] = G->p2p[3 * (size_t)q + k];
+            // the neighbour's earlier work on those buffers comes first
+            SF_CUDA_TRY(cudaStreamWaitEvent(st, G->ev[q], 0));
+        }
+        G->barrier();
+    } else {
+        // separate processes: CUDA IPC handles of the allocations holding A, B and the
+        // counters (+ offsets), all-gathered over NCCL; opened once per handle
+        sf_status s = need_nccl();
+        if (s) return s;
+        static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+        if (!range) {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                return sf_set_error(SF_ERR_CUDA, "cuMemGetAddressRange unavailable");
+            range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+        }
+        struct Rec {
+            cudaIpcMemHandle_t hd[3];
+            int64_t off[3];
+        };
+        Rec me;
+        memset(&me, 0, sizeof me);
+        for (int k = 0; k < 3; ++k) {
+            CUdeviceptr base = 0;
+            size_t sz = 0;
+            if (range(&base, &sz, reinterpret_cast<CUdeviceptr>(mine[k])) != CUDA_SUCCESS)
+                return sf_set_error(SF_ERR_CUDA, "cuMemGetAddressRange failed");
+            SF_CUDA_TRY(cudaIpcGetMemHandle(&me.hd[k], reinterpret_cast<void *>(base)));
+            me.off[k] = reinterpret_cast<char *>(mine[k]) - reinterpret_cast<char *>(base);
+        }
+        std::vector<Rec> all(h->nranks);
+        Rec *d = nullptr;
+        SF_CUDA_TRY(cudaMalloc(&d, sizeof(Rec) * (h->nranks + 1)));
+        SF_CUDA_TRY(cudaMemcpyAsync(d + h->nranks, &me, sizeof(Rec), cudaMemcpyHostToDevice, st));
+        SF_NCCL_TRY(api().AllGather(d + h->nranks, d, sizeof(Rec), ncclChar, static_cast<ncclComm_t>(h->comm), st));
+        SF_CUDA_TRY(cudaMemcpyAsync(all.data(), d, sizeof(Rec) * h->nranks, cudaMemcpyDeviceToHost, st));
+        SF_CUDA_TRY(cudaStreamSynchronize(st));
+        cudaFree(d);
+        for (int side = 0; side < 2; ++side) {
+            const int q = nb[side];
+            if (q < 0 || q >= h->nranks) continue;
+            for (int k = 0; k < 3; ++k) {
+                void *p = nullptr;
+                if ((s = ipc_open(h, all[q].hd[k], &p))) return s;
+                theirs[side][k] = static_cast<char *>(p) + all[q].off[k];
+            }
+        }
+    }
+    for (int side = 0; side < 2; ++side) {
+        h->p2p_nbr[side][0] = static_cast<float *>(theirs[side][0]);
+        h->p2p_nbr[side][1] = static_cast<float *>(theirs[side][1]);
+        // the left neighbour's counter [1] is written by its right neighbour (this rank), the
+        // right neighbour's counter [0] by its left neighbour
+        h->p2p_nflag[side] = theirs[side][2] ? static_cast<uint32_t *>(theirs[side][2]) + (side == 0 ? 1 : 0)
+                                             : nullptr;
+    }
+    return SF_OK;
+}
+
+void sf_comm_p2p_release(sf_handle *h)
+{
+    for (auto &e : h->ipc_open) cudaIpcCloseMemHandle(e.second);
+    h->ipc_open.clear();
 }

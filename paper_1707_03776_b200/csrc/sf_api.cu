@@ -64,6 +64,37 @@ extern "C" sf_status sf_fd_weights(int space_order, double *w)
     return SF_OK;
 }
 
+// ------------------------------------------------------------------ stream memory operations
+// (SF_OPT_P2P counters: a stream-ordered 32-bit write after the boundary work, a stream wait
+// on the value in the neighbour -- no kernel ever spins on another rank)
+typedef CUresult (*sf_pfn_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static sf_pfn_value32 memop_fn(const char *name)
+{
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+        return reinterpret_cast<sf_pfn_value32>(p);
+    return nullptr;
+}
+static sf_status stream_write32(cudaStream_t st, uint32_t *addr, uint32_t v)
+{
+    static sf_pfn_value32 fn = memop_fn("cuStreamWriteValue32");
+    if (!fn) return sf_set_error(SF_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+    // default flags: a memory fence orders the preceding peer stores before the value
+    if (fn(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v, 0) != CUDA_SUCCESS)
+        return sf_set_error(SF_ERR_CUDA, "cuStreamWriteValue32 failed");
+    return SF_OK;
+}
+static sf_status stream_wait32(cudaStream_t st, uint32_t *addr, uint32_t v)
+{
+    static sf_pfn_value32 fn = memop_fn("cuStreamWaitValue32");
+    if (!fn) return sf_set_error(SF_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+    // CU_STREAM_WAIT_VALUE_GEQ (0): (int32)(*addr - v) >= 0, wrap-around safe
+    if (fn(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v, 0) != CUDA_SUCCESS)
+        return sf_set_error(SF_ERR_CUDA, "cuStreamWaitValue32 failed");
+    return SF_OK;
+}
+
 // ------------------------------------------------------------------ tensor maps (TMA)
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder()
 {
@@ -223,6 +254,9 @@ struct StepBufs {
     int64_t xa = 0, xb = 0;  // planes to compute (xa == xb: the handle's full range)
     int64_t xa2 = 0, xb2 = 0;  // optional second range in the same launch
     int ctas_cap = 0;          // > 0: at most this many persistent TMA CTAs (split interior)
+    int itp_cur = -1;          // side-stream record index of the `cur` level (SF_OPT_P2P ordering)
+    bool force_generic = false;            // thread-per-point kernel (P2P boundary launch)
+    const int64_t *mq = nullptr, *md = nullptr;  // peer-store mirror (SfStepArgs::mq / md)
 };
 
 // Library-internal device allocations come from the device's stream-ordered memory pool
@@ -378,8 +412,13 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
 
     SfLaunch L{};
     L.ndim = h->ndim;
-    L.variant = resolve_variant(h);
+    L.variant = b.force_generic ? SF_VAR_GENERIC : resolve_variant(h);
     L.vy = resolve_vy(h);
+    if (b.mq) {
+        for (int k = 0; k < 4; ++k) a.mq[k] = b.mq[k];
+        a.md[0] = b.md[0];
+        a.md[1] = b.md[1];
+    }
     L.ctas = resolve_ctas(h);
     if (b.ctas_cap > 0 && b.ctas_cap < L.ctas) L.ctas = b.ctas_cap;
     L.sms = h->sms;
@@ -697,6 +736,8 @@ extern "C" void sf_destroy(sf_handle *h)
     if (h->side) cudaStreamDestroy(h->side);
     if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
     if (h->hi_stream) cudaStreamDestroy(h->hi_stream);
+    sf_comm_p2p_release(h);
+    if (h->p2p_flags) (cudaFree)(h->p2p_flags);
     if (h->ev_pre) cudaEventDestroy(h->ev_pre);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
     if (h->ev_xch) cudaEventDestroy(h->ev_xch);
@@ -966,6 +1007,26 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         h->comm_sms = value;
         drop_graphs(h);
         return SF_OK;
+    case SF_OPT_P2P:
+        if (value) {
+            if (h->nranks < 2) return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_P2P needs a slab handle (nranks > 1)");
+            for (int q = 0; q < h->nranks; ++q) {  // every rank must run the split step
+                int64_t x0 = 0, nl = 0;
+                sf_status s = sf_slab_plan(h->gshape[0], h->so, q, h->nranks, &x0, &nl);
+                if (s) return s;
+                if (nl <= 2 * h->r)
+                    return sf_set_error(SF_ERR_SHAPE, "SF_OPT_P2P: rank %d owns %lld planes <= 2r", q, (long long)nl);
+            }
+            if (!h->p2p_flags) {
+                // plain cudaMalloc (not the stream-ordered pool): CUDA IPC exports it
+                SF_CUDA_TRY((cudaMalloc)((void **)&h->p2p_flags, 2 * sizeof(uint32_t)));
+                SF_CUDA_TRY(cudaMemset(h->p2p_flags, 0, 2 * sizeof(uint32_t)));
+                SF_CUDA_TRY(cudaDeviceSynchronize());
+                h->p2p_seq = 0;
+            }
+        }
+        h->p2p = value != 0;
+        return SF_OK;
     case SF_OPT_SNAP_HALF:
         h->snap_half = value != 0;
         drop_graphs(h);
@@ -1082,18 +1143,98 @@ static sf_status ensure_split_lists(sf_handle *h, SfSparse &sp)
 
 static sf_status launch_inject_list(sf_handle *h, const SfSparse &sp, float *u, const float *vals,
                                     const int *list, int nl, float *snap_patch, const float *grad_snap,
-                                    float *grad, float gscale, cudaStream_t st)
+                                    float *grad, float gscale, cudaStream_t st,
+                                    const int64_t *mq = nullptr, const int64_t *md = nullptr)
 {
     if (nl <= 0 || !vals) return SF_OK;
     ProfScope ps(h, PK_INJECT, st);
+    SfMirror mir{};
+    mir.plane = h->N / h->nb[0];
+    if (mq) {
+        for (int k = 0; k < 4; ++k) mir.mq[k] = mq[k];
+        mir.md[0] = md[0];
+        mir.md[1] = md[1];
+    }
     if (sp.jk > 0) {
         k_inject_ell_list<<<(nl + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.jk, sp.ej_pt, sp.ej_coef, sp.ntgt,
                                                             list, nl, vals, snap_patch, grad_snap, grad, gscale,
-                                                            h->snap_half ? 1 : 0);
+                                                            h->snap_half ? 1 : 0, mir);
     } else {
         return sf_set_error(SF_ERR_INVALID_ARG, "split injection needs <= 8 contributions per target");
     }
     SF_CUDA_TRY(cudaGetLastError());
+    return SF_OK;
+}
+
+// Split step with the peer-store halo exchange (SF_OPT_P2P).  High-priority
+// stream: the boundary planes by the thread-per-point kernel, which also stores each owned
+// boundary plane into the neighbour's halo of the same level (peer-mapped pointer), and
+// their injection (mirrored likewise); then one counter write per neighbour.  The main
+// stream computes the interior meanwhile and finally waits until both neighbours' counters
+// reach this step (their planes are in this rank's halo).  Ordering across ranks:
+//   RAW  the halo of level n+1 is read (next step's boundary launch, this level's
+//        record) only after the counter wait of step n;
+//   WAR  a neighbour overwrites the buffer of this rank's `cur` level (its halo) at step
+//        n+1, after this step's counter -- written after this rank's last reads of that halo
+//        (the boundary launch above and the side-stream record of `cur`).
+// The boundary launch uses the generic kernel: a mirror test in the hot TMA loop measured
+// 17 % slower on configs[1], and the boundary launch is 2r planes (the TMA kernel would
+// re-read 2r warm-up planes for them anyway).
+static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepBufs bi, int mode,
+                             float *snap_patch, const float *grad_snap, cudaStream_t st, bool *fused_itp)
+{
+    sf_status s;
+    const int64_t r = h->r;
+    const int ob = b.out == h->p2p_own[0] ? 0 : b.out == h->p2p_own[1] ? 1 : -1;
+    if (ob < 0) return sf_set_error(SF_ERR_INVALID_ARG, "P2P step on a buffer outside the published state");
+    int64_t plan[7], qp[7];
+    if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank, h->nranks, plan))) return s;
+    const int64_t plane = h->N / h->nb[0];
+    auto delta = [](const float *to, const float *from) {
+        return (int64_t)(reinterpret_cast<uintptr_t>(to) - reinterpret_cast<uintptr_t>(from));
+    };
+    int64_t mq[4] = {0, 0, 0, 0}, md[2] = {0, 0};
+    if (plan[5]) {  // owned [r, 2r) -> left neighbour's right halo
+        if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank - 1, h->nranks, qp))) return s;
+        mq[0] = plan[0];
+        mq[1] = plan[0] + r;
+        md[0] = delta(h->p2p_nbr[0][ob] + qp[3] * plane, b.out + plan[0] * plane);
+    }
+    if (plan[6]) {  // owned [nl, nl + r) -> right neighbour's left halo
+        if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank + 1, h->nranks, qp))) return s;
+        mq[2] = plan[2];
+        mq[3] = plan[2] + r;
+        md[1] = delta(h->p2p_nbr[1][ob] + qp[1] * plane, b.out + plan[2] * plane);
+    }
+    bb.force_generic = true;
+    bb.mq = mq;
+    bb.md = md;
+    bool fused = false, f2 = false, fi2 = false;
+    SF_CUDA_TRY(cudaEventRecord(h->ev_pre, st));
+    SF_CUDA_TRY(cudaStreamWaitEvent(h->hi_stream, h->ev_pre, 0));
+    if ((s = launch_step(h, bb, mode, h->hi_stream, &fused, fused_itp))) return s;
+    const bool need_inj = !fused && b.inj && b.inj->ntgt > 0 && b.inj_vals;
+    if (need_inj) {
+        if ((s = ensure_split_lists(h, *b.inj))) return s;
+        if ((s = launch_inject_list(h, *b.inj, b.out, b.inj_vals, b.inj->jl_bnd, b.inj->n_bnd, snap_patch,
+                                    grad_snap, b.grad, b.gscale, h->hi_stream, mq, md)))
+            return s;
+    }
+    if (b.itp_cur >= 0 && h->itp_pending[b.itp_cur & 1])
+        SF_CUDA_TRY(cudaStreamWaitEvent(h->hi_stream, h->ev_itp[b.itp_cur & 1], 0));
+    SF_CUDA_TRY(cudaEventRecord(h->ev_bnd, h->hi_stream));
+    const uint32_t seq = h->p2p_seq + 1;
+    for (int side = 0; side < 2; ++side)
+        if (h->p2p_nflag[side] && (s = stream_write32(h->hi_stream, h->p2p_nflag[side], seq))) return s;
+    if ((s = launch_step(h, bi, mode, st, &f2, &fi2))) return s;
+    // (the interior TMA launch may inject its own planes' targets itself)
+    if (need_inj && !f2 && (s = launch_inject_list(h, *b.inj, b.out, b.inj_vals, b.inj->jl_int, b.inj->n_int,
+                                                   snap_patch, grad_snap, b.grad, b.gscale, st)))
+        return s;
+    SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_bnd, 0));
+    if (plan[5] && (s = stream_wait32(st, h->p2p_flags + 0, seq))) return s;
+    if (plan[6] && (s = stream_wait32(st, h->p2p_flags + 1, seq))) return s;
+    h->p2p_seq = seq;
     return SF_OK;
 }
 
@@ -1125,6 +1266,7 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
     // the NCCL exchange kernels (and the side-stream records) run concurrently
     const int reserve = h->comm_sms >= 0 ? h->comm_sms : (h->nranks > 1 ? 8 : 0);
     if (reserve > 0) bi.ctas_cap = std::max(1, h->sms - reserve);
+    if (h->p2p && h->nranks > 1) return do_step_p2p(h, b, bb, bi, mode, snap_patch, grad_snap, st, fused_itp);
     SF_CUDA_TRY(cudaEventRecord(h->ev_pre, st));
     SF_CUDA_TRY(cudaStreamWaitEvent(h->hi_stream, h->ev_pre, 0));
     if ((s = launch_step(h, bb, mode, h->hi_stream, &fused, fused_itp))) return s;
@@ -1203,6 +1345,7 @@ static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, fl
     sf_status s;
     h->itp_pending[0] = h->itp_pending[1] = false;
     if (h->nranks > 1) {  // make the halo of u^0 valid for the first stencil / record
+        if (h->p2p && (s = sf_comm_p2p_setup(h, A, B, st))) return s;
         if ((s = post_step_exchange(h, B, st))) return s;
     }
     if ((s = side_interp(h, h->rec, false, B, rec, 0, st))) return s;
@@ -1221,6 +1364,7 @@ static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, fl
         float *rrow = rec ? rec + (int64_t)(n + 1) * h->rec.np : nullptr;
         if ((s = wait_interp(h, n - 1, st))) return s;
         StepBufs b{cur, out, slot, nullptr, 0, 0, nullptr, 0.f, &h->src, wrow, &h->rec, rrow};
+        b.itp_cur = n;
         bool fused_itp = false;
         if ((s = do_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, slot, nullptr, st, &fused_itp))) return s;
         if ((s = side_interp(h, h->rec, fused_itp, out, rrow, n + 1, st))) return s;
@@ -1247,6 +1391,7 @@ static sf_status adjoint_body(sf_handle *h, const float *res, float *srca, float
     float *A = v, *B = v + N;  // A = v^{nt}, B = v^{nt-1}
     sf_status s;
     if (h->nranks > 1) {
+        if (h->p2p && (s = sf_comm_p2p_setup(h, A, B, st))) return s;
         if ((s = post_step_exchange(h, B, st))) return s;
     }
     h->itp_pending[0] = h->itp_pending[1] = false;
@@ -1262,6 +1407,7 @@ static sf_status adjoint_body(sf_handle *h, const float *res, float *srca, float
         float *srow = srca ? srca + (int64_t)(n - 1) * h->src.np : nullptr;
         StepBufs b{cur, out, nullptr, g ? snaps : nullptr, g ? n / save_every : 0, nsnap,
                    g ? grad : nullptr, gscale, &h->rec, rrow, &h->src, srow};
+        b.itp_cur = j;
         bool fused_itp = false;
         if ((s = do_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, nullptr,
                          g ? snap_slot(snaps, h, n / save_every) : nullptr, st, &fused_itp)))

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/sf.h"
@@ -120,6 +121,16 @@ struct sf_handle {
     SfGraphCache gfwd, gadj;
     cudaStream_t gstream = nullptr;
     cudaEvent_t ev_gin = nullptr, ev_gout = nullptr;
+    // peer-store halo exchange (SF_OPT_P2P): the boundary-plane kernel stores the
+    // owned boundary planes straight into the neighbours' halos (peer-mapped pointers) and
+    // signals with a stream-ordered counter write; the neighbour's stream waits on the value
+    bool p2p = false;
+    uint32_t *p2p_flags = nullptr;    // own device counters: [0] written by the left, [1] by the right neighbour
+    uint32_t p2p_seq = 0;             // P2P steps completed (the value the next step writes is seq + 1)
+    float *p2p_own[2] = {nullptr, nullptr};                  // own state buffers (A, B) of the current call
+    float *p2p_nbr[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [left/right][A/B] of the neighbours
+    uint32_t *p2p_nflag[2] = {nullptr, nullptr};             // the neighbours' counters this rank writes
+    std::vector<std::pair<std::string, void *>> ipc_open;    // opened IPC handles (NCCL mode), closed at destroy
 };
 
 // error reporting (thread-local message)
@@ -134,6 +145,10 @@ sf_status sf_set_error(sf_status s, const char *fmt, ...);
 
 // comm.cu
 sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st);
+// SF_OPT_P2P: publish this rank's state buffers (A, B) and counters, fetch the neighbours'
+// (local group: in-process pointers; NCCL: CUDA IPC handles all-gathered over NCCL)
+sf_status sf_comm_p2p_setup(sf_handle *h, float *A, float *B, cudaStream_t st);
+void sf_comm_p2p_release(sf_handle *h);
 sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st, int rank);
 sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st, int rank);
 bool sf_comm_is_local(void *comm);

@@ -82,12 +82,20 @@ __global__ void k_inject_ell(float *__restrict__ u, const int64_t *__restrict__ 
     if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(snap_ld(grad_snap, g, snap_half), d), grad[g]);
 }
 
+// peer-store halo exchange (SF_OPT_P2P): a target in plane [mq[0], mq[1]) / [mq[2], mq[3])
+// also writes its final value at byte offset md[0] / md[1] (the neighbour's halo)
+struct SfMirror {
+    int64_t plane;   // points per x-plane
+    int64_t mq[4];
+    int64_t md[2];
+};
+
 // k_inject_ell restricted to a list of target rows (split boundary / interior launches)
 __global__ void k_inject_ell_list(float *__restrict__ u, const int64_t *__restrict__ tgt, int K,
                                   const int *__restrict__ ept, const float *__restrict__ ecoef, int ntgt,
                                   const int *__restrict__ list, int nl, const float *__restrict__ vals,
                                   void *__restrict__ snap_patch, const void *__restrict__ grad_snap,
-                                  float *__restrict__ grad, float gscale, int snap_half)
+                                  float *__restrict__ grad, float gscale, int snap_half, SfMirror mir)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nl) return;
@@ -100,6 +108,9 @@ __global__ void k_inject_ell_list(float *__restrict__ u, const int64_t *__restri
     }
     const float un = __fadd_rn(u[g], d);
     u[g] = un;
+    const int64_t q = g / mir.plane;
+    if (q >= mir.mq[0] && q < mir.mq[1]) *reinterpret_cast<float *>(reinterpret_cast<char *>(u + g) + mir.md[0]) = un;
+    else if (q >= mir.mq[2] && q < mir.mq[3]) *reinterpret_cast<float *>(reinterpret_cast<char *>(u + g) + mir.md[1]) = un;
     // save step: the snapshot holds the new level after injection (== snap + d in fp32)
     if (snap_patch) snap_st(snap_patch, g, un, snap_half);
     if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(snap_ld(grad_snap, g, snap_half), d), grad[g]);

@@ -131,6 +131,12 @@ __device__ __forceinline__ float sf_beta_sep(float sx, float sy, float sz, float
     return __fmul_rn(__fsub_rn(1.0f, s), sf_rcp(__fadd_rn(1.0f, s)));
 }
 
+// byte offset of a peer-store mirror (SfStepArgs::md): the same element in the neighbour's buffer
+__device__ __forceinline__ float *sf_mirror(float *p, int64_t db)
+{
+    return reinterpret_cast<float *>(reinterpret_cast<char *>(p) + db);
+}
+
 // Kernel parameter block shared by all stencil variants.
 struct SfStepArgs {
     const float *cur;      // u^n (read, with neighbours)
@@ -149,6 +155,12 @@ struct SfStepArgs {
     int64_t xa, xb;        // planes [xa, xb) of the buffer to compute
     int64_t xa2, xb2;      // optional second range [xa2, xb2) in the same launch (xa2 == xb2: none)
     SfWeights w;
+    // Peer-store halo exchange (SF_OPT_P2P): an output plane q in [mq[0], mq[1])
+    // is also stored at byte offset md[0] from its own address (the left neighbour's right
+    // halo, a peer-mapped pointer), q in [mq[2], mq[3]) at md[1] (the right neighbour's
+    // left halo).  Empty ranges: no mirror.
+    int64_t mq[4];
+    int64_t md[2];
     int l2_prefetch;       // TMA kernel: L2 prefetch distance in planes (0 = off)
     // Fused sparse work of the TMA kernel (NULL *_beg = none).  Lists are per consumer
     // warp w of tile t = blockIdx.y * gridDim.x + blockIdx.x: entries

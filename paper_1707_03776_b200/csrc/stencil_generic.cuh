@@ -50,6 +50,8 @@ k_generic3d(SfStepArgs a)
         a.grad[idx] = sf_grad(a.grad[idx], a.gscale, sn, S);
     }
     a.out[idx] = o;
+    if (x >= a.mq[0] && x < a.mq[1]) *sf_mirror(a.out + idx, a.md[0]) = o;      // peer halo (f1)
+    else if (x >= a.mq[2] && x < a.mq[3]) *sf_mirror(a.out + idx, a.md[1]) = o;
     if (MODE == SF_MODE_SAVE) {
         if (a.snap_half) reinterpret_cast<__half *>(a.snap_out)[idx] = __float2half_rn(o);
         else a.snap_out[idx] = o;
@@ -98,6 +100,8 @@ k_generic2d(SfStepArgs a)
         a.grad[idx] = sf_grad(a.grad[idx], a.gscale, sn, S);
     }
     a.out[idx] = o;
+    if (x >= a.mq[0] && x < a.mq[1]) *sf_mirror(a.out + idx, a.md[0]) = o;      // peer halo (f1)
+    else if (x >= a.mq[2] && x < a.mq[3]) *sf_mirror(a.out + idx, a.md[1]) = o;
     if (MODE == SF_MODE_SAVE) {
         if (a.snap_half) reinterpret_cast<__half *>(a.snap_out)[idx] = __float2half_rn(o);
         else a.snap_out[idx] = o;

@@ -580,15 +580,17 @@ def _slab_inputs(p, rank, nranks):
     return x0, nl, m, eta
 
 
-@pytest.mark.parametrize("nranks,variant", [(2, 2), (3, 2), (3, 1)])
-def test_slab_decomposition_bitwise_local_transport(nranks, variant):
+@pytest.mark.parametrize("nranks,variant,p2p", [(2, 2, 0), (3, 2, 0), (3, 1, 0), (2, 2, 1), (3, 2, 1), (3, 1, 1)])
+def test_slab_decomposition_bitwise_local_transport(nranks, variant, p2p):
     """The multi-GPU slab path (local [n0_loc + 2r] buffers, split boundary/interior
     launches with the persistent-kernel SM reservation, per-step halo exchange, owner-only
     injection and records, record all-reduce inside the gradient) run as rank threads on
     ONE device through the in-process transport (same planes as the NCCL exchange): the
     records, the owned planes of both final levels and of the gradient, and J are bitwise
     those of the single-domain run (reading C18).  Sources and receivers straddle the slab
-    boundaries."""
+    boundaries.  p2p = 1: SF_OPT_P2P -- the boundary kernel stores the boundary planes
+    straight into the neighbours' halos and the streams order on counters; the
+    transport then only runs once per call (the initial halo)."""
     S = sf()
     p = synth.random_problem(3, (41, 30, 64), 8, 50, seed=91, nbl=5, nsrc=3, nrec=40)
     h = p.h
@@ -614,7 +616,16 @@ def test_slab_decomposition_bitwise_local_transport(nranks, variant):
                           src_coords=p.src_coords.astype(np.float64),
                           rec_coords=p.rec_coords.astype(np.float64), comm=group, rank=rank, nranks=nranks)
         pr.set_tuning(variant, 0, 0)
+        if p2p:
+            pr.set_option(8, 1)
+        pr.set_profiling(True)
+        pr.profile(reset=True)
         rec, u, _ = pr.forward(dev(p.wavelet))
+        torch.cuda.current_stream().synchronize()
+        other = pr.profile(reset=True)["other_launches"]
+        pr.set_profiling(False)
+        # transport exchanges: one per step, or only the initial one with peer stores
+        assert (other <= 2) if p2p else (other >= p.nt - 1), other
         g, J = pr.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
         torch.cuda.current_stream().synchronize()
         res = (x0, nl, rec.cpu().numpy(), u.cpu().numpy()[:, r:r + nl], g.cpu().numpy()[r:r + nl], J)
