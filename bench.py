@@ -203,6 +203,8 @@ def run_ours(args):
         prop.set_option(2, 1)
     if args.graph:
         prop.set_option(5, 1)
+    if args.p2p and slab:
+        prop.set_option(8, 1)   # peer-store halo exchange instead of NCCL send/recv
     if args.snap_half:
         prop.set_option(7, 1)
     wav = dev(p.wavelet)
@@ -327,6 +329,8 @@ def run_ours(args):
                        "snapshots": ("fp16" if args.snap_half else "fp32") if grad_mode else None,
                        "damping": ("separable profiles (sf_desc.sigma): beta regenerated in-kernel" if sep else
                                    "eta array (hoisted beta streamed)" if eta_d is not None else "none"),
+                       "halo_exchange": (("peer stores from the boundary kernel + stream counters"
+                                          if args.p2p else "NCCL send/recv") if slab else None),
                        "schedule": ("split (boundary planes, then interior)" if split else
                                     "single launch per step") + (", CUDA graph replay" if args.graph else ""),
                        "kernel_tuning": tuning},
@@ -457,6 +461,8 @@ def main():
     ap.add_argument("--split", action="store_true",
                     help="1 GPU: run the slab schedule (boundary planes first, interior second) "
                          "to measure its cost without communication")
+    ap.add_argument("--p2p", action="store_true",
+                    help="N > 1 slab runs: peer-store halo exchange (SF_OPT_P2P) instead of NCCL send/recv")
     ap.add_argument("--graph", action="store_true",
                     help="replay each step as a CUDA graph (SF_OPT_GRAPH; for launch-bound grids)")
     ap.add_argument("--snap-half", action="store_true",
