@@ -176,7 +176,7 @@ class Propagator:
     def set_option(self, option: int, value: int):
         """sf_set_option: 1 L2 prefetch distance, 2 split boundary launches, 3 fuse-max points,
         4 SMs left free by the split interior launch, 5 CUDA-graph replay of whole calls,
-        7 fp16 snapshots."""
+        7 fp16 snapshots, 8 peer-store halo exchange in slab mode."""
         check(lib().sf_set_option(self._h, int(option), int(value)))
         if int(option) == 7:
             self.snap_dtype = torch.float16 if value else torch.float32
