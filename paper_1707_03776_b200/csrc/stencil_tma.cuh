@@ -145,7 +145,9 @@ struct Cfg {
     // coefficient ring DC output planes.  Leads are balanced: DU up to R + 5 while the
     // coefficient ring keeps SF_DC_MIN stages, then the rest to the coefficients (up to 4;
     // below SF_DC_MIN only when even DU = R + 2 leaves no more, e.g. r = 8 GRAD + damping)
-    static constexpr int DC_MIN = SF_DC_MIN;
+    // r >= 7: two coefficient stages are enough and the freed stage deepens the u ring's
+    // lead from 1 to 2 planes (configs[3]: -1.1 %, A/B)
+    static constexpr int DC_MIN = R >= 7 ? 2 : SF_DC_MIN;
     static constexpr int DU_WANT = R + 5;
     static constexpr int DU_FIT = (BUDGET - DC_MIN * CST) / UST;
     static constexpr int DU = DU_FIT >= DU_WANT ? DU_WANT : (DU_FIT >= R + 2 ? DU_FIT : R + 2);
