@@ -793,3 +793,34 @@ def test_fp16_snapshots_forward_and_gradient():
     assert rel(out[0], g32.cpu().numpy()) < 2.0 ** -11 * 4
     assert prop.gradient_workspace_bytes(3) < make_prop(p).gradient_workspace_bytes(3)
     prop.close()
+
+
+def test_p2p_option_errors():
+    """SF_OPT_P2P needs a slab handle whose every rank owns more than 2r planes."""
+    S = sf()
+    p = synth.random_problem(3, (20, 16, 32), 8, 10, seed=5, nbl=0, nsrc=1, nrec=2)
+    prop = make_prop(p)
+    with pytest.raises(S.SfError):
+        prop.set_option(8, 1)           # single-domain handle
+    prop.close()
+    group = S.local_group_create(3)
+
+    def rank_fn(rank):
+        x0, nl, m, eta = _slab_inputs(p, rank, 3)
+        pr = S.Propagator(dev(m), None if eta is None else dev(eta), shape=p.shape, h=p.h,
+                          space_order=p.space_order, nt=p.nt, dt=p.dt,
+                          src_coords=p.src_coords.astype(np.float64),
+                          rec_coords=p.rec_coords.astype(np.float64), comm=group, rank=rank, nranks=3)
+        try:
+            pr.set_option(8, 1)        # 20 planes / 3 ranks: 6-7 planes <= 2r = 8
+            return None
+        except S.SfError as e:
+            return e.status
+        finally:
+            pr.close()
+
+    try:
+        outs = _run_ranks(3, rank_fn)
+    finally:
+        S.local_group_destroy(group)
+    assert outs == ["SF_ERR_SHAPE"] * 3, outs
