@@ -824,3 +824,31 @@ def test_p2p_option_errors():
     finally:
         S.local_group_destroy(group)
     assert outs == ["SF_ERR_SHAPE"] * 3, outs
+
+
+def test_nccl_single_rank_transport():
+    """The NCCL plumbing on the box: libnccl resolved at run time (the copy torch loaded),
+    communicator from an ncclUniqueId, the in-stream gradient all-reduce (fp32 + fp64 J)
+    -- on one rank the sum is the identity, bitwise."""
+    import socket
+
+    import torch.distributed as dist
+    S = sf()
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        comm = S.nccl_comm_init(S.nccl_unique_id(), 1, 0)
+        p = synth.random_problem(3, (20, 18, 32), 4, 20, seed=8, nbl=3, nsrc=1, nrec=5)
+        prop = make_prop(p)
+        g = torch.randn(p.shape, device="cuda")
+        g0 = g.clone()
+        g, J = prop.allreduce_gradient(comm, g, 1.25, rank=0)
+        torch.cuda.synchronize()
+        assert torch.equal(g, g0) and J == 1.25
+        prop.close()
+        S.nccl_comm_destroy(comm)
+    finally:
+        dist.destroy_process_group()
