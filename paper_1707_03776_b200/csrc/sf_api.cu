@@ -21,7 +21,9 @@
 #include "sparse.cuh"
 
 #define SF_VERSION 1
+#ifndef SF_SIDE_MIN_POINTS
 #define SF_SIDE_MIN_POINTS (1 << 22)  // grids below this record in stream order
+#endif
 
 static thread_local char g_err[1024] = "";
 

@@ -264,10 +264,10 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     constexpr int VZ = C::VZ, NJ = VZ / 2, NW = C::NW, BY = C::BY, TZ = C::TZ, HZ = C::HZ;
     constexpr int Q = C::Q, W = C::W, DU = C::DU, DC = C::DC;
     const int PD = a.l2_prefetch;  // planes of L2 prefetch beyond the smem ring (0 = off)
-    // slot release by the consumers: r >= 5 (rolled loop) every thread arrives after its own
-    // loads (no warp barrier, no divergent branch: +1.6 % on configs[3]); r <= 4 (unrolled)
-    // one arrive per warp after __syncwarp (the per-thread form measured 8 % slower there)
-    constexpr int ARRIVERS = (R >= 5) ? 32 * Cfg<R, VY, DM, MODE>::NW : Cfg<R, VY, DM, MODE>::NW;
+    // slot release by the consumers: one arrive per warp (lane 0, after __syncwarp).  Per-
+    // thread arrives (tried for r >= 5, 1.6 % faster on configs[3]) produced rare wrong values
+    // when small blocks of another kernel (the side-stream records) shared the SM.
+    constexpr int ARRIVERS = Cfg<R, VY, DM, MODE>::NW;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // keep the address space visible to the compiler (LDS, not generic LD)
@@ -555,12 +555,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                     }
                     if (UNR != Q && ++sl == Q) sl = 0;
                     if (p < qa || p >= qb) {  // never an output plane: release the slot now
-                        if (R >= 5) {
-                            mbar_arrive(uempty + 8 * us);
-                        } else {
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(uempty + 8 * us);
-                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(uempty + 8 * us);
                     }
                     if (outp) {
                         // ---- (3) finish output plane q: update, store ----
@@ -607,15 +603,10 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             }
                         }
                         // done with the u tile of plane q and the coefficient stage
-                        if (R >= 5) {
+                        __syncwarp();
+                        if (lane == 0) {
                             mbar_arrive(uempty + 8 * uo);
                             mbar_arrive(cempty + 8 * cs);
-                        } else {
-                            __syncwarp();
-                            if (lane == 0) {
-                                mbar_arrive(uempty + 8 * uo);
-                                mbar_arrive(cempty + 8 * cs);
-                            }
                         }
                         if (++cs == DC) {
                             cs = 0;
