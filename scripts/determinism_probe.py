@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Determinism probe: a BASELINE config (default configs[4]) at full grid, short record,
-repeated in one process (fresh
-and reused handles, optionally after a configs[3] full-grid forward), every result
-compared bitwise with the first.  Prints which stage diverges (records, J, gradient)."""
+repeated in one process (fresh handles, optionally after a configs[3] full-grid forward),
+every result compared bitwise with the first (or with a generic-kernel run,
+--ref-generic).  Prints which stage diverges and where (records, state, snapshots, J,
+gradient).  Found the r >= 5 slot-release race fixed in round 1."""
 import argparse
 import os
 import sys
