@@ -37,6 +37,8 @@ def main():
     ap.add_argument("--save-every", type=int, default=3)
     ap.add_argument("--noise", action="store_true", help="background matmuls on another stream (staggers CTA starts)")
     ap.add_argument("--no-grad", action="store_true", help="forward only")
+    ap.add_argument("--snap-half", action="store_true", help="fp16 snapshots (SF_OPT_SNAP_HALF)")
+    ap.add_argument("--sep", action="store_true", help="separable damping profiles instead of the eta array")
     args = ap.parse_args()
     if args.pre_c3:
         p3 = synth.make_config(3, nt=6)
@@ -55,9 +57,11 @@ def main():
     ref = None
     bad = 0
     if args.ref_generic:
-        prop = sf.Propagator(dev(p.m), None if p.damp is None else dev(p.damp), shape=p.shape, h=p.h, space_order=p.space_order, nt=p.nt,
+        prop = sf.Propagator(dev(p.m), None if (p.damp is None or args.sep) else dev(p.damp), sigma=p.sigma if args.sep else None, shape=p.shape, h=p.h, space_order=p.space_order, nt=p.nt,
                              dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords)
         prop.set_tuning(1, 0, 0)
+        if args.snap_half:
+            prop.set_option(7, 1)
         rec, u, snaps = prop.forward(dev(p.wavelet), save_every=se)
         if args.no_grad:
             g, J = torch.zeros(1, device="cuda"), 0.0
@@ -69,9 +73,11 @@ def main():
         prop.close()
         print("generic reference: J", J, flush=True)
     for i in range(args.reps):
-        prop = sf.Propagator(dev(p.m), None if p.damp is None else dev(p.damp), shape=p.shape, h=p.h, space_order=p.space_order, nt=p.nt,
+        prop = sf.Propagator(dev(p.m), None if (p.damp is None or args.sep) else dev(p.damp), sigma=p.sigma if args.sep else None, shape=p.shape, h=p.h, space_order=p.space_order, nt=p.nt,
                              dt=p.dt, src_coords=p.src_coords, rec_coords=p.rec_coords)
         prop.set_tuning(args.variant, args.vy, args.ctas)
+        if args.snap_half:
+            prop.set_option(7, 1)
         if args.prefetch >= 0:
             prop.set_option(1, args.prefetch)
         if args.fuse_max >= 0:
