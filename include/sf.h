@@ -175,7 +175,8 @@ SF_API sf_status sf_get_profile_detail(sf_handle *h, double *ms_by_kind, long lo
  * values. */
 SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
 /* Options (sf_set_option): */
-#define SF_OPT_L2_PREFETCH 1   /* TMA kernel: L2 prefetch distance in planes (default 8, 0 = off)   */
+#define SF_OPT_L2_PREFETCH 1   /* TMA kernel: L2 prefetch distance in planes (default 0 = off; 8 was
+                                  measured 8 % slower on configs[1] with the final kernel)         */
 #define SF_OPT_SPLIT 2         /* 1: boundary planes first, then interior (always on in slab mode;
                                   on one GPU it only reorders work: results are bitwise identical) */
 #define SF_OPT_FUSE_MAX 3      /* largest point set injected / interpolated inside the stencil

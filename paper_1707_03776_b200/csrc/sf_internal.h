@@ -92,7 +92,7 @@ struct sf_handle {
     double *dJ = nullptr;
     // tuning
     int variant = SF_VAR_AUTO, vy = 0, ctas = 0;
-    int l2_prefetch = 8;            // TMA L2 prefetch distance (planes); env SF_L2_PREFETCH
+    int l2_prefetch = 0;            // TMA L2 prefetch distance (planes, 0 = off); env SF_L2_PREFETCH
     // slab decomposition
     int rank = 0, nranks = 1;
     void *comm = nullptr;
