@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--ctas", default="0")
     ap.add_argument("--grad", action="store_true", help="time the adjoint with fused gradient")
     ap.add_argument("--sep", action="store_true", help="separable damping profiles (16 B/pt)")
-    ap.add_argument("--prefetch", default="8", help="comma list of L2 prefetch distances (planes)")
+    ap.add_argument("--prefetch", default="0", help="comma list of L2 prefetch distances (planes)")
     ap.add_argument("--random-init", action="store_true",
                     help="start from a random (incompressible) wavefield instead of zeros")
     args = ap.parse_args()
