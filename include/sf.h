@@ -208,6 +208,12 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   NCCL; the state buffer `u`/`v` must come from cudaMalloc, e.g.
                                   torch's caching allocator).  Every rank must own > 2r planes
                                   (SF_ERR_SHAPE).  Bitwise equal to the NCCL exchange. (default 0) */
+#define SF_OPT_ZSPLIT 9        /* 3D TMA kernel, space order >= 10: 1 (default) runs a z remainder
+                                  of n2 = 128 k + rem, 0 < rem <= 64, as a second launch of narrow
+                                  56 x 32 tiles (the 128-column tiles there would be mostly idle
+                                  lanes); sources are then injected by the standalone kernel.
+                                  Bitwise the same.  (Lower orders run at the HBM roofline, where
+                                  the extra launch costs more than the idle lanes.)             */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */

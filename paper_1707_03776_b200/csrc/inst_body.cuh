@@ -13,11 +13,11 @@
 
 namespace {
 
-template <int VY, int DM, int MODE>
+template <int VY, int DM, int MODE, int LZ>
 cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    using C = sftma::Cfg<SF_R, VY, DM, MODE>;
-    auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE>;
+    using C = sftma::Cfg<SF_R, VY, DM, MODE, LZ>;
+    auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE, LZ>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -28,7 +28,7 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
     // one), items dealt round-robin.  The chunk count minimises rounds x (chunk + 2r): each
     // item re-reads 2r warm-up planes of u^n.  L.ctas overrides the CTA count.
     const int64_t PT = (a.xb - a.xa) + (a.xb2 - a.xa2);
-    const int64_t tiles = ((a.n2 + C::TZ - 1) / C::TZ) * ((a.n1 + C::BY - 1) / C::BY);
+    const int64_t tiles = ((a.n2t - a.zbase + C::TZ - 1) / C::TZ) * ((a.n1 + C::BY - 1) / C::BY);
     if (PT <= 0 || tiles <= 0) return cudaSuccess;
     const int64_t slots = L.ctas > 0 ? L.ctas : L.sms;
     double best = 1e300;
@@ -66,22 +66,22 @@ cudaError_t launch_generic(const SfLaunch &L, const SfStepArgs &a, cudaStream_t 
     return cudaGetLastError();
 }
 
-template <int VY, int DM>
+template <int VY, int DM, int LZ>
 cudaError_t launch_tma_dm(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     switch (L.mode) {
-    case SF_MODE_PLAIN: return launch_tma<VY, DM, SF_MODE_PLAIN>(L, a, st);
-    case SF_MODE_SAVE: return launch_tma<VY, DM, SF_MODE_SAVE>(L, a, st);
-    default: return launch_tma<VY, DM, SF_MODE_GRAD>(L, a, st);
+    case SF_MODE_PLAIN: return launch_tma<VY, DM, SF_MODE_PLAIN, LZ>(L, a, st);
+    case SF_MODE_SAVE: return launch_tma<VY, DM, SF_MODE_SAVE, LZ>(L, a, st);
+    default: return launch_tma<VY, DM, SF_MODE_GRAD, LZ>(L, a, st);
     }
 }
 
-template <int VY>
+template <int VY, int LZ>
 cudaError_t launch_tma_vy(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    if (L.damp == SF_DAMP_ARRAY) return launch_tma_dm<VY, SF_DAMP_ARRAY>(L, a, st);
-    if (L.damp == SF_DAMP_SEP) return launch_tma_dm<VY, SF_DAMP_SEP>(L, a, st);
-    return launch_tma_dm<VY, SF_DAMP_NONE>(L, a, st);
+    if (L.damp == SF_DAMP_ARRAY) return launch_tma_dm<VY, SF_DAMP_ARRAY, LZ>(L, a, st);
+    if (L.damp == SF_DAMP_SEP) return launch_tma_dm<VY, SF_DAMP_SEP, LZ>(L, a, st);
+    return launch_tma_dm<VY, SF_DAMP_NONE, LZ>(L, a, st);
 }
 
 template <int VY, int DM, int MODE>
@@ -103,13 +103,14 @@ int smem_vy(int damp, int mode)
 
 }  // namespace
 
-// Tile shapes (stencil_tma.cuh Geo): vy = 2 -> two rows per thread (14-row tiles; 128
-// columns for r <= 4, 64 for r >= 5); vy = 1 -> one row per thread, 7 x 128 tiles.
+// Tile shapes (stencil_tma.cuh Geo): vy = 2 -> two rows per thread, 14 x 128 tiles; vy = 1
+// -> one row per thread, 7 x 128 tiles; narrow (lz = 8, the z remainder): 56 x 32 tiles.
 cudaError_t SF_CAT(sf_launch_step_r, SF_R)(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     if (L.variant == SF_VAR_TMA) {
-        if (L.vy == 1) return launch_tma_vy<1>(L, a, st);
-        return launch_tma_vy<2>(L, a, st);
+        if (L.lz == 8) return launch_tma_vy<2, 8>(L, a, st);
+        if (L.vy == 1) return launch_tma_vy<1, 32>(L, a, st);
+        return launch_tma_vy<2, 32>(L, a, st);
     }
     switch (L.mode) {
     case SF_MODE_PLAIN: return launch_generic<SF_MODE_PLAIN>(L, a, st);

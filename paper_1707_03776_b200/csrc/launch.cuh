@@ -20,6 +20,7 @@ struct SfLaunch {
     int damp;         // SfDampMode: none, beta array, separable profiles
     int mode;         // SfMode
     int snap_slot;    // GRAD: snapshot slot for the 4D snapshot tensor map
+    int lz;           // TMA lane layout: 32 (128-column tiles) or 8 (narrow 32-column tiles)
     const SfTmaMaps *maps;
 };
 

@@ -202,6 +202,8 @@ static const int TILE_NW = 7;
 static int tile_vz(const sf_handle *, int) { return 4; }
 static int tile_tz(const sf_handle *h, int vy) { return 32 * tile_vz(h, vy); }
 static int tile_by(int vy) { return TILE_NW * vy; }
+// narrow tiles of the z remainder (Geo<R, 2, 8>): 8 lanes x 4 z, 4 lane rows x 2 rows x 7 warps
+static const int NARROW_TZ = 32, NARROW_BY = 56;
 
 // persistent CTAs of the TMA kernel (0 = one per SM)
 static int resolve_ctas(const sf_handle *h) { return h->ctas > 0 ? h->ctas : h->sms; }
@@ -409,6 +411,8 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     a.xb = b.xa < b.xb ? b.xb : h->xb;
     a.xa2 = b.xa2;
     a.xb2 = b.xb2;
+    a.zbase = 0;
+    a.n2t = a.n2;
     a.w = h->w;
     a.l2_prefetch = h->l2_prefetch;
 
@@ -431,30 +435,49 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     a.hdt = (float)(0.5 * h->dt);
     L.mode = mode;
     L.snap_slot = b.snap_slot;
-    SfTmaMaps maps;
-    memset(&maps, 0, sizeof maps);
-    if (L.variant == SF_VAR_TMA) {
+    L.lz = 32;
+    // z remainder (SF_OPT_ZSPLIT): n2 = 128 k + rem with 0 < rem <= 64 -> the 128-column tiles
+    // cover [0, 128 k) and a second launch of narrow 56 x 32 tiles covers the rem columns
+    // (the 128-column tiles there would be mostly idle lanes; configs[4]: 400 = 3 x 128 + 16).
+    // Only for r >= 5, where the kernel is latency-bound and idle lanes cost time (400^3 so12:
+    // 256 vs 296 us); at r <= 4 it runs at the HBM roofline and the extra launch costs
+    // (400^3 so8: 233 vs 225 us).
+    int64_t zrem = 0;
+    if (L.variant == SF_VAR_TMA && h->ndim == 3 && h->zsplit && L.vy == 2 && h->r >= 5) {
+        const int64_t rem = a.n2 % tile_tz(h, 2);
+        if (rem > 0 && rem <= 64 && a.n2 > tile_tz(h, 2)) zrem = rem;
+    }
+    auto build_maps = [&](SfTmaMaps &m, int TZ, int BY) -> sf_status {
+        memset(&m, 0, sizeof m);
         const int HZ = ((h->r + 3) / 4) * 4;
-        const int TZ = tile_tz(h, L.vy), BY = tile_by(L.vy);
         const int64_t d3[3] = {h->nb[2], h->nb[1], h->nb[0]};
         const uint32_t bcur[3] = {(uint32_t)(TZ + 2 * HZ), (uint32_t)(BY + 2 * h->r), 1};
         const uint32_t bpl[3] = {(uint32_t)TZ, (uint32_t)BY, 1};
         sf_status s;
-        if ((s = make_map(&maps.cur, b.cur, 3, d3, bcur))) return s;
-        if ((s = make_map(&maps.old, b.out, 3, d3, bpl))) return s;
-        if ((s = make_map(&maps.c3, h->c3, 3, d3, bpl))) return s;
-        if (h->beta && (s = make_map(&maps.beta, h->beta, 3, d3, bpl))) return s;
+        if ((s = make_map(&m.cur, b.cur, 3, d3, bcur))) return s;
+        if ((s = make_map(&m.old, b.out, 3, d3, bpl))) return s;
+        if ((s = make_map(&m.c3, h->c3, 3, d3, bpl))) return s;
+        if (h->beta && (s = make_map(&m.beta, h->beta, 3, d3, bpl))) return s;
         if (mode == SF_MODE_GRAD) {
             const int64_t d4[4] = {h->nb[2], h->nb[1], h->nb[0], b.nsnap};
             const uint32_t b4[4] = {(uint32_t)TZ, (uint32_t)BY, 1, 1};
-            if ((s = make_map(&maps.snap, b.snaps, 4, d4, b4, h->snap_half))) return s;
-            if ((s = make_map(&maps.grad, b.grad, 3, d3, bpl))) return s;
+            if ((s = make_map(&m.snap, b.snaps, 4, d4, b4, h->snap_half))) return s;
+            if ((s = make_map(&m.grad, b.grad, 3, d3, bpl))) return s;
         }
+        return SF_OK;
+    };
+    SfTmaMaps maps, nmaps;
+    memset(&maps, 0, sizeof maps);
+    if (L.variant == SF_VAR_TMA) {
+        sf_status s;
+        if ((s = build_maps(maps, tile_tz(h, L.vy), tile_by(L.vy)))) return s;
+        if (zrem && (s = build_maps(nmaps, NARROW_TZ, NARROW_BY))) return s;
     }
     L.maps = &maps;
     // fuse only small point sets (a few shots' sources): large sets (receiver grids) would
-    // put dependent table loads on the stencil's critical path -> standalone kernels
-    if (L.variant == SF_VAR_TMA && mode != SF_MODE_GRAD && b.inj && b.inj->ntgt > 0 &&
+    // put dependent table loads on the stencil's critical path -> standalone kernels.  Not
+    // with the z split (the fused lists index the 128-column tiles only)
+    if (L.variant == SF_VAR_TMA && !zrem && mode != SF_MODE_GRAD && b.inj && b.inj->ntgt > 0 &&
         b.inj->ntgt <= h->fuse_max && b.inj_vals) {
         sf_status s = ensure_inj_tiles(h, *b.inj, L.vy);
         if (s) return s;
@@ -473,8 +496,20 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
 
     cudaError_t e;
     {
-        ProfScope ps(h, PK_STENCIL, st);
+        ProfScope ps(h, PK_STENCIL, st);  // one scope over both launches of a z split
+        if (zrem) a.n2t = a.n2 - zrem;
         e = launch_step_r(h->r, L, a, st);
+        if (e == cudaSuccess && zrem) {
+            SfLaunch Ln = L;
+            Ln.lz = 8;
+            Ln.maps = &nmaps;
+            SfStepArgs an = a;
+            an.zbase = a.n2 - zrem;
+            an.n2t = a.n2;
+            h->n_all++;
+            h->n_kind[PK_OTHER]++;  // counted; its time is inside the stencil scope
+            e = launch_step_r(h->r, Ln, an, st);
+        }
     }
     if (e != cudaSuccess) return sf_set_error(SF_ERR_CUDA, "stencil launch: %s", cudaGetErrorString(e));
     return SF_OK;
@@ -1028,6 +1063,10 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
             }
         }
         h->p2p = value != 0;
+        return SF_OK;
+    case SF_OPT_ZSPLIT:
+        h->zsplit = value != 0;
+        drop_graphs(h);
         return SF_OK;
     case SF_OPT_SNAP_HALF:
         h->snap_half = value != 0;

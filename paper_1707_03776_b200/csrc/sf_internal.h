@@ -124,6 +124,7 @@ struct sf_handle {
     // peer-store halo exchange (SF_OPT_P2P): the boundary-plane kernel stores the
     // owned boundary planes straight into the neighbours' halos (peer-mapped pointers) and
     // signals with a stream-ordered counter write; the neighbour's stream waits on the value
+    bool zsplit = true;               // SF_OPT_ZSPLIT: narrow tiles for a z remainder <= 64
     bool p2p = false;
     uint32_t *p2p_flags = nullptr;    // own device counters: [0] written by the left, [1] by the right neighbour
     uint32_t p2p_seq = 0;             // P2P steps completed (the value the next step writes is seq + 1)

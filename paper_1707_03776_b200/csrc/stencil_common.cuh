@@ -154,6 +154,7 @@ struct SfStepArgs {
     int64_t n0b, n1, n2;   // buffer extents (n0b includes slab halo planes)
     int64_t xa, xb;        // planes [xa, xb) of the buffer to compute
     int64_t xa2, xb2;      // optional second range [xa2, xb2) in the same launch (xa2 == xb2: none)
+    int64_t zbase, n2t;    // TMA kernel: its tiles cover the columns [zbase, n2t) (0, n2: all)
     SfWeights w;
     // Peer-store halo exchange (SF_OPT_P2P): an output plane q in [mq[0], mq[1])
     // is also stored at byte offset md[0] from its own address (the left neighbour's right

@@ -131,19 +131,25 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
 // 7 consumer warps + 1 producer = 8 warps = 2 per SM sub-partition, which leaves each
 // thread the full 255 registers (a ninth warp would put 3 warps on one sub-partition and
 // cap every thread at 168 registers).
-template <int R, int VY>
+// Lane layout: LZ lanes along z x (32 / LZ) lane rows along y per warp.  LZ = 32 (default):
+// a warp covers VY rows x 128 columns.  LZ = 8 ("narrow" tiles, 32 columns x 56 rows): the z
+// remainder of grids whose n2 is not a multiple of 128 (configs[4]: 400 = 3 x 128 + 16),
+// where 128-column tiles would be mostly idle lanes.  8 lanes x 16 B = one 128-B shared-
+// memory wavefront per row, so the lane rows never share a bank phase (conflict-free).
+template <int R, int VY, int LZ = 32>
 struct Geo {
     static constexpr int VZ = 4;
     static constexpr int NW = 7;                        // consumer warps
-    static constexpr int BY = NW * VY;                  // rows per tile
-    static constexpr int TZ = 32 * VZ;                  // columns per tile
+    static constexpr int LY = 32 / LZ;                  // lane rows per warp
+    static constexpr int BY = NW * LY * VY;             // rows per tile
+    static constexpr int TZ = LZ * VZ;                  // columns per tile
     static constexpr int HZ = ((R + 3) / 4) * 4;        // z halo rounded up to 16 B
 };
 
-template <int R, int VY, int DM, int MODE>
+template <int R, int VY, int DM, int MODE, int LZ = 32>
 struct Cfg {
     static constexpr bool DAMP = (DM == SF_DAMP_ARRAY);  // beta array streamed
-    using G = Geo<R, VY>;
+    using G = Geo<R, VY, LZ>;
     static constexpr int VZ = G::VZ, NW = G::NW, BY = G::BY, TZ = G::TZ, HZ = G::HZ;
     static constexpr int W = TZ + 2 * HZ;               // smem row pitch of the u tile
     static constexpr int H = BY + 2 * R;                // rows of the u tile
@@ -264,14 +270,14 @@ __device__ __forceinline__ Seg next_seg(int64_t w, int64_t end, int64_t P1, int6
     return s;
 }
 
-template <int R, int VY, int DM, int MODE>
-__global__ void __launch_bounds__(Cfg<R, VY, DM, MODE>::THREADS, 1)
+template <int R, int VY, int DM, int MODE, int LZ = 32>
+__global__ void __launch_bounds__(Cfg<R, VY, DM, MODE, LZ>::THREADS, 1)
 k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_old,
         const __grid_constant__ CUtensorMap tm_c3, const __grid_constant__ CUtensorMap tm_beta,
         const __grid_constant__ CUtensorMap tm_snap, const __grid_constant__ CUtensorMap tm_grad,
         const SfStepArgs a, const int snap_slot, const int chunk, const int nchunk)
 {
-    using C = Cfg<R, VY, DM, MODE>;
+    using C = Cfg<R, VY, DM, MODE, LZ>;
     constexpr bool DAMP = C::DAMP;
     constexpr int VZ = C::VZ, NJ = VZ / 2, NW = C::NW, BY = C::BY, TZ = C::TZ, HZ = C::HZ;
     constexpr int Q = C::Q, W = C::W, DU = C::DU, DC = C::DC;
@@ -279,7 +285,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     // slot release by the consumers: one arrive per warp (lane 0, after __syncwarp).  Per-
     // thread arrives (tried for r >= 5, 1.6 % faster on configs[3]) produced rare wrong values
     // when small blocks of another kernel (the side-stream records) shared the SM.
-    constexpr int ARRIVERS = Cfg<R, VY, DM, MODE>::NW;
+    constexpr int ARRIVERS = C::NW;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // keep the address space visible to the compiler (LDS, not generic LD)
@@ -291,7 +297,9 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 
     const int lane = threadIdx.x, wy = threadIdx.y;
     const int64_t P1 = a.xb - a.xa, PT = P1 + (a.xb2 - a.xa2);
-    const int ntz = (int)((a.n2 + TZ - 1) / TZ);
+    // tiles cover the columns [zbase, n2t) (a split launch: the 128-column tiles, then the
+    // narrow remainder tiles); neighbours beyond that range are still read (real halo)
+    const int ntz = (int)((a.n2t - a.zbase + TZ - 1) / TZ);
     const int tiles = ntz * (int)((a.n1 + BY - 1) / BY);
     const int items = tiles * nchunk;
     if ((int)blockIdx.x >= items) return;  // uniform over the CTA
@@ -328,7 +336,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                          w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
                 const Seg sg = next_seg(w, w1, P1, PT, a);
                 w += sg.qb - sg.qa;
-                const int z0 = (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
+                const int z0 = (int)a.zbase + (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
                 const int NP = (int)(sg.qb - sg.qa) + 2 * R;
                 for (int i = 0; i < NP; ++i) {
                     const int p = (int)(sg.qa - R) + i;   // plane of u^n
@@ -385,12 +393,15 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     // ---------------------------------------------------- consumer warps
     f2_t V[Q][VY][NJ];  // own u at planes (fp32 pairs), slot = iteration index mod Q
     static_assert(Q <= 17, "slot switch covers r <= 8");
-    const int rown = R + VY * wy;       // first own row in the u tile
+    constexpr int LY = C::G::LY;
+    const int lz = lane % LZ, ly = lane / LZ;        // lane position in the warp's block
+    const int rr = VY * (wy * LY + ly);              // first own row in the tile
+    const int rown = R + rr;                         // first own row in the u tile
     const float *ubase = reinterpret_cast<const float *>(smem);
     const float *cbase = reinterpret_cast<const float *>(cring);
     constexpr int UF = C::UST / 4, CF = C::CST / 4, PF = C::PL / 4;  // strides in floats
-    const int own_off = rown * W + HZ + VZ * lane;      // own values in a u tile
-    const int po = VY * wy * TZ + VZ * lane;            // own values (row 0) in a plane
+    const int own_off = rown * W + HZ + VZ * lz;        // own values in a u tile
+    const int po = rr * TZ + VZ * lz;                   // own values (row 0) in a plane
     int us = 0, uo = DU - R, cs = 0;                    // uo: u slot of plane q = p - R
     uint32_t uph = 0, cph = 0;
     const int n2 = (int)a.n2;
@@ -410,9 +421,9 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                  w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
         const Seg sg = next_seg(w, w1, P1, PT, a);
         w += sg.qb - sg.qa;
-        const int z0 = (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
-        const int zg = z0 + VZ * lane;
-        const int yg = y0 + VY * wy;
+        const int z0 = (int)a.zbase + (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
+        const int zg = z0 + VZ * lz;
+        const int yg = y0 + rr;
         const bool zact = zg < a.n2;
         // separable damping: profiles of the own rows / columns (clamped reads at ragged edges)
         float SY[VY];

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--nt", type=int, default=40)
     ap.add_argument("--damp", action="store_true")
     ap.add_argument("--vy", type=int, default=2)
+    ap.add_argument("--zsplit", type=int, default=1, help="SF_OPT_ZSPLIT (narrow tiles for a z remainder)")
     ap.add_argument("--variant", type=int, default=2, help="1 generic, 2 TMA")
     ap.add_argument("--ctas", default="0", help="comma list of persistent CTA counts (0 = auto)")
     ap.add_argument("--shapes", default="336x336x336,336x336x384,336x336x320,336x336x256,336x392x336")
@@ -31,6 +32,7 @@ def main():
         eta = torch.full(shape, 0.01, device="cuda") if args.damp else None
         prop = sf.Propagator(m, eta, shape=shape, h=10.0, space_order=args.so, nt=args.nt, dt=1.0,
                              src_coords=None, rec_coords=None)
+        prop.set_option(9, args.zsplit)
         N = int(np.prod(shape))
         g = torch.Generator(device="cuda").manual_seed(0)
         u0 = torch.randn((2,) + shape, device="cuda", generator=g) * 1e-3

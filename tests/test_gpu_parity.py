@@ -875,3 +875,45 @@ def test_tma_bitwise_with_concurrent_records():
     for o in outs[1:]:
         for a, b in zip(o, outs[0]):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("shape,so", [((34, 30, 144), 10), ((30, 60, 144), 12), ((26, 22, 192), 16),
+                                      ((22, 58, 296), 14)])
+def test_z_remainder_narrow_tiles_bitwise(shape, so):
+    """SF_OPT_ZSPLIT (space order >= 10): n2 = 128 k + rem (rem 16 / 16 / 64 / 40) -> 128-column tiles over the
+    first 128 k columns, then narrow 56 x 32 tiles over the rest.  Forward (records, state,
+    snapshots) and gradient are bitwise equal to the unsplit launch and within 1e-4 of the
+    oracle; a source and receivers sit in the remainder columns, rows span several narrow
+    tiles (ragged last tile)."""
+    p = synth.random_problem(3, shape, so, 60, seed=31, nbl=5, nsrc=2, nrec=12)
+    n2 = shape[2]
+    p.src_coords[1, 2] = (n2 - 8.3) * p.h
+    p.rec_coords[0, 2] = (n2 - 7.4) * p.h
+    p.rec_coords[1, 2] = (n2 - 9.0) * p.h
+    rng = np.random.default_rng(5)
+    m_true = (p.m * rng.uniform(0.9, 1.1, p.m.shape)).astype(np.float32)
+    d_obs = oracle.forward(p, m=m_true)["rec"].astype(np.float32)
+    ro, uo, sno = oracle_forward(p, save_every=4)
+    go = oracle.gradient(p, d_obs, save_every=4)
+    outs = []
+    for z in (1, 0):
+        prop = make_prop(p)
+        prop.set_option(9, z)
+        assert prop.tuning()["variant"] == 2
+        prop.set_profiling(True)
+        prop.profile(reset=True)
+        rec, u, snaps = prop.forward(dev(p.wavelet), save_every=4)
+        torch.cuda.synchronize()
+        launches = prop.profile(reset=True)["other_launches"]
+        prop.set_profiling(False)
+        g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=4)
+        torch.cuda.synchronize()
+        outs.append((rec.cpu().numpy(), u.cpu().numpy(), snaps.cpu().numpy(), g.cpu().numpy(), J, launches))
+        prop.close()
+    on, off = outs
+    for a, b in zip(on[:4], off[:4]):
+        assert np.array_equal(a, b)
+    assert on[4] == off[4]
+    assert on[5] >= off[5] + (p.nt - 1)  # one narrow launch per step
+    assert rel(on[0], ro) <= TOL and rel(on[1], uo) <= TOL and rel(on[2], sno) <= TOL
+    assert rel(on[3], go["grad"]) <= TOL, rel(on[3], go["grad"])
