@@ -2,7 +2,8 @@
 // persistent (one CTA per SM, each walking (tile, x-chunk) items).
 //
 // Hot kernel of the path (memory-bandwidth bound).  A tile
-// is BY = 7 VY rows (y) x TZ = 32 VZ columns (z); a CTA walks its (tile, x-chunk) items --
+// is BY = 7 VY (32 / LZ) rows (y) x TZ = LZ VZ columns (z) -- LZ = 32: 14 x 128 tiles; LZ = 8:
+// 56 x 32 "narrow" tiles for a z remainder (SF_OPT_ZSPLIT); a CTA walks its (tile, x-chunk) items --
 // each a run of planes of one tile column streamed along x (the outermost, slab axis) --
 // keeping its TMA pipeline running across items.  Per plane p of a segment:
 //   * the producer warp's elected lane issues TMA (cp.async.bulk.tensor) loads:
@@ -11,8 +12,9 @@
 //       - old / c3 / beta (+ snapshot / gradient in GRAD mode) of output plane q = p - R
 //         into a DC-deep coefficient ring (with separable damping, DM = SF_DAMP_SEP, beta
 //         is regenerated from three 1D profiles instead: 16 B/pt instead of 20);
-//     completion via mbarrier transaction counts (full), slot reuse via consumer arrivals
-//     (empty; per warp for r <= 4, per thread for r >= 5);
+//     completion via mbarrier transaction counts (full), slot reuse via one consumer
+//     arrive per warp (empty), each preceded by a generic -> async proxy fence (the slot's
+//     LDS reads vs the TMA refill: write-after-read across proxies);
 //   * each consumer warp (VY rows, VZ consecutive z per lane) pushes its own u values of
 //     plane p into a register queue of depth 2R+1 (compile-time rotated by unrolling the
 //     plane loop by 2R+1: no register moves), then finishes output plane q = p - R:
