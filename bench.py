@@ -401,11 +401,15 @@ def cpu_baseline(p, seconds):
     import oracle
     oracle.build()
     N = int(np.prod(p.shape))
-    probe = 3
-    t0 = time.perf_counter()
-    oracle.forward(p, nt=probe, wavelet=p.wavelet[:probe])
-    tp = time.perf_counter() - t0
-    k = int(max(probe, min(p.nt, (probe - 1) * seconds / max(tp, 1e-3) + 1)))
+    # per-update time from two short runs (their difference cancels the fixed setup cost:
+    # tables, first touch of the fp64 arrays)
+    tps = []
+    for probe in (2, 4):
+        t0 = time.perf_counter()
+        oracle.forward(p, nt=probe, wavelet=p.wavelet[:probe])
+        tps.append(time.perf_counter() - t0)
+    per_update = max((tps[1] - tps[0]) / 2.0, 1e-4)
+    k = int(max(4, min(p.nt, seconds / per_update + 1)))
     t0 = time.perf_counter()
     oracle.forward(p, nt=k, wavelet=p.wavelet[:k])
     t = time.perf_counter() - t0
