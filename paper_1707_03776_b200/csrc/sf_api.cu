@@ -520,7 +520,10 @@ static sf_status launch_interp(sf_handle *h, const SfSparse &sp, const float *u,
 {
     if (sp.np == 0 || !out) return SF_OK;
     ProfScope ps(h, PK_INTERP, st);
-    k_interp_ell<<<(sp.np + 127) / 128, 128, 0, st>>>(u, sp.e_idx, sp.e_w, sp.i_owned, sp.np, sp.ik, out);
+    // grid-stride over at most one block per SM: the record kernel runs beside the persistent
+    // stencil (side stream), where fewer, longer-lived blocks disturb it less
+    const int nb = std::min((sp.np + 127) / 128, h->sms);
+    k_interp_ell<<<nb, 128, 0, st>>>(u, sp.e_idx, sp.e_w, sp.i_owned, sp.np, sp.ik, out);
     SF_CUDA_TRY(cudaGetLastError());
     return SF_OK;
 }

@@ -49,14 +49,14 @@ __global__ void k_interp_ell(const float *__restrict__ u, const int64_t *__restr
                              const float *__restrict__ W, const int *__restrict__ owned, int np, int K,
                              float *__restrict__ out)
 {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= np) return;
-    float acc = 0.0f;
-    for (int c = 0; c < K; ++c) {
-        const float w = W[(int64_t)c * np + p];
-        if (w != 0.0f) acc = __fmaf_rn(w, __ldcg(u + idx[(int64_t)c * np + p]), acc);
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        for (int c = 0; c < K; ++c) {
+            const float w = W[(int64_t)c * np + p];
+            if (w != 0.0f) acc = __fmaf_rn(w, __ldcg(u + idx[(int64_t)c * np + p]), acc);
+        }
+        out[p] = owned ? (owned[p] ? acc : 0.0f) : acc;
     }
-    out[p] = owned ? (owned[p] ? acc : 0.0f) : acc;
 }
 
 // Injection from ELL tables ([K][ntgt] slot-major, zero coefficients pad): bitwise equal
