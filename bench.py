@@ -479,6 +479,11 @@ def main():
     ap.add_argument("--ref-steps-nt", type=int, default=6,
                     help="--impl reference: time samples per timed step of the oracle")
     args = ap.parse_args()
+    if args.p2p:
+        # the counter waits of the peer-store exchange are blocking stream operations: give
+        # every stream its own hardware queue so no wait can stall an unrelated stream
+        # (must be set before the CUDA context exists)
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     if args.impl == "reference":
         res = run_reference(args)
     else:

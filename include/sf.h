@@ -207,7 +207,11 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   share pointers, NCCL ranks CUDA IPC handles (all-gathered over
                                   NCCL; the state buffer `u`/`v` must come from cudaMalloc, e.g.
                                   torch's caching allocator).  Every rank must own > 2r planes
-                                  (SF_ERR_SHAPE).  Bitwise equal to the NCCL exchange. (default 0) */
+                                  (SF_ERR_SHAPE).  Bitwise equal to the NCCL exchange.  Across
+                                  processes the counter waits are blocking stream operations:
+                                  run with CUDA_DEVICE_MAX_CONNECTIONS >= 16 so none can stall an
+                                  unrelated stream sharing its hardware queue; in-process rank
+                                  threads (local group) order with events instead. (default 0) */
 #define SF_OPT_ZSPLIT 9        /* 3D TMA kernel, space order >= 10: 1 (default) runs a z remainder
                                   of n2 = 128 k + rem, 0 < rem <= 64, as a second launch of narrow
                                   56 x 32 tiles (the 128-column tiles there would be mostly idle

@@ -128,6 +128,7 @@ struct LocalGroup {
     std::vector<cudaEvent_t> ev, done;
     std::vector<void *> ptr;
     std::vector<void *> p2p;  // [rank][3]: state buffers A, B and the P2P counters
+    std::vector<cudaEvent_t> bnd;  // [rank]: the rank's boundary-done event (SF_OPT_P2P)
     void barrier()
     {
         std::unique_lock<std::mutex> lk(mu);
@@ -196,6 +197,7 @@ extern "C" sf_status sf_local_group_create(int nranks, void **group_out)
     G->done.resize(nranks);
     G->ptr.assign(nranks, nullptr);
     G->p2p.assign(3 * (size_t)nranks, nullptr);
+    G->bnd.assign(nranks, nullptr);
     for (int q = 0; q < nranks; ++q) {
         SF_CUDA_TRY(cudaEventCreateWithFlags(&G->ev[q], cudaEventDisableTiming));
         SF_CUDA_TRY(cudaEventCreateWithFlags(&G->done[q], cudaEventDisableTiming));
@@ -354,6 +356,7 @@ sf_status sf_comm_p2p_setup(sf_handle *h, float *A, float *B, cudaStream_t st)
     void *theirs[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
     if (LocalGroup *G = as_local(h->comm)) {
         for (int k = 0; k < 3; ++k) G->p2p[3 * (size_t)h->rank + k] = mine[k];
+        G->bnd[h->rank] = h->ev_bnd;
         SF_CUDA_TRY(cudaEventRecord(G->ev[h->rank], st));
         G->barrier();
         for (int side = 0; side < 2; ++side) {
@@ -425,4 +428,23 @@ void sf_comm_p2p_release(sf_handle *h)
 {
     for (auto &e : h->ipc_open) cudaIpcCloseMemHandle(e.second);
     h->ipc_open.clear();
+}
+
+// SF_OPT_P2P step ordering inside one process (local group): the rank threads share one
+// device context, where a counter wait (cuStreamWaitValue32) enqueued ahead of the
+// neighbour's counter write can block that write through a shared hardware queue (seen
+// as a hang with 3 ranks x 5 streams > CUDA_DEVICE_MAX_CONNECTIONS = 8).  Events cannot:
+// each rank records its boundary-done event, a host barrier makes every record precede
+// the neighbours' waits, and a second barrier keeps the next step's record after them.
+bool sf_comm_p2p_local(sf_handle *h) { return as_local(h->comm) != nullptr; }
+
+sf_status sf_comm_p2p_local_step(sf_handle *h, cudaStream_t st, bool left, bool right)
+{
+    LocalGroup *G = as_local(h->comm);
+    if (!G) return sf_set_error(SF_ERR_INVALID_ARG, "not a local group");
+    G->barrier();
+    if (left) SF_CUDA_TRY(cudaStreamWaitEvent(st, G->bnd[h->rank - 1], 0));
+    if (right) SF_CUDA_TRY(cudaStreamWaitEvent(st, G->bnd[h->rank + 1], 0));
+    G->barrier();
+    return SF_OK;
 }

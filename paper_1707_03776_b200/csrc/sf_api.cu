@@ -1268,7 +1268,8 @@ static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepB
         SF_CUDA_TRY(cudaStreamWaitEvent(h->hi_stream, h->ev_itp[b.itp_cur & 1], 0));
     SF_CUDA_TRY(cudaEventRecord(h->ev_bnd, h->hi_stream));
     const uint32_t seq = h->p2p_seq + 1;
-    for (int side = 0; side < 2; ++side)
+    const bool local = sf_comm_p2p_local(h);  // in-process ranks: events, not counters
+    for (int side = 0; side < 2 && !local; ++side)
         if (h->p2p_nflag[side] && (s = stream_write32(h->hi_stream, h->p2p_nflag[side], seq))) return s;
     if ((s = launch_step(h, bi, mode, st, &f2, &fi2))) return s;
     // (the interior TMA launch may inject its own planes' targets itself)
@@ -1276,8 +1277,12 @@ static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepB
                                                    snap_patch, grad_snap, b.grad, b.gscale, st)))
         return s;
     SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_bnd, 0));
-    if (plan[5] && (s = stream_wait32(st, h->p2p_flags + 0, seq))) return s;
-    if (plan[6] && (s = stream_wait32(st, h->p2p_flags + 1, seq))) return s;
+    if (local) {
+        if ((s = sf_comm_p2p_local_step(h, st, plan[5] != 0, plan[6] != 0))) return s;
+    } else {
+        if (plan[5] && (s = stream_wait32(st, h->p2p_flags + 0, seq))) return s;
+        if (plan[6] && (s = stream_wait32(st, h->p2p_flags + 1, seq))) return s;
+    }
     h->p2p_seq = seq;
     return SF_OK;
 }

@@ -150,6 +150,8 @@ sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st);
 // (local group: in-process pointers; NCCL: CUDA IPC handles all-gathered over NCCL)
 sf_status sf_comm_p2p_setup(sf_handle *h, float *A, float *B, cudaStream_t st);
 void sf_comm_p2p_release(sf_handle *h);
+bool sf_comm_p2p_local(sf_handle *h);
+sf_status sf_comm_p2p_local_step(sf_handle *h, cudaStream_t st, bool left, bool right);
 sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st, int rank);
 sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st, int rank);
 bool sf_comm_is_local(void *comm);
