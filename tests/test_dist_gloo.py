@@ -209,3 +209,21 @@ def test_bench_weak_scaling_slabs_tile_the_global_model():
     sig = synth.damping_profile(gshape, p.nbl, p.h, 2500.0)
     np.testing.assert_allclose(eta, (m.astype(np.float64) * sig).astype(np.float32))
     assert np.all(eta[p.nbl:-p.nbl, p.nbl:-p.nbl, p.nbl:-p.nbl] == 0)
+
+
+def test_bench_multishot_ranks_get_distinct_shots():
+    """bench.py --gpus N --config 4: every rank runs its own shot (BASELINE configs[4], one
+    shot per GPU) on the same full 400^3 model -- distinct source positions, identical
+    model and receiver grid, no slab decomposition."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    shots = [bench.build_problem(nt_override=4, rank=q, nranks=3, cfg=4) for q in range(3)]
+    p0, m0, d0, g0 = shots[0]
+    assert g0 == p0.shape == (400, 400, 400) and d0 is None
+    xs = [s[0].src_coords[0, 0] for s in shots]
+    assert len(set(xs)) == 3
+    for p, m, d, g in shots[1:]:
+        assert g == g0 and d is None
+        assert np.array_equal(m, m0)
+        assert np.array_equal(p.rec_coords, p0.rec_coords)
