@@ -688,13 +688,16 @@ def test_multishot_allreduce_local_transport():
 
 
 # ------------------------------------------------------------ CUDA graph replay
-@pytest.mark.parametrize("cfg", [0, 1])
+@pytest.mark.parametrize("cfg", [0, 1, "narrow"])
 def test_graph_replay_bitwise(cfg):
     """SF_OPT_GRAPH: the first call runs eagerly, the second identical call is captured as
     one CUDA graph (on the handle's stream, event-ordered after the caller's stream) and
     replayed afterwards: records, states and gradients bitwise those of eager calls; a
     tuning change drops the graph; a restart state (same buffers, new contents) is honoured."""
-    p = synth.make_config(cfg, scale=1.0 if cfg == 0 else 0.15, nt=60)
+    if cfg == "narrow":  # so12 with a 16-column z remainder: two stencil launches per step
+        p = synth.random_problem(3, (40, 44, 144), 12, 40, seed=3, nbl=5, nsrc=2, nrec=9)
+    else:
+        p = synth.make_config(cfg, scale=1.0 if cfg == 0 else 0.15, nt=60)
     p.m_true = (p.m * 0.9).astype(np.float32)
     d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
     ref = make_prop(p)
