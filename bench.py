@@ -75,7 +75,8 @@ class ClockSampler:
     def start(self):
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+             "clocks.mem,power.limit")
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
@@ -93,7 +94,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.f.close()
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, pw, mem, plim = [], None, set(), [], [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:
             for line in f:
@@ -108,8 +109,15 @@ class ClockSampler:
                 for nm, v in zip(names, c[5:9]):
                     if v.lower() == "active":
                         reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                try:
+                    pw.append(float(c[3]))
+                    mem.append(float(c[9]))
+                    plim = float(c[10])
+                except (ValueError, IndexError):
+                    pass
+        med = lambda a: statistics.median(a) if a else None
+        return {"sm_mhz": med(sm), "sm_max_mhz": smax, "mem_mhz": med(mem), "power_w": med(pw),
+                "power_limit_w": plim, "reasons": sorted(reasons), "samples": len(sm)}
 
 
 # ---------------------------------------------------------------------------- workload
