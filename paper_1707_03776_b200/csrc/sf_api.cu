@@ -301,18 +301,6 @@ static sf_status upload(T **dst, const std::vector<T> &v)
 }
 
 
-static void free_itp(SfItpTiles &T)
-{
-    cudaFree(T.beg);
-    cudaFree(T.q);
-    cudaFree(T.lane);
-    cudaFree(T.k);
-    cudaFree(T.j);
-    cudaFree(T.p);
-    cudaFree(T.w);
-    cudaFree(T.left);
-    T = SfItpTiles{};
-}
 
 static void free_inj(SfInjTiles &T)
 {
@@ -383,11 +371,9 @@ static sf_status ensure_inj_tiles(sf_handle *h, SfSparse &sp, int by)
     return SF_OK;
 }
 
-static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStream_t st,
-                             bool *fused, bool *fused_itp)
+static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStream_t st, bool *fused)
 {
     *fused = false;
-    *fused_itp = false;
     SfStepArgs a{};
     a.cur = b.cur;
     a.out = b.out;
@@ -528,16 +514,6 @@ static sf_status launch_interp(sf_handle *h, const SfSparse &sp, const float *u,
     return SF_OK;
 }
 
-static sf_status launch_interp_left(sf_handle *h, const SfSparse &sp, const float *u, float *out,
-                                    cudaStream_t st)
-{
-    if (sp.itiles.nleft == 0 || !out) return SF_OK;
-    ProfScope ps(h, PK_INTERP, st);
-    k_interp_list<<<(sp.itiles.nleft + 127) / 128, 128, 0, st>>>(u, sp.itiles.left, sp.itiles.nleft,
-                                                                 sp.i_idx, sp.i_w, sp.nc, out);
-    SF_CUDA_TRY(cudaGetLastError());
-    return SF_OK;
-}
 
 static sf_status launch_inject(sf_handle *h, const SfSparse &sp, float *u, const float *vals,
                                float *snap_patch, const float *grad_snap, float *grad, float gscale,
@@ -560,15 +536,12 @@ static sf_status launch_inject(sf_handle *h, const SfSparse &sp, float *u, const
 // ------------------------------------------------------------------ sparse tables
 static void free_sparse(SfSparse &s)
 {
-    cudaFree(s.i_idx);
-    cudaFree(s.i_w);
     cudaFree(s.i_owned);
     cudaFree(s.j_tgt);
     cudaFree(s.j_rowptr);
     cudaFree(s.j_pt);
     cudaFree(s.j_coef);
     free_inj(s.tiles);
-    free_itp(s.itiles);
     cudaFree(s.e_idx);
     cudaFree(s.e_w);
     cudaFree(s.ej_pt);
@@ -664,13 +637,9 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
     out.np = np;
     out.nc = nc;
     out.h_tgt = tgt;
-    out.h_iidx = iidx;
-    out.h_iw = iw;
     out.ntgt = (int)tgt.size();
     out.nent = (int)ents.size();
     sf_status s;
-    if ((s = upload(&out.i_idx, iidx))) return s;
-    if ((s = upload(&out.i_w, iw))) return s;
     if (h->nranks > 1 && (s = upload(&out.i_owned, owned))) return s;
     if (out.ntgt > 0) {
         if ((s = upload(&out.j_tgt, tgt))) return s;
@@ -1225,7 +1194,7 @@ static sf_status launch_inject_list(sf_handle *h, const SfSparse &sp, float *u, 
 // 17 % slower on configs[1], and the boundary launch is 2r planes (the TMA kernel would
 // re-read 2r warm-up planes for them anyway).
 static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepBufs bi, int mode,
-                             float *snap_patch, const float *grad_snap, cudaStream_t st, bool *fused_itp)
+                             float *snap_patch, const float *grad_snap, cudaStream_t st)
 {
     sf_status s;
     const int64_t r = h->r;
@@ -1253,10 +1222,10 @@ static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepB
     bb.force_generic = true;
     bb.mq = mq;
     bb.md = md;
-    bool fused = false, f2 = false, fi2 = false;
+    bool fused = false, f2 = false;
     SF_CUDA_TRY(cudaEventRecord(h->ev_pre, st));
     SF_CUDA_TRY(cudaStreamWaitEvent(h->hi_stream, h->ev_pre, 0));
-    if ((s = launch_step(h, bb, mode, h->hi_stream, &fused, fused_itp))) return s;
+    if ((s = launch_step(h, bb, mode, h->hi_stream, &fused))) return s;
     const bool need_inj = !fused && b.inj && b.inj->ntgt > 0 && b.inj_vals;
     if (need_inj) {
         if ((s = ensure_split_lists(h, *b.inj))) return s;
@@ -1271,7 +1240,7 @@ static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepB
     const bool local = sf_comm_p2p_local(h);  // in-process ranks: events, not counters
     for (int side = 0; side < 2 && !local; ++side)
         if (h->p2p_nflag[side] && (s = stream_write32(h->hi_stream, h->p2p_nflag[side], seq))) return s;
-    if ((s = launch_step(h, bi, mode, st, &f2, &fi2))) return s;
+    if ((s = launch_step(h, bi, mode, st, &f2))) return s;
     // (the interior TMA launch may inject its own planes' targets itself)
     if (need_inj && !f2 && (s = launch_inject_list(h, *b.inj, b.out, b.inj_vals, b.inj->jl_int, b.inj->n_int,
                                                    snap_patch, grad_snap, b.grad, b.gscale, st)))
@@ -1292,13 +1261,13 @@ static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepB
 // first, injects there, hands them to NCCL on the comm stream and computes the interior
 // while the halos travel; the stream then waits for the exchange.
 static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, const float *grad_snap,
-                         cudaStream_t st, bool *fused_itp)
+                         cudaStream_t st)
 {
     sf_status s;
     bool fused = false;
     const int64_t r = h->r, xa = h->xa, xb = h->xb;
     if (!h->split || xb - xa <= 2 * r) {
-        if ((s = launch_step(h, b, mode, st, &fused, fused_itp))) return s;
+        if ((s = launch_step(h, b, mode, st, &fused))) return s;
         if (!fused && (s = launch_inject(h, *b.inj, b.out, b.inj_vals, snap_patch, grad_snap, b.grad,
                                          b.gscale, st)))
             return s;
@@ -1307,7 +1276,7 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
     }
     // boundary planes at both ends in ONE launch on the high-priority stream, overlapping
     // the interior launch on `st`; then the exchange on the comm stream
-    bool f2 = false, fi2 = false;
+    bool f2 = false;
     StepBufs bb = b, bi = b;
     bb.xa = xa, bb.xb = xa + r, bb.xa2 = xb - r, bb.xb2 = xb;
     bi.xa = xa + r, bi.xb = xb - r;
@@ -1315,10 +1284,10 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
     // the NCCL exchange kernels (and the side-stream records) run concurrently
     const int reserve = h->comm_sms >= 0 ? h->comm_sms : (h->nranks > 1 ? 8 : 0);
     if (reserve > 0) bi.ctas_cap = std::max(1, h->sms - reserve);
-    if (h->p2p && h->nranks > 1) return do_step_p2p(h, b, bb, bi, mode, snap_patch, grad_snap, st, fused_itp);
+    if (h->p2p && h->nranks > 1) return do_step_p2p(h, b, bb, bi, mode, snap_patch, grad_snap, st);
     SF_CUDA_TRY(cudaEventRecord(h->ev_pre, st));
     SF_CUDA_TRY(cudaStreamWaitEvent(h->hi_stream, h->ev_pre, 0));
-    if ((s = launch_step(h, bb, mode, h->hi_stream, &fused, fused_itp))) return s;
+    if ((s = launch_step(h, bb, mode, h->hi_stream, &fused))) return s;
     const bool need_inj = !fused && b.inj && b.inj->ntgt > 0 && b.inj_vals;
     if (need_inj) {
         if ((s = ensure_split_lists(h, *b.inj))) return s;
@@ -1332,7 +1301,7 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
         if ((s = sf_comm_halo_exchange(h, b.out, h->comm_stream))) return s;
         SF_CUDA_TRY(cudaEventRecord(h->ev_xch, h->comm_stream));
     }
-    if ((s = launch_step(h, bi, mode, st, &f2, &fi2))) return s;
+    if ((s = launch_step(h, bi, mode, st, &f2))) return s;
     if (need_inj && (s = launch_inject_list(h, *b.inj, b.out, b.inj_vals, b.inj->jl_int, b.inj->n_int, snap_patch,
                                             grad_snap, b.grad, b.gscale, st)))
         return s;
@@ -1343,18 +1312,18 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
 // Records of a level run on the handle's side stream, concurrently with the next
 // stencil step (which only reads that level); the stencil two steps later overwrites
 // the level, so it waits for the record first.  ev_itp[level & 1] marks completion.
-static sf_status side_interp(sf_handle *h, SfSparse &sp, bool fused_itp, const float *lvl, float *row,
-                             int level, cudaStream_t st)
+static sf_status side_interp(sf_handle *h, SfSparse &sp, const float *lvl, float *row, int level,
+                             cudaStream_t st)
 {
-    if (!row || sp.np == 0 || (fused_itp && sp.itiles.nleft == 0)) return SF_OK;
+    if (!row || sp.np == 0) return SF_OK;
     if (h->N < SF_SIDE_MIN_POINTS) {
         // small grids are launch-bound: the cross-stream events would cost more than the
         // overlap buys -> interpolate in stream order
-        return fused_itp ? launch_interp_left(h, sp, lvl, row, st) : launch_interp(h, sp, lvl, row, st);
+        return launch_interp(h, sp, lvl, row, st);
     }
     SF_CUDA_TRY(cudaEventRecord(h->ev_ready, st));
     SF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_ready, 0));
-    sf_status s = fused_itp ? launch_interp_left(h, sp, lvl, row, h->side) : launch_interp(h, sp, lvl, row, h->side);
+    sf_status s = launch_interp(h, sp, lvl, row, h->side);
     if (s) return s;
     SF_CUDA_TRY(cudaEventRecord(h->ev_itp[level & 1], h->side));
     h->itp_pending[level & 1] = true;
@@ -1397,7 +1366,7 @@ static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, fl
         if (h->p2p && (s = sf_comm_p2p_setup(h, A, B, st))) return s;
         if ((s = post_step_exchange(h, B, st))) return s;
     }
-    if ((s = side_interp(h, h->rec, false, B, rec, 0, st))) return s;
+    if ((s = side_interp(h, h->rec, B, rec, 0, st))) return s;
     if (snaps && h->snap_half) {
         k_f32_to_f16<<<592, 256, 0, st>>>(reinterpret_cast<__half *>(snaps), B, N);
         SF_CUDA_TRY(cudaGetLastError());
@@ -1414,9 +1383,8 @@ static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, fl
         if ((s = wait_interp(h, n - 1, st))) return s;
         StepBufs b{cur, out, slot, nullptr, 0, 0, nullptr, 0.f, &h->src, wrow, &h->rec, rrow};
         b.itp_cur = n;
-        bool fused_itp = false;
-        if ((s = do_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, slot, nullptr, st, &fused_itp))) return s;
-        if ((s = side_interp(h, h->rec, fused_itp, out, rrow, n + 1, st))) return s;
+        if ((s = do_step(h, b, save ? SF_MODE_SAVE : SF_MODE_PLAIN, slot, nullptr, st))) return s;
+        if ((s = side_interp(h, h->rec, out, rrow, n + 1, st))) return s;
     }
     if ((s = join_side(h, st))) return s;
     // u^{nt-1} was written into A when nt is even: restore (u^{nt-2}, u^{nt-1}) order
@@ -1444,7 +1412,7 @@ static sf_status adjoint_body(sf_handle *h, const float *res, float *srca, float
         if ((s = post_step_exchange(h, B, st))) return s;
     }
     h->itp_pending[0] = h->itp_pending[1] = false;
-    if ((s = side_interp(h, h->src, false, B, srca ? srca + (int64_t)(h->nt - 1) * h->src.np : nullptr,
+    if ((s = side_interp(h, h->src, B, srca ? srca + (int64_t)(h->nt - 1) * h->src.np : nullptr,
                          0, st)))
         return s;
     for (int n = h->nt - 1, j = 0; n >= 1; --n, ++j) {
@@ -1457,11 +1425,10 @@ static sf_status adjoint_body(sf_handle *h, const float *res, float *srca, float
         StepBufs b{cur, out, nullptr, g ? snaps : nullptr, g ? n / save_every : 0, nsnap,
                    g ? grad : nullptr, gscale, &h->rec, rrow, &h->src, srow};
         b.itp_cur = j;
-        bool fused_itp = false;
         if ((s = do_step(h, b, g ? SF_MODE_GRAD : SF_MODE_PLAIN, nullptr,
-                         g ? snap_slot(snaps, h, n / save_every) : nullptr, st, &fused_itp)))
+                         g ? snap_slot(snaps, h, n / save_every) : nullptr, st)))
             return s;
-        if ((s = side_interp(h, h->src, fused_itp, out, srow, j + 1, st))) return s;
+        if ((s = side_interp(h, h->src, out, srow, j + 1, st))) return s;
     }
     if ((s = join_side(h, st))) return s;
     if (h->nt % 2 == 0) return swap_halves(h, A, B, st);

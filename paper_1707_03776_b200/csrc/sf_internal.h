@@ -18,24 +18,11 @@ struct SfInjTiles {
     int *q = nullptr, *lj = nullptr, *t = nullptr;
 };
 
-// Interpolation points grouped by (tile, consumer warp) for the fused interpolation;
-// points whose nonzero corners are not all owned by one lane stay in `left`.
-struct SfItpTiles {
-    int by = 0;
-    int *beg = nullptr;    // [ntiles * by + 1]
-    int *q = nullptr, *lane = nullptr, *k = nullptr, *j = nullptr, *p = nullptr;
-    float *w = nullptr;
-    int *left = nullptr;
-    int nleft = 0;
-};
-
 // Sparse point set on the device (one for sources, one for receivers).
 struct SfSparse {
     int np = 0;          // points
     int nc = 0;          // corners per point (2^ndim)
-    // interpolation (row p: nc corners, fixed order, last axis fastest)
-    int64_t *i_idx = nullptr;
-    float *i_w = nullptr;
+    // interpolation: ELL tables e_idx / e_w below (nonzero corners in corner order)
     int *i_owned = nullptr;  // slab mode: 1 if this rank writes the record row
     // injection: CSR by target grid point
     int ntgt = 0;
@@ -55,10 +42,7 @@ struct SfSparse {
     int *jl_bnd = nullptr, *jl_int = nullptr;
     int n_bnd = -1, n_int = 0;
     std::vector<int64_t> h_tgt;  // host copy of the target offsets
-    std::vector<int64_t> h_iidx; // host copy of the interpolation corners
-    std::vector<float> h_iw;
     SfInjTiles tiles;
-    SfItpTiles itiles;
 };
 
 // One cached CUDA graph of a whole sf_forward / sf_adjoint call (SF_OPT_GRAPH): the

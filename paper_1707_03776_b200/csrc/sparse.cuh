@@ -130,22 +130,6 @@ __global__ void k_csr_to_ell(const int *__restrict__ rowptr, const int *__restri
     }
 }
 
-// interpolation of a listed subset of points (those the TMA epilogue could not fuse)
-__global__ void k_interp_list(const float *__restrict__ u, const int *__restrict__ list, int nl,
-                              const int64_t *__restrict__ idx, const float *__restrict__ W, int nc,
-                              float *__restrict__ out)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nl) return;
-    const int p = list[i];
-    float acc = 0.0f;
-    for (int c = 0; c < nc; ++c) {
-        const float w = W[(int64_t)p * nc + c];
-        if (w != 0.0f) acc = __fmaf_rn(w, u[idx[(int64_t)p * nc + c]], acc);
-    }
-    out[p] = acc;
-}
-
 __global__ void k_inject(float *__restrict__ u, const int64_t *__restrict__ tgt,
                          const int *__restrict__ rowptr, const int *__restrict__ ent_pt,
                          const float *__restrict__ ent_coef, int ntgt,

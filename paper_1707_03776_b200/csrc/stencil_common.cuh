@@ -163,18 +163,12 @@ struct SfStepArgs {
     int64_t mq[4];
     int64_t md[2];
     int l2_prefetch;       // TMA kernel: L2 prefetch distance in planes (0 = off)
-    // Fused sparse work of the TMA kernel (NULL *_beg = none).  Lists are per consumer
-    // warp w of tile t = blockIdx.y * gridDim.x + blockIdx.x: entries
-    // [beg[t * BY + w], beg[t * BY + w + 1]) sorted by output plane q; every entry is
-    // owned by one lane, which applies it to its registers before the store:
-    //   injection: inj_q, inj_lj (lane * 4 + j), inj_t (row of the CSR
-    //     inj_rowptr / inj_pt / inj_coef, values inj_vals[pt]) -> out[t] += sum coef vals;
-    //   interpolation: points whose nonzero corners are all this lane's points:
-    //     itp_q, itp_lane, itp_k (#corners), itp_j / itp_w [4 per entry], itp_p ->
-    //     itp_out[p] = sum_c w_c out[j_c] (corner order, == k_interp).
+    // Fused injection of small point sets in the TMA kernel (NULL inj_beg = none).  Lists
+    // are per (tile, consumer warp): entries [beg[tile * NW + w], beg[tile * NW + w + 1])
+    // sorted by output plane q; every entry is owned by one lane, which applies it to its
+    // registers before the store: inj_q, inj_lj ((row * 32 + lane) * 4 + z),
+    // inj_t (row of the CSR inj_rowptr / inj_pt / inj_coef, values inj_vals[pt]) ->
+    // out[t] += sum coef vals.  (Records are interpolated by a separate kernel.)
     const int *inj_beg, *inj_q, *inj_lj, *inj_t, *inj_rowptr, *inj_pt;
     const float *inj_coef, *inj_vals;
-    const int *itp_beg, *itp_q, *itp_lane, *itp_k, *itp_j, *itp_p;
-    const float *itp_w;
-    float *itp_out;
 };
