@@ -617,9 +617,12 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
             if (wt != 0.0 && own_corner) ents.push_back({off, p, c, wt});
         }
     }
-    std::stable_sort(ents.begin(), ents.end(), [](const Ent &a, const Ent &b) {
+    // deterministic order: target, then point, then corner (unique keys); points given in
+    // grid order (receiver grids) arrive sorted already -> skip the sort
+    auto key_less = [](const Ent &a, const Ent &b) {
         return std::tie(a.tgt, a.pt, a.c) < std::tie(b.tgt, b.pt, b.c);
-    });
+    };
+    if (!std::is_sorted(ents.begin(), ents.end(), key_less)) std::sort(ents.begin(), ents.end(), key_less);
     std::vector<int64_t> tgt;
     std::vector<int> rowptr, pt;
     std::vector<int64_t> etgt;
