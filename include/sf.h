@@ -179,8 +179,8 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   measured 8 % slower on configs[1] with the final kernel)         */
 #define SF_OPT_SPLIT 2         /* 1: boundary planes first, then interior (always on in slab mode;
                                   on one GPU it only reorders work: results are bitwise identical) */
-#define SF_OPT_FUSE_MAX 3      /* largest point set injected / interpolated inside the stencil
-                                  kernel (default 256); larger sets use standalone kernels       */
+#define SF_OPT_FUSE_MAX 3      /* largest point set injected inside the stencil kernel (default
+                                  256); larger sets use the standalone injection kernel          */
 #define SF_OPT_COMM_SMS 4      /* split schedule: SMs the persistent interior launch leaves free
                                   for the concurrent halo exchange (NCCL kernels) and the side-
                                   stream records (default 8 in slab mode, 0 on one GPU; 0..64)   */
