@@ -557,10 +557,22 @@ static void free_sparse(SfSparse &s)
 // error.  Slab mode (C18): axis-0 corners are mapped to the local buffer; a record row
 // is owned by the rank owning the base plane; injection corners by the rank owning
 // the corner's plane.
-static sf_status build_sparse(sf_handle *h, int np, const double *coords, const float *m_dev,
-                              SfSparse &out, const char *what)
+// Host half of the sparse tables (coordinates only: runs before / while m is uploaded).
+struct SparsePlan {
+    int np = 0, nc = 0;
+    std::vector<int> owned;
+    std::vector<int64_t> tgt, etgt;  // injection targets (CSR rows) / per-entry targets
+    std::vector<int> rowptr, pt;
+    std::vector<double> ew;          // per-entry interpolation weight (the coefficient's W)
+    int K = 1;                       // interpolation ELL slots
+    std::vector<int64_t> eidx;       // [K][np]
+    std::vector<float> ewf;          // [K][np]
+};
+
+static sf_status plan_sparse(const sf_handle *h, int np, const double *coords, SparsePlan &pl,
+                             const char *what)
 {
-    out = SfSparse{};
+    pl = SparsePlan{};
     if (np <= 0) return SF_OK;
     if (!coords) return sf_set_error(SF_ERR_INVALID_ARG, "%s coordinates are NULL", what);
     const int nd = h->ndim;
@@ -607,8 +619,8 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
                 }
                 off = off * h->nb[a] + ia;
             }
-            // interpolation corner (zero weights kept in the table, skipped by the kernel;
-            // non-owned rows point at a valid in-buffer index only when owned)
+            // interpolation corner (zero weights dropped from the ELL below; non-owned rows
+            // point at a valid in-buffer index only when owned)
             const bool inbuf = (h->nranks == 1) || owned[p];
             iidx[(size_t)p * nc + c] = inbuf ? off : 0;
             iw[(size_t)p * nc + c] = inbuf ? (float)wt : 0.0f;
@@ -623,35 +635,65 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
         return std::tie(a.tgt, a.pt, a.c) < std::tie(b.tgt, b.pt, b.c);
     };
     if (!std::is_sorted(ents.begin(), ents.end(), key_less)) std::sort(ents.begin(), ents.end(), key_less);
-    std::vector<int64_t> tgt;
-    std::vector<int> rowptr, pt;
-    std::vector<int64_t> etgt;
-    std::vector<double> ew;
+    pl.pt.reserve(ents.size());
+    pl.etgt.reserve(ents.size());
+    pl.ew.reserve(ents.size());
     for (size_t e = 0; e < ents.size(); ++e) {
         if (e == 0 || ents[e].tgt != ents[e - 1].tgt) {
-            tgt.push_back(ents[e].tgt);
-            rowptr.push_back((int)e);
+            pl.tgt.push_back(ents[e].tgt);
+            pl.rowptr.push_back((int)e);
         }
-        pt.push_back(ents[e].pt);
-        etgt.push_back(ents[e].tgt);
-        ew.push_back(ents[e].w);
+        pl.pt.push_back(ents[e].pt);
+        pl.etgt.push_back(ents[e].tgt);
+        pl.ew.push_back(ents[e].w);
     }
-    rowptr.push_back((int)ents.size());
-    out.np = np;
-    out.nc = nc;
-    out.h_tgt = tgt;
-    out.ntgt = (int)tgt.size();
-    out.nent = (int)ents.size();
+    pl.rowptr.push_back((int)ents.size());
+    // interpolation ELL (slot-major): nonzero corners in corner order, zero padded
+    int K = 1;
+    for (int p = 0; p < np; ++p) {
+        int k = 0;
+        for (int c = 0; c < nc; ++c) k += iw[(size_t)p * nc + c] != 0.0f;
+        K = std::max(K, k);
+    }
+    pl.eidx.assign((size_t)K * np, 0);
+    pl.ewf.assign((size_t)K * np, 0.0f);
+    for (int p = 0; p < np; ++p) {
+        int k = 0;
+        for (int c = 0; c < nc; ++c) {
+            const float w = iw[(size_t)p * nc + c];
+            if (w == 0.0f) continue;
+            pl.eidx[(size_t)k * np + p] = iidx[(size_t)p * nc + c];
+            pl.ewf[(size_t)k * np + p] = w;
+            ++k;
+        }
+    }
+    pl.np = np;
+    pl.nc = nc;
+    pl.K = K;
+    pl.owned = std::move(owned);
+    return SF_OK;
+}
+
+// Device half: upload the planned tables, injection coefficients W dt^2 / m at the targets.
+static sf_status commit_sparse(sf_handle *h, const SparsePlan &pl, const float *m_dev, SfSparse &out)
+{
+    out = SfSparse{};
+    if (pl.np <= 0) return SF_OK;
+    out.np = pl.np;
+    out.nc = pl.nc;
+    out.h_tgt = pl.tgt;
+    out.ntgt = (int)pl.tgt.size();
+    out.nent = (int)pl.pt.size();
     sf_status s;
-    if (h->nranks > 1 && (s = upload(&out.i_owned, owned))) return s;
+    if (h->nranks > 1 && (s = upload(&out.i_owned, pl.owned))) return s;
     if (out.ntgt > 0) {
-        if ((s = upload(&out.j_tgt, tgt))) return s;
-        if ((s = upload(&out.j_rowptr, rowptr))) return s;
-        if ((s = upload(&out.j_pt, pt))) return s;
+        if ((s = upload(&out.j_tgt, pl.tgt))) return s;
+        if ((s = upload(&out.j_rowptr, pl.rowptr))) return s;
+        if ((s = upload(&out.j_pt, pl.pt))) return s;
         int64_t *d_etgt = nullptr;
         double *d_ew = nullptr;
-        if ((s = upload(&d_etgt, etgt))) return s;
-        if ((s = upload(&d_ew, ew))) return s;
+        if ((s = upload(&d_etgt, pl.etgt))) return s;
+        if ((s = upload(&d_ew, pl.ew))) return s;
         SF_CUDA_TRY(cudaMalloc(&out.j_coef, sizeof(float) * out.nent));
         k_inject_coef<<<(out.nent + 255) / 256, 256>>>(m_dev, d_etgt, d_ew, out.nent, h->dt * h->dt,
                                                        out.j_coef);
@@ -661,7 +703,7 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
         cudaFree(d_ew);
         // injection ELL (slot-major), when every target has few contributions
         int kmax = 0;
-        for (size_t t = 0; t + 1 < rowptr.size(); ++t) kmax = std::max(kmax, rowptr[t + 1] - rowptr[t]);
+        for (size_t t = 0; t + 1 < pl.rowptr.size(); ++t) kmax = std::max(kmax, pl.rowptr[t + 1] - pl.rowptr[t]);
         if (kmax <= 8) {
             out.jk = kmax;
             SF_CUDA_TRY(cudaMalloc(&out.ej_pt, sizeof(int) * (size_t)kmax * out.ntgt));
@@ -672,30 +714,9 @@ static sf_status build_sparse(sf_handle *h, int np, const double *coords, const 
             SF_CUDA_TRY(cudaDeviceSynchronize());
         }
     }
-    // interpolation ELL (slot-major): nonzero corners in corner order, zero padded
-    {
-        int K = 1;
-        for (int p = 0; p < np; ++p) {
-            int k = 0;
-            for (int c = 0; c < nc; ++c) k += iw[(size_t)p * nc + c] != 0.0f;
-            K = std::max(K, k);
-        }
-        std::vector<int64_t> eidx((size_t)K * np, 0);
-        std::vector<float> ew((size_t)K * np, 0.0f);
-        for (int p = 0; p < np; ++p) {
-            int k = 0;
-            for (int c = 0; c < nc; ++c) {
-                const float w = iw[(size_t)p * nc + c];
-                if (w == 0.0f) continue;
-                eidx[(size_t)k * np + p] = iidx[(size_t)p * nc + c];
-                ew[(size_t)k * np + p] = w;
-                ++k;
-            }
-        }
-        out.ik = K;
-        if ((s = upload(&out.e_idx, eidx))) return s;
-        if ((s = upload(&out.e_w, ew))) return s;
-    }
+    out.ik = pl.K;
+    if ((s = upload(&out.e_idx, pl.eidx))) return s;
+    if ((s = upload(&out.e_w, pl.ewf))) return s;
     return SF_OK;
 }
 
@@ -763,6 +784,17 @@ extern "C" void sf_destroy(sf_handle *h)
 static sf_status create_common(const sf_desc *d, sf_handle *h)
 {
     if (const char *e = getenv("SF_L2_PREFETCH")) h->l2_prefetch = atoi(e);
+    // sparse tables first (host work on the coordinates only: overlaps an upload of m still
+    // in flight, sf_forward_host), receivers -- the large set -- before sources
+    SparsePlan prec, psrc;
+    {
+        const int r0 = d->space_order / 2;
+        h->r = r0;
+        h->h = d->h;
+        sf_status s0;
+        if ((s0 = plan_sparse(h, d->nrec, d->rec_coords, prec, "receiver"))) return s0;
+        if ((s0 = plan_sparse(h, d->nsrc, d->src_coords, psrc, "source"))) return s0;
+    }
     {
         int dev = 0, v = 0;
         if (cudaGetDevice(&dev) == cudaSuccess &&
@@ -834,8 +866,8 @@ static sf_status create_common(const sf_desc *d, sf_handle *h)
         return sf_set_error(SF_ERR_CFL, "Courant number %.4f exceeds the stability limit %.4f "
                             "(so %d, %dD)", courant, lim, d->space_order, d->ndim);
     sf_status s;
-    if ((s = build_sparse(h, d->nsrc, d->src_coords, d->m, h->src, "source"))) return s;
-    if ((s = build_sparse(h, d->nrec, d->rec_coords, d->m, h->rec, "receiver"))) return s;
+    if ((s = commit_sparse(h, psrc, d->m, h->src))) return s;
+    if ((s = commit_sparse(h, prec, d->m, h->rec))) return s;
     SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     SF_CUDA_TRY(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
     {
@@ -1701,6 +1733,7 @@ struct HostCache {
     size_t nm = 0, nd = 0, nw = 0, nr = 0, nu = 0;
     cudaStream_t copy = nullptr;  // record downloads overlapping the next time window
     cudaEvent_t ev = nullptr;
+    cudaEvent_t evh = nullptr;    // uploads done (orders sf_create's legacy-stream work)
 };
 HostCache g_hc;
 
@@ -1737,7 +1770,11 @@ extern "C" sf_status sf_forward_host(const sf_desc *hd, const float *wavelet_hos
         SF_CUDA_TRY(cudaMemcpyAsync(g_hc.damp, hd->damp, N * sizeof(float), cudaMemcpyHostToDevice, st));
     if (nw) SF_CUDA_TRY(cudaMemcpyAsync(g_hc.wav, wavelet_host, nw * sizeof(float), cudaMemcpyHostToDevice, st));
     SF_CUDA_TRY(cudaMemsetAsync(g_hc.u, 0, 2 * N * sizeof(float), st));
-    SF_CUDA_TRY(cudaStreamSynchronize(st));  // sf_create runs on the legacy stream
+    // sf_create's device work runs on the legacy stream: order it after the uploads by an
+    // event instead of a host sync, so that its host-side table building overlaps them
+    if (!g_hc.evh) SF_CUDA_TRY(cudaEventCreateWithFlags(&g_hc.evh, cudaEventDisableTiming));
+    SF_CUDA_TRY(cudaEventRecord(g_hc.evh, st));
+    SF_CUDA_TRY(cudaStreamWaitEvent(cudaStreamLegacy, g_hc.evh, 0));
     sf_desc dd = *hd;
     dd.m = g_hc.m;
     dd.damp = hd->damp ? g_hc.damp : nullptr;
