@@ -41,6 +41,21 @@
 #define SF_MBAR_SUSPEND_NS 0x100000
 #endif
 
+// Debug builds (-DSF_DEBUG_BOUNDS): every shared-memory load is checked against its ring
+// slot and every global store against its buffer; a violation traps (compute-sanitizer is
+// not available on the test pool).
+#ifdef SF_DEBUG_BOUNDS
+#define SF_CHK(p, lo, hi)                                                                   \
+    do {                                                                                   \
+        if ((const float *)(p) < (const float *)(lo) || (const float *)(p) + 4 > (const float *)(hi)) \
+            __trap();                                                                      \
+    } while (0)
+#else
+#define SF_CHK(p, lo, hi) \
+    do {                  \
+    } while (0)
+#endif
+
 namespace sftma {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -491,7 +506,10 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                         // y rows rown - R .. rown + VY - 1 + R (own rows included)
                         f2_t Y[VY + 2 * R][NJ];
 #pragma unroll
-                        for (int t = 0; t < VY + 2 * R; ++t) ldp<VZ>(uq + own_off + (t - R) * W, Y[t]);
+                        for (int t = 0; t < VY + 2 * R; ++t) {
+                            SF_CHK(uq + own_off + (t - R) * W, uq, uq + W * C::H);
+                            ldp<VZ>(uq + own_off + (t - R) * W, Y[t]);
+                        }
 #pragma unroll
                         for (int j = 0; j < VY; ++j)
 #pragma unroll
@@ -502,6 +520,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                         for (int j = 0; j < VY; ++j) {
 #pragma unroll
                             for (int c = 0; c < HZ / VZ; ++c) {
+                                SF_CHK(uq + own_off + j * W - HZ + VZ * c, uq, uq + W * C::H);
+                                SF_CHK(uq + own_off + j * W + VZ + VZ * c, uq, uq + W * C::H);
                                 ldp<VZ>(uq + own_off + j * W - HZ + VZ * c, ZL[j] + NJ * c);
                                 ldp<VZ>(uq + own_off + j * W + VZ + VZ * c, ZR[j] + NJ * c);
                             }
@@ -554,7 +574,10 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                         constexpr int S = decltype(ic)::value;
                         constexpr int SQ = (S - R + Q) % Q;
 #pragma unroll
-                        for (int j = 0; j < VY; ++j) ldp<VZ>(ut + own_off + j * W, V[S][j]);
+                        for (int j = 0; j < VY; ++j) {
+                            SF_CHK(ut + own_off + j * W, ut, ut + W * C::H);
+                            ldp<VZ>(ut + own_off + j * W, V[S][j]);
+                        }
                         if (outp) {
 #pragma unroll
                             for (int j = 0; j < VY; ++j)
@@ -591,6 +614,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                         f2_t ov[VY][NJ], cv[VY][NJ], bv[VY][NJ], sv[VY][NJ], gv[VY][NJ];
 #pragma unroll
                         for (int j = 0; j < VY; ++j) {
+                            SF_CHK(cp + j * TZ, cbase + cs * CF, cbase + cs * CF + C::NPL * PF);
+                            SF_CHK(cp + PF + j * TZ, cbase + cs * CF, cbase + cs * CF + C::NPL * PF);
                             ldp<VZ>(cp + j * TZ, ov[j]);
                             ldp<VZ>(cp + PF + j * TZ, cv[j]);
                             int nxt = 2;
@@ -695,6 +720,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             // (measured 5 % faster on configs[3])
 #pragma unroll
                             for (int j = 0; j < VY; ++j) {
+                                if (act[j]) SF_CHK(optr + j * n2, a.out, a.out + a.n0b * plane);
                                 stp_if<VZ>(optr + j * n2, res2[j], act[j]);
                                 if (MODE == SF_MODE_SAVE) {
                                     if (a.snap_half) {
@@ -712,6 +738,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                                 for (int j = 0; j < VY; ++j) {
                                     if (yg + j < a.n1) {
+                                        SF_CHK(optr + j * a.n2, a.out, a.out + a.n0b * plane);
                                         stp<VZ>(optr + j * a.n2, res2[j]);
                                         if (MODE == SF_MODE_SAVE) {
                                             if (a.snap_half) stsnap_half<VZ>(a.snap_out, sptr + j * a.n2, res2[j]);
