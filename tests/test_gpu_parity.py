@@ -973,3 +973,28 @@ def test_bench_json_contract():
     for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
         assert k in d["e2e"], k
     assert "workload" in d["config"]
+
+
+@pytest.mark.parametrize("so", [12, 16])
+def test_gradient_high_order_damped_tma(so):
+    """GRAD mode at the tightest shared-memory plans (r = 6 / 8 with the beta array: the u
+    ring shrinks to its minimum depth and two coefficient stages of five planes): gradient
+    and J vs the oracle, and bitwise equal to the generic kernel; adjoint source records
+    too."""
+    p = synth.random_problem(3, (34, 30, 64), so, 60, seed=17, nbl=6, nsrc=1, nrec=16)
+    rng = np.random.default_rng(8)
+    p.m_true = (p.m * rng.uniform(0.88, 1.12, p.m.shape)).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    go = oracle.gradient(p, d_obs, save_every=2)
+    outs = []
+    for variant in (2, 1):
+        prop = make_prop(p)
+        prop.set_tuning(variant, 0, 0)
+        assert prop.tuning()["variant"] == variant
+        g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
+        torch.cuda.synchronize()
+        outs.append((g.cpu().numpy(), J))
+        prop.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+    assert rel(outs[0][0], go["grad"]) <= TOL, rel(outs[0][0], go["grad"])
+    assert abs(outs[0][1] - go["J"]) <= 1e-4 * go["J"]
