@@ -188,7 +188,8 @@ def test_forward_snapshots():
         assert rel(sg[k], so_[k]) <= TOL, k
 
 
-@pytest.mark.parametrize("ndim,shape,so", [(2, (51, 44), 4), (3, (28, 26, 64), 8), (3, (24, 22, 20), 6)])
+@pytest.mark.parametrize("ndim,shape,so", [(2, (51, 44), 4), (3, (28, 26, 64), 8), (3, (24, 22, 20), 6),
+                                         (3, (30, 28, 144), 12), (3, (26, 24, 64), 16)])
 def test_adjoint_parity(ndim, shape, so):
     p = synth.random_problem(ndim, shape, so, 70, seed=21, nbl=5, nsrc=2, nrec=8)
     res = np.random.default_rng(1).standard_normal((p.nt, 8)).astype(np.float32)
