@@ -204,23 +204,80 @@ def adjoint(prob=None, *, res=None, m=None, damp=None, shape=None, h=None, space
     return {"srca": srca[:, :nsrc], "v_state": st, "grad": g}
 
 
-def gradient(prob, d_obs, m=None, save_every: int = 1, snap_dtype=None):
+def _snap_round(snaps, snap_dtype):
+    if snap_dtype == "float16":
+        return snaps.astype(np.float32).astype(np.float16).astype(np.float64)
+    if snap_dtype is not None:
+        raise ValueError(f"snap_dtype {snap_dtype!r}")
+    return snaps
+
+
+def gradient(prob, d_obs, m=None, save_every: int = 1, snap_dtype=None, checkpoint: int = 0):
     """FWI gradient at model m (default prob.m): forward with snapshots, residual
     res = d_syn - d_obs, J = 1/2 sum res^2, adjoint with correlation (C13/C14).
     snap_dtype='float16': the snapshots are stored in IEEE half precision before the
     correlation (reading C23: u^n -> fp32 -> fp16, round to nearest even at both steps,
-    numpy's conversions; widened exactly).  Returns dict(grad, J, res, d_syn)."""
+    numpy's conversions; widened exactly).  Returns dict(grad, J, res, d_syn, srca).
+
+    checkpoint = S > 0 (a multiple of save_every): checkpoint-recompute (SURVEY §8(c)
+    item 4), for runs whose fp64 snapshots do not fit host memory.  The forward runs in
+    time windows [c, c + S] (c = 0, S, 2S, ...; the last one ragged), each restarted from
+    the state pair (u^{c-1}, u^c) the previous window ended with, which is kept as the
+    window's checkpoint; the record rows are the windows' rows (row c of a window is P u^c
+    again).  The backward sweep takes the windows last to first: it recomputes the
+    window's forward from its checkpoint with snapshots every k (levels c, c+k, ..., all
+    in the window because S % k == 0), then runs the adjoint over the same window
+    -- adjoint time steps t = c+S .. c+1 on res[c : c+S+1], continuing the (v^{t+1}, v^t)
+    pair of the later window -- which adds that window's correlation terms.  Every level,
+    record row and gradient term is computed by the same operations as in the stored-
+    snapshot run, so the result is bitwise identical (pinned in tests/test_oracle_pins.py).
+    Memory: 2 N (nt-1)/S checkpoint floats + N (S/k + 1) snapshot floats."""
     mm = prob.m if m is None else m
+    if checkpoint:
+        return _gradient_ckpt(prob, d_obs, mm, save_every, snap_dtype, int(checkpoint))
     fw = forward(prob, m=mm, save_every=save_every)
     res = fw["rec"] - _f64(d_obs)
     J = 0.5 * float(np.sum(res * res))
-    snaps = fw["snaps"]
-    if snap_dtype == "float16":
-        snaps = snaps.astype(np.float32).astype(np.float16).astype(np.float64)
-    elif snap_dtype is not None:
-        raise ValueError(f"snap_dtype {snap_dtype!r}")
+    snaps = _snap_round(fw["snaps"], snap_dtype)
     ad = adjoint(prob, res=res, m=mm, save_every=save_every, snaps=snaps)
-    return {"grad": ad["grad"], "J": J, "res": res, "d_syn": fw["rec"]}
+    return {"grad": ad["grad"], "J": J, "res": res, "d_syn": fw["rec"], "srca": ad["srca"]}
+
+
+def _gradient_ckpt(prob, d_obs, mm, k, snap_dtype, S):
+    if k < 1 or S < 1 or S % k:
+        raise ValueError(f"checkpoint {S} must be a positive multiple of save_every {k}")
+    nt = prob.nt
+    shape = tuple(int(s) for s in prob.shape)
+    nsrc = len(prob.src_coords) if prob.src_coords is not None else 0
+    nrec = len(prob.rec_coords) if prob.rec_coords is not None else 0
+    wav = _f64(prob.wavelet).reshape(nt, -1) if nsrc else None
+    windows = [(c, min(c + S, nt - 1)) for c in range(0, nt - 1, S)]
+    # forward sweep: record rows and one checkpoint (u^{c-1}, u^c) per window
+    rec = np.zeros((nt, nrec))
+    ckpt = []
+    st = np.zeros((2,) + shape)
+    for c, e in windows:
+        ckpt.append(st)
+        fw = forward(prob, m=mm, nt=e - c + 1, wavelet=None if wav is None else wav[c:e + 1],
+                     u_state=st)
+        rec[c:e + 1] = fw["rec"]
+        st = fw["u_state"]
+    res = rec - _f64(d_obs)
+    J = 0.5 * float(np.sum(res * res))
+    # backward sweep: recompute each window's snapshots, adjoint over the same window
+    grad = np.zeros(shape)
+    srca = np.zeros((nt, nsrc))
+    vst = np.zeros((2,) + shape)
+    for (c, e), st in zip(reversed(windows), reversed(ckpt)):
+        L = e - c + 1
+        fw = forward(prob, m=mm, nt=L, wavelet=None if wav is None else wav[c:e + 1],
+                     u_state=st, save_every=k)
+        ad = adjoint(prob, res=res[c:e + 1], m=mm, nt=L, v_state=vst, save_every=k,
+                     snaps=_snap_round(fw["snaps"], snap_dtype), grad=grad)
+        grad = ad["grad"]
+        vst = ad["v_state"]
+        srca[c:e + 1] = ad["srca"]
+    return {"grad": grad, "J": J, "res": res, "d_syn": rec, "srca": srca}
 
 
 # ------------------------------------------------------------------ other paper workloads (f4)

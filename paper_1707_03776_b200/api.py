@@ -10,6 +10,7 @@ library's CUDA kernels.  Arrays:
 from __future__ import annotations
 
 import ctypes
+import functools
 from typing import Optional
 
 import numpy as np
@@ -81,6 +82,16 @@ def nccl_comm_destroy(comm: int):
     check(lib().sf_nccl_comm_destroy(ctypes.c_void_p(comm)))
 
 
+def _ondev(fn):
+    """Run a Propagator method with the handle's device current: the library allocates,
+    launches and creates streams on the current device."""
+    @functools.wraps(fn)
+    def w(self, *a, **k):
+        with torch.cuda.device(self.device):
+            return fn(self, *a, **k)
+    return w
+
+
 class Propagator:
     """One acoustic problem bound to a device handle (sf_create / sf_create_slab).
 
@@ -133,14 +144,15 @@ class Propagator:
                 d.sigma[a] = sa.ctypes.data
         self._desc = d
         hnd = ctypes.c_void_p()
-        torch.cuda.synchronize()
-        if comm is not None or self.nranks > 1:
-            check(lib().sf_create_slab(ctypes.byref(d), ctypes.c_void_p(comm), rank, nranks,
-                                       ctypes.byref(hnd)))
-        else:
-            check(lib().sf_create(ctypes.byref(d), ctypes.byref(hnd)))
-        self._h = hnd
         self.device = m.device
+        with torch.cuda.device(self.device):
+            torch.cuda.synchronize()
+            if comm is not None or self.nranks > 1:
+                check(lib().sf_create_slab(ctypes.byref(d), ctypes.c_void_p(comm), rank, nranks,
+                                           ctypes.byref(hnd)))
+            else:
+                check(lib().sf_create(ctypes.byref(d), ctypes.byref(hnd)))
+        self._h = hnd
         self.snap_dtype = torch.float32
 
     # -------------------------------------------------------------- lifetime
@@ -168,11 +180,13 @@ class Propagator:
     def zeros_state(self):
         return torch.zeros((2,) + self.local_shape, device=self.device, dtype=torch.float32)
 
+    @_ondev
     def set_tuning(self, variant: int = 0, vy: int = 0, ctas: int = 0):
         """sf_set_tuning: variant (0 auto, 1 generic, 2 TMA), rows per thread (0 auto, 1, 2),
         persistent CTAs (0 = one per SM)."""
         check(lib().sf_set_tuning(self._h, variant, vy, ctas))
 
+    @_ondev
     def set_option(self, option: int, value: int):
         """sf_set_option: 1 L2 prefetch distance, 2 split boundary launches, 3 fuse-max points,
         4 SMs left free by the split interior launch, 5 CUDA-graph replay of whole calls,
@@ -181,14 +195,17 @@ class Propagator:
         if int(option) == 7:
             self.snap_dtype = torch.float16 if value else torch.float32
 
+    @_ondev
     def tuning(self):
         v, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         check(lib().sf_get_tuning(self._h, ctypes.byref(v), ctypes.byref(b), ctypes.byref(c)))
         return {"variant": v.value, "vy": b.value, "ctas": c.value}
 
+    @_ondev
     def set_profiling(self, on: bool = True):
         check(lib().sf_set_profiling(self._h, 1 if on else 0))
 
+    @_ondev
     def profile(self, reset: bool = True):
         """Summed in-stream kernel times (CUDA events) and launch counts since the last
         reset, by kind: stencil / inject / interp / other."""
@@ -202,6 +219,7 @@ class Propagator:
         return out
 
     # -------------------------------------------------------------- the path
+    @_ondev
     def forward(self, wavelet: Optional[torch.Tensor], *, u: Optional[torch.Tensor] = None,
                 rec: Optional[torch.Tensor] = None, save_every: int = 0,
                 snaps: Optional[torch.Tensor] = None, stream=None):
@@ -223,6 +241,7 @@ class Propagator:
                                _ptr(snaps), int(save_every), _stream(stream)))
         return rec, u, snaps
 
+    @_ondev
     def adjoint(self, res: Optional[torch.Tensor], *, v: Optional[torch.Tensor] = None,
                 srca: Optional[torch.Tensor] = None, snaps: Optional[torch.Tensor] = None,
                 save_every: int = 0, grad: Optional[torch.Tensor] = None, stream=None):
@@ -245,6 +264,7 @@ class Propagator:
                                _ptr(snaps), int(save_every), _ptr(grad), _stream(stream)))
         return srca, v, grad
 
+    @_ondev
     def residual(self, d_syn: torch.Tensor, d_obs: torch.Tensor, res: Optional[torch.Tensor] = None,
                  stream=None):
         _dev(d_syn, "d_syn", (self.nt, self.nrec))
@@ -258,6 +278,7 @@ class Propagator:
     def gradient_workspace_bytes(self, save_every: int) -> int:
         return int(lib().sf_gradient_workspace_bytes(self._h, int(save_every)))
 
+    @_ondev
     def gradient(self, wavelet: torch.Tensor, d_obs: torch.Tensor, *, save_every: int = 1,
                  grad: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None, stream=None):
         """sf_gradient: returns (grad [local grid], J)."""
@@ -278,6 +299,7 @@ class Propagator:
     def gradient_ckpt_workspace_bytes(self, save_every: int, segment: int) -> int:
         return int(lib().sf_gradient_ckpt_workspace_bytes(self._h, int(save_every), int(segment)))
 
+    @_ondev
     def gradient_ckpt(self, wavelet: torch.Tensor, d_obs: torch.Tensor, *, save_every: int = 1,
                       segment: int, grad: Optional[torch.Tensor] = None, ws: Optional[torch.Tensor] = None,
                       stream=None):
@@ -299,6 +321,7 @@ class Propagator:
                                      int(save_every), int(segment), _stream(stream)))
         return grad, J.value
 
+    @_ondev
     def allreduce_gradient(self, comm: int, grad: torch.Tensor, J: Optional[float] = None, rank: int = 0,
                            stream=None):
         return allreduce_gradient(comm, grad, J, handle=self, rank=rank, stream=stream)

@@ -1,6 +1,7 @@
 // inst_body.cuh -- instantiates every stencil-step kernel for one radius SF_R
 // (included by inst_r<R>.cu).  Dispatch: variant x (by, damp, mode).
 #include <algorithm>
+#include <atomic>
 #include "launch.cuh"
 #include "stencil_generic.cuh"
 #include "stencil_tma.cuh"
@@ -18,11 +19,16 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     using C = sftma::Cfg<SF_R, VY, DM, MODE, LZ>;
     auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE, LZ>;
-    static bool attr = false;
-    if (!attr) {
+    // the dynamic shared-memory limit is a per-device function attribute: cached per device
+    // in an atomic bitmask (handles on several GPUs, concurrent rank threads)
+    static std::atomic<uint64_t> attr{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0ull;
+    if (!bit || !(attr.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr.fetch_or(bit, std::memory_order_release);
     }
     // persistent grid: (tile, x-chunk) items, at most one CTA per SM (shared memory admits
     // one), items dealt round-robin.  The chunk count minimises rounds x (chunk + 2r): each

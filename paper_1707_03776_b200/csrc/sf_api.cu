@@ -1208,7 +1208,9 @@ static sf_status launch_inject_list(sf_handle *h, const SfSparse &sp, float *u, 
                                                             list, nl, vals, snap_patch, grad_snap, grad, gscale,
                                                             h->snap_half ? 1 : 0, mir);
     } else {
-        return sf_set_error(SF_ERR_INVALID_ARG, "split injection needs <= 8 contributions per target");
+        k_inject_csr_list<<<(nl + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.j_rowptr, sp.j_pt, sp.j_coef, list,
+                                                            nl, vals, snap_patch, grad_snap, grad, gscale,
+                                                            h->snap_half ? 1 : 0, mir);
     }
     SF_CUDA_TRY(cudaGetLastError());
     return SF_OK;
@@ -1735,7 +1737,11 @@ struct HostCache {
     cudaEvent_t ev = nullptr;
     cudaEvent_t evh = nullptr;    // uploads done (orders sf_create's legacy-stream work)
 };
-HostCache g_hc;
+// one cache per device: its buffers, stream and events belong to the device that was
+// current when they were created (cudaMalloc is synchronous, so a buffer is usable on any
+// stream of its device as soon as ensure() returns)
+constexpr int SF_HC_DEVICES = 64;
+HostCache g_hcs[SF_HC_DEVICES];
 
 sf_status ensure(float **p, size_t *cap, size_t n)
 {
@@ -1756,6 +1762,10 @@ extern "C" sf_status sf_forward_host(const sf_desc *hd, const float *wavelet_hos
     sf_status s = validate_desc(hd);
     if (s) return s;
     cudaStream_t st = S(stream);
+    int dev = 0;
+    SF_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= SF_HC_DEVICES) return sf_set_error(SF_ERR_INVALID_ARG, "device %d", dev);
+    HostCache &g_hc = g_hcs[dev];
     std::lock_guard<std::mutex> lk(g_hc.mu);
     size_t N = 1;
     for (int a = 0; a < hd->ndim; ++a) N *= (size_t)hd->shape[a];

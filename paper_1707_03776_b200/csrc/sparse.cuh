@@ -116,6 +116,30 @@ __global__ void k_inject_ell_list(float *__restrict__ u, const int64_t *__restri
     if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(snap_ld(grad_snap, g, snap_half), d), grad[g]);
 }
 
+// k_inject restricted to a list of target rows (split launches when some target has more
+// than 8 contributions, i.e. no ELL table): the same terms in the same order as k_inject
+__global__ void k_inject_csr_list(float *__restrict__ u, const int64_t *__restrict__ tgt,
+                                  const int *__restrict__ rowptr, const int *__restrict__ ent_pt,
+                                  const float *__restrict__ ent_coef, const int *__restrict__ list, int nl,
+                                  const float *__restrict__ vals, void *__restrict__ snap_patch,
+                                  const void *__restrict__ grad_snap, float *__restrict__ grad, float gscale,
+                                  int snap_half, SfMirror mir)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nl) return;
+    const int t = list[i];
+    float d = 0.0f;
+    for (int e = rowptr[t]; e < rowptr[t + 1]; ++e) d = __fmaf_rn(ent_coef[e], vals[ent_pt[e]], d);
+    const int64_t g = tgt[t];
+    const float un = __fadd_rn(u[g], d);
+    u[g] = un;
+    const int64_t q = g / mir.plane;
+    if (q >= mir.mq[0] && q < mir.mq[1]) *reinterpret_cast<float *>(reinterpret_cast<char *>(u + g) + mir.md[0]) = un;
+    else if (q >= mir.mq[2] && q < mir.mq[3]) *reinterpret_cast<float *>(reinterpret_cast<char *>(u + g) + mir.md[1]) = un;
+    if (snap_patch) snap_st(snap_patch, g, un, snap_half);
+    if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(snap_ld(grad_snap, g, snap_half), d), grad[g]);
+}
+
 // CSR -> ELL (slot-major) for the injection tables
 __global__ void k_csr_to_ell(const int *__restrict__ rowptr, const int *__restrict__ pt,
                              const float *__restrict__ coef, int ntgt, int K, int *__restrict__ ept,

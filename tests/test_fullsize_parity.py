@@ -1,0 +1,170 @@
+"""Full-size, full-length parity: every BASELINE config at its stated grid AND its stated nt,
+GPU (C-ABI, the launch configuration bench.py times) vs the fp64 oracle on the same seeded
+inputs (north_star: rel L2 <= 1e-4 on receiver records, final wavefields and gradients).
+
+The gradients run the configs' own model pairs (d_obs = synthetic(true), gradient at the
+smoothed initial model, residual = synthetic(initial) - synthetic(true), BJ.cfg[2]/[4]);
+each side forms its own d_obs (GPU from its forward, oracle from its forward), so the whole
+pipeline is compared.  The oracle gradient uses checkpoint-recompute (SURVEY 8(c) item 4,
+oracle.gradient(checkpoint=S), pinned bitwise to the stored-snapshot form) because its fp64
+snapshots would not fit host memory.
+
+These runs take minutes of host time each (the oracle at ~0.3 GPts/s), so they are opt-in:
+SF_FULLSIZE=1 (or a comma list of config indices, e.g. SF_FULLSIZE=1,3).  Each test writes
+its errors (overall relative L2, worst per-trace relative L2, max abs error / max abs value,
+J) as JSON under $SF_PARITY_OUT (default gpurun_out/parity/); the committed copies live in
+profiles/ (r02_parity_c*.json).
+"""
+import json
+import math
+import os
+import time
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+
+_SEL = os.environ.get("SF_FULLSIZE", "")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not _SEL, reason="full-size parity is opt-in (SF_FULLSIZE)")]
+TOL = 1e-4
+
+
+def _want(ci):
+    return _SEL in ("1", "all") or str(ci) in _SEL.split(",")
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def trace_stats(g, o):
+    """Per-trace errors of a record [nt][npoint]: the worst relative L2 over traces whose
+    energy is >= 1e-6 of the strongest trace's (weaker ones are numerically empty), and
+    the max abs error relative to the record's max abs value."""
+    g = np.asarray(g, np.float64)
+    o = np.asarray(o, np.float64)
+    en = np.linalg.norm(o, axis=0)
+    live = en >= 1e-6 * en.max()
+    per = np.linalg.norm(g - o, axis=0)[live] / en[live]
+    return {"rel_l2": rel(g, o), "worst_trace_rel_l2": float(per.max()),
+            "worst_trace": int(np.flatnonzero(live)[per.argmax()]), "live_traces": int(live.sum()),
+            "max_abs_err_over_max_abs": float(np.abs(g - o).max() / np.abs(o).max())}
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def make_prop(p, m=None):
+    import paper_1707_03776_b200 as sf
+    m = p.m if m is None else m
+    pr = sf.Propagator(dev(m), None if p.damp is None else dev(p.damp), shape=p.shape, h=p.h,
+                       space_order=p.space_order, nt=p.nt, dt=p.dt,
+                       src_coords=p.src_coords.astype(np.float64),
+                       rec_coords=p.rec_coords.astype(np.float64))
+    return pr
+
+
+def ckpt_segment(nt, k):
+    """S = the multiple of k nearest sqrt(2 (nt-1) k): minimises checkpoint + window memory
+    2 N (nt-1)/S + N S/k."""
+    return max(k, int(round(math.sqrt(2.0 * (nt - 1) * k) / k)) * k)
+
+
+def _dump(ci, out):
+    d = os.environ.get("SF_PARITY_OUT", os.path.join("gpurun_out", "parity"))
+    os.makedirs(d, exist_ok=True)
+    out["config"] = ci
+    out["oracle_threads"] = oracle.num_threads()
+    with open(os.path.join(d, f"parity_c{ci}.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out))
+
+
+def _forward_case(ci):
+    p = synth.make_config(ci)
+    t0 = time.time()
+    prop = make_prop(p)
+    tun = prop.tuning()
+    rec, u, _ = prop.forward(dev(p.wavelet))
+    torch.cuda.synchronize()
+    rg, ug = rec.cpu().numpy(), u.cpu().numpy()
+    prop.close()
+    del rec, u
+    t1 = time.time()
+    o = oracle.forward(p)
+    t2 = time.time()
+    out = {"kind": "forward", "shape": list(p.shape), "space_order": p.space_order, "nt": p.nt,
+           "tuning": tun, "rec": trace_stats(rg, o["rec"]),
+           "u_last_rel_l2": rel(ug[1], o["u_state"][1]), "u_prev_rel_l2": rel(ug[0], o["u_state"][0]),
+           "u_last_norm": float(np.linalg.norm(o["u_state"][1])),
+           "gpu_s": t1 - t0, "oracle_s": t2 - t1}
+    _dump(ci, out)
+    assert out["rec"]["rel_l2"] <= TOL
+    assert out["u_last_rel_l2"] <= TOL and out["u_prev_rel_l2"] <= TOL
+
+
+def _gradient_case(ci, shot=0):
+    p = synth.make_config(ci, shot=shot) if ci == 4 else synth.make_config(ci)
+    k = p.save_every
+    t0 = time.time()
+    # GPU: d_obs = forward at the true model, gradient at the initial model
+    pt = make_prop(p, m=p.m_true)
+    d_obs_g, _, _ = pt.forward(dev(p.wavelet))
+    pt.close()
+    prop = make_prop(p)
+    tun = prop.tuning()
+    g, J = prop.gradient(dev(p.wavelet), d_obs_g, save_every=k)
+    torch.cuda.synchronize()
+    gg = g.cpu().numpy()
+    dg = d_obs_g.cpu().numpy()
+    prop.close()
+    del g, d_obs_g
+    torch.cuda.empty_cache()
+    t1 = time.time()
+    # oracle: its own d_obs, checkpointed gradient
+    d_obs_o = oracle.forward(p, m=p.m_true)["rec"]
+    S = ckpt_segment(p.nt, k)
+    go = oracle.gradient(p, d_obs_o, save_every=k, checkpoint=S)
+    t2 = time.time()
+    out = {"kind": "gradient", "shape": list(p.shape), "space_order": p.space_order, "nt": p.nt,
+           "save_every": k, "checkpoint_segment": S, "shot": shot, "tuning": tun,
+           "d_obs": trace_stats(dg, d_obs_o), "d_syn_oracle_rel_residual":
+               float(np.linalg.norm(go["res"]) / np.linalg.norm(d_obs_o)),
+           "grad_rel_l2": rel(gg, go["grad"]), "J_gpu": J, "J_oracle": go["J"],
+           "J_rel_err": abs(J - go["J"]) / go["J"], "gpu_s": t1 - t0, "oracle_s": t2 - t1}
+    _dump(ci, out)
+    assert out["d_obs"]["rel_l2"] <= TOL
+    assert out["grad_rel_l2"] <= TOL and out["J_rel_err"] <= TOL
+
+
+@pytest.mark.skipif(not _want(0), reason="not selected")
+def test_config0_full():
+    _forward_case(0)
+
+
+@pytest.mark.skipif(not _want(1), reason="not selected")
+def test_config1_full():
+    _forward_case(1)
+
+
+@pytest.mark.skipif(not _want(2), reason="not selected")
+def test_config2_full_gradient():
+    _gradient_case(2)
+
+
+@pytest.mark.skipif(not _want(3), reason="not selected")
+def test_config3_full():
+    _forward_case(3)
+
+
+@pytest.mark.skipif(not _want(4), reason="not selected")
+def test_config4_full_gradient_one_shot():
+    _gradient_case(4, shot=0)

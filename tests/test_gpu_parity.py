@@ -581,8 +581,9 @@ def _slab_inputs(p, rank, nranks):
     return x0, nl, m, eta
 
 
-@pytest.mark.parametrize("nranks,variant,p2p", [(2, 2, 0), (3, 2, 0), (3, 1, 0), (2, 2, 1), (3, 2, 1), (3, 1, 1)])
-def test_slab_decomposition_bitwise_local_transport(nranks, variant, p2p):
+@pytest.mark.parametrize("nranks,variant,p2p,dense", [(2, 2, 0, 0), (3, 2, 0, 0), (3, 1, 0, 0), (2, 2, 1, 0),
+                                                      (3, 2, 1, 0), (3, 1, 1, 0), (2, 2, 0, 1), (3, 2, 1, 1)])
+def test_slab_decomposition_bitwise_local_transport(nranks, variant, p2p, dense):
     """The multi-GPU slab path (local [n0_loc + 2r] buffers, split boundary/interior
     launches with the persistent-kernel SM reservation, per-step halo exchange, owner-only
     injection and records, record all-reduce inside the gradient) run as rank threads on
@@ -591,13 +592,18 @@ def test_slab_decomposition_bitwise_local_transport(nranks, variant, p2p):
     those of the single-domain run (reading C18).  Sources and receivers straddle the slab
     boundaries.  p2p = 1: SF_OPT_P2P -- the boundary kernel stores the boundary planes
     straight into the neighbours' halos and the streams order on counters; the
-    transport then only runs once per call (the initial halo)."""
+    transport then only runs once per call (the initial halo).  dense = 1: 20 receivers
+    inside one grid cell at a rank boundary, so their 8 corners get 20 contributions each
+    and the adjoint injection takes the CSR path (no ELL table) in the split launches."""
     S = sf()
     p = synth.random_problem(3, (41, 30, 64), 8, 50, seed=91, nbl=5, nsrc=3, nrec=40)
     h = p.h
     p.src_coords[0, 0] = 13.5 * h          # on / across the rank boundaries (41 planes)
     p.src_coords[1, 0] = 20.2 * h
     p.rec_coords[:20, 0] = np.linspace(8 * h, 33 * h, 20)
+    if dense:
+        cell = np.array([13.0, 14.0, 30.0]) * h
+        p.rec_coords[20:] = (cell + np.random.default_rng(5).uniform(0.1, 0.9, (20, 3)) * h).astype(np.float32)
     p.m_true = (p.m * 0.92).astype(np.float32)
     d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
     prop = make_prop(p)
@@ -999,3 +1005,18 @@ def test_gradient_high_order_damped_tma(so):
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
     assert rel(outs[0][0], go["grad"]) <= TOL, rel(outs[0][0], go["grad"])
     assert abs(outs[0][1] - go["J"]) <= 1e-4 * go["J"]
+    # adjoint source records: GPU forward snapshots + GRAD-mode adjoint driven by the
+    # oracle's residual, vs the oracle's srca (and gradient), both variants bitwise
+    sr = []
+    for variant in (2, 1):
+        prop = make_prop(p)
+        prop.set_tuning(variant, 0, 0)
+        _, _, snaps = prop.forward(dev(p.wavelet), save_every=2)
+        srca, _, g = prop.adjoint(dev(go["res"]), snaps=snaps, save_every=2,
+                                  grad=torch.zeros(p.shape, device="cuda"))
+        torch.cuda.synchronize()
+        sr.append((srca.cpu().numpy(), g.cpu().numpy()))
+        prop.close()
+    assert np.array_equal(sr[0][0], sr[1][0]) and np.array_equal(sr[0][1], sr[1][1])
+    assert rel(sr[0][0], go["srca"]) <= TOL, rel(sr[0][0], go["srca"])
+    assert rel(sr[0][1], go["grad"]) <= TOL

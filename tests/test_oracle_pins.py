@@ -351,9 +351,22 @@ def _taylor_problem():
     return base, m0, mt, eta
 
 
-def test_taylor_gradient_fp64():
+def _taylor_prob(base, m0, eta, **kw):
+    """The Taylor setup as a synth.Problem, so the test goes through oracle.gradient."""
+    b = dict(base, **kw)
+    return synth.Problem("taylor", 2, b["shape"], b["h"], b["space_order"], b["nt"], b["dt"],
+                         m0, eta, np.asarray(b["src_coords"]), np.asarray(b["wavelet"]),
+                         np.asarray(b["rec_coords"]))
+
+
+@pytest.mark.parametrize("checkpoint", [0, 7])
+def test_taylor_gradient_fp64(checkpoint):
     """J(m0 + e dm) - J(m0) = O(e) and - e <g, dm> leaves O(e^2): ratios of successive
-    residuals as e halves are ~2 and ~4 ([1.9, 2.1] and [3.6, 4.4]) (north_star)."""
+    residuals as e halves are ~2 and ~4 ([1.9, 2.1] and [3.6, 4.4]) (north_star).
+    g and J(m0) come from oracle.gradient itself (plain and checkpoint-recompute), so
+    its residual sign (d_syn - d_obs) and J = 1/2 sum res^2 are pinned: a flipped
+    residual flips <g, dm> (first-order ratio -> ~1), a dropped 1/2 breaks both ratios.
+    J(m0 + e dm) is formed here from the oracle's forward record alone."""
     base, m0, mt, eta = _taylor_problem()
     d_obs = oracle.forward(m=mt, damp=eta, **base)["rec"]
 
@@ -361,13 +374,9 @@ def test_taylor_gradient_fp64():
         r = oracle.forward(m=m, damp=eta, **base)["rec"] - d_obs
         return 0.5 * np.sum(r * r)
 
-    fw = oracle.forward(m=m0, damp=eta, save_every=1, **base)
-    res = fw["rec"] - d_obs
-    ad = oracle.adjoint(m=m0, damp=eta, res=res, save_every=1, snaps=fw["snaps"],
-                        **{k: v for k, v in base.items() if k != "wavelet"})
-    g = ad["grad"]
+    out = oracle.gradient(_taylor_prob(base, m0, eta), d_obs, save_every=1, checkpoint=checkpoint)
+    g, J0 = out["grad"], out["J"]
     dm = mt - m0
-    J0 = 0.5 * np.sum(res * res)
     gd = np.sum(g * dm)
     r1, r2 = [], []
     for e in (0.1, 0.05, 0.025, 0.0125):
@@ -378,6 +387,36 @@ def test_taylor_gradient_fp64():
     q2 = [r2[i] / r2[i + 1] for i in range(3)]
     assert all(1.9 <= q <= 2.1 for q in q1), q1
     assert all(3.6 <= q <= 4.4 for q in q2), q2
+
+
+@pytest.mark.parametrize("k,S,nt", [(1, 7, 60), (4, 8, 61), (4, 16, 49), (3, 300, 40), (2, 2, 30)])
+def test_gradient_checkpoint_recompute_bitwise_2d(k, S, nt):
+    """checkpoint-recompute gives the stored-snapshot gradient, record,
+    J and adjoint source record bit for bit (ragged last window, S > nt, S = k)."""
+    base, m0, mt, eta = _taylor_problem()
+    base = dict(base, nt=nt, wavelet=base["wavelet"][:nt])
+    d_obs = oracle.forward(m=mt, damp=eta, **base)["rec"]
+    pr = _taylor_prob(base, m0, eta)
+    a = oracle.gradient(pr, d_obs, save_every=k)
+    b = oracle.gradient(pr, d_obs, save_every=k, checkpoint=S)
+    assert np.linalg.norm(a["grad"]) > 0
+    for key in ("grad", "d_syn", "res", "srca"):
+        assert np.array_equal(a[key], b[key]), key
+    assert a["J"] == b["J"]
+
+
+def test_gradient_checkpoint_recompute_bitwise_3d_fp16():
+    """Same in 3D with damping, several sources and fp16 snapshots (reading C23)."""
+    p = synth.random_problem(3, (16, 18, 20), 8, 41, seed=3, nbl=3, nsrc=2, nrec=12)
+    d_obs = oracle.forward(p, m=(p.m * 0.9).astype(np.float32))["rec"]
+    for dt_ in (None, "float16"):
+        a = oracle.gradient(p, d_obs, save_every=3, snap_dtype=dt_)
+        b = oracle.gradient(p, d_obs, save_every=3, snap_dtype=dt_, checkpoint=9)
+        for key in ("grad", "d_syn", "srca"):
+            assert np.array_equal(a[key], b[key]), (key, dt_)
+        assert a["J"] == b["J"]
+    with pytest.raises(ValueError):
+        oracle.gradient(p, d_obs, save_every=3, checkpoint=10)
 
 
 def test_gradient_subsampled_consistent():
@@ -396,8 +435,9 @@ def test_gradient_subsampled_consistent():
 
 
 def test_gradient_identity_from_stored_levels():
-    """Gradient identity (SURVEY 8(c) pins; north_star "g += v u_tt"): the oracle's fused
-    correlation (in-register S plus the injection patch, C13) equals the plain definitions
+    """Gradient identity (SURVEY 8(c) pins; north_star "g += v u_tt"): the oracle's
+    correlation (formed in its adjoint loop from the stored u^n and the three v levels
+    it holds, C13) equals the plain definitions
     written out on stored levels,
         g = -sum_{n=1}^{nt-1} u^n (v^{n+1} - 2 v^n + v^{n-1}) / dt^2
           = -sum_{n=0}^{nt-1} v^n (u^{n+1} - 2 u^n + u^{n-1}) / dt^2   (summation by parts,
