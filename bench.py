@@ -121,7 +121,9 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- workload
-def build_problem(nt_override=None, rank=0, nranks=1, cfg=1):
+def build_problem(nt_override=None, rank=0, nranks=1, cfg=1, strong=False):
+    """(problem, local m, local eta, global shape).  N > 1 splits the grid into x-slabs
+    (configs[1] / configs[3]) or runs one shot per rank (configs[4])."""
     import synth
     if cfg == 4:
         # multi-shot FWI gradient (BASELINE configs[4], P:592-596): one shot per rank on the
@@ -131,33 +133,108 @@ def build_problem(nt_override=None, rank=0, nranks=1, cfg=1):
     p = synth.make_config(cfg, nt=nt_override)
     if nranks == 1:
         return p, p.m, p.damp, p.shape
-    if cfg != 1:
-        raise SystemExit("multi-GPU bench runs configs[1] weak-scaled (slab decomposition) "
-                         "or configs[4] (one shot per GPU + gradient all-reduce)")
-    # weak scaling: global grid (336 N) x 336 x 336 = the configs[1] model tiled along x
-    # (its physical part is x-invariant); the absorbing layer stays at the global x edges.
+    if cfg not in (1, 3):
+        raise SystemExit("multi-GPU bench: configs[1] / configs[3] slab-decomposed (weak, or --strong "
+                         "for configs[3]) or configs[4] (one shot per GPU + gradient all-reduce)")
+    spec = slab_spec(p, nranks, strong)
+    x0, n0_loc = slab_range(spec, rank, nranks)
     r = p.space_order // 2
-    n0 = p.shape[0]
-    gshape = (n0 * nranks,) + p.shape[1:]
+    m_loc = spec["m_planes"](x0 - r, x0 + n0_loc + r)
+    eta_loc = spec["eta_planes"](x0 - r, x0 + n0_loc + r)
+    return spec["p"], m_loc, eta_loc, spec["gshape"]
+
+
+def slab_range(spec, rank, nranks):
+    import paper_1707_03776_b200 as sf
+    return sf.slab_plan(spec["gshape"][0], spec["p"].space_order, rank, nranks)
+
+
+def slab_spec(p, nranks, strong):
+    """Global slab problem: configs[1] / configs[3] tiled along x (weak: 336 N / 1024 N planes;
+    both models are x-invariant, so the tiling is exact) or, --strong, configs[3] as given.
+    Returns the global problem (sources / receivers moved to the global geometry) and
+    functions giving the model / damping of a plane range [lo, hi) as host fp32 arrays
+    (planes outside the grid replicate the edge: halo planes of m / eta are unused)."""
     import synth as S
-    vmax = 2500.0
-    # damping of the global grid from its per-axis profiles (reading C7), evaluated on this
-    # rank's planes only (no global 3D array per rank)
-    p.sigma = S.damping_profiles_1d(gshape, p.nbl, p.h, vmax)
-    x0 = rank * n0
-    lo, hi = x0 - r, x0 + n0 + r
-    idx = np.clip(np.arange(lo, hi), 0, gshape[0] - 1)
-    m_col = p.m[0]  # every x-plane of the padded configs[1] model is identical
-    m_loc = np.ascontiguousarray(np.broadcast_to(m_col, (hi - lo,) + p.shape[1:]), dtype=np.float32)
-    sx, sy, sz = (a.astype(np.float64) for a in p.sigma)
-    sig_loc = sx[idx][:, None, None] + sy[None, :, None] + sz[None, None, :]
-    eta_loc = (m_loc.astype(np.float64) * sig_loc).astype(np.float32)
-    src = p.src_coords.copy()
-    src[:, 0] = gshape[0] * p.h / 2.0
-    rec = p.rec_coords.copy()
-    rec[:, 0] = rec[:, 0] + (nranks - 1) * n0 * p.h / 2.0
-    p.src_coords, p.rec_coords = src, rec
-    return p, m_loc, eta_loc, gshape
+    n0 = p.shape[0]
+    gn0 = n0 if strong else n0 * nranks
+    gshape = (gn0,) + tuple(p.shape[1:])
+    m_col = p.m[0]                        # every x-plane of these models is identical
+    sig = None
+    if p.damp is not None:
+        # damping of the global grid from its per-axis profiles (reading C7), evaluated on
+        # the requested planes only (no global 3D array per rank)
+        vmax = 2500.0                     # configs[1] (the only damped slab config)
+        p.sigma = S.damping_profiles_1d(gshape, p.nbl, p.h, vmax)
+        sig = [a.astype(np.float64) for a in p.sigma]
+
+    def m_planes(lo, hi):
+        return np.ascontiguousarray(np.broadcast_to(m_col, (hi - lo,) + gshape[1:]), dtype=np.float32)
+
+    def eta_planes(lo, hi):
+        if sig is None:
+            return None
+        idx = np.clip(np.arange(lo, hi), 0, gn0 - 1)
+        s3 = sig[0][idx][:, None, None] + sig[1][None, :, None] + sig[2][None, None, :]
+        return (m_planes(lo, hi).astype(np.float64) * s3).astype(np.float32)
+
+    if not strong:
+        src = p.src_coords.copy()
+        src[:, 0] = gn0 * p.h / 2.0 if p.damp is not None else (gn0 - 1) * p.h / 2.0
+        if p.damp is not None:
+            # configs[1]: the 256 x 256 surface grid, centred in the global x extent
+            rec = p.rec_coords.copy()
+            rec[:, 0] = rec[:, 0] + (nranks - 1) * n0 * p.h / 2.0
+        else:
+            # configs[3]: one receiver per plane along x at (y = centre, z = 0) (SURVEY 8.0)
+            rec = np.stack([np.arange(gn0) * p.h, np.full(gn0, p.rec_coords[0, 1]), np.zeros(gn0)],
+                           axis=1).astype(np.float32)
+        p.src_coords, p.rec_coords = src.astype(np.float32), rec
+    return {"p": p, "gshape": gshape, "m_planes": m_planes, "eta_planes": eta_planes}
+
+
+def slab_bitwise_check(args, cfg, comm, rank, world, nt_check=12):
+    """The slab run of a short record (nt_check samples) vs the single-domain run of the SAME
+    global problem on this rank's GPU: the owned planes of both final levels and the summed
+    records must be bitwise equal (reading C18).  Returns the flag agreed over all ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1707_03776_b200 as sf
+    import synth
+    p = synth.make_config(cfg, nt=nt_check)
+    spec = slab_spec(p, world, args.strong)
+    p, gshape = spec["p"], spec["gshape"]
+    r = p.space_order // 2
+    x0, nl = slab_range(spec, rank, world)
+    dev = lambda x: None if x is None else torch.from_numpy(x).cuda()
+    kw = dict(shape=gshape, h=p.h, space_order=p.space_order, nt=p.nt, dt=p.dt,
+              src_coords=p.src_coords, rec_coords=p.rec_coords,
+              sigma=p.sigma if (args.sep and p.damp is not None) else None)
+    sep = kw["sigma"] is not None
+    wav = dev(np.ascontiguousarray(p.wavelet))
+    ps = sf.Propagator(dev(spec["m_planes"](x0 - r, x0 + nl + r)),
+                       None if sep else dev(spec["eta_planes"](x0 - r, x0 + nl + r)),
+                       comm=comm, rank=rank, nranks=world, **kw)
+    if args.p2p:
+        ps.set_option(8, 1)
+    rec_s, u_s, _ = ps.forward(wav)
+    torch.cuda.synchronize()
+    ps.close()
+    dist.all_reduce(rec_s)                  # one owner per receiver row: the sum is exact
+    p1 = sf.Propagator(dev(spec["m_planes"](0, gshape[0])),
+                       None if sep else dev(spec["eta_planes"](0, gshape[0])), **kw)
+    rec_1, u_1, _ = p1.forward(wav)
+    torch.cuda.synchronize()
+    p1.close()
+    ok = bool(torch.equal(rec_s, rec_1)) and bool(torch.equal(u_s[:, r:r + nl], u_1[:, x0:x0 + nl]))
+    del u_1, rec_1, u_s, rec_s
+    torch.cuda.empty_cache()
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return {"bitwise_equal": bool(t.item()), "nt": nt_check,
+            "what": "slab run vs single-domain run of the same global problem on each rank's GPU: "
+                    "owned planes of both final levels + summed records"}
 
 
 WORKLOADS = {
@@ -166,7 +243,7 @@ WORKLOADS = {
        "65536 receivers, 1 source",
     2: "configs[2]: 3D FWI gradient 256^3 phys + nbl 40 -> 336^3, so8, nt=1000, save every 4 "
        "(fwd+save, residual, adjoint+correlation; d_obs from the true model outside the timed region)",
-    3: "configs[3]: 3D acoustic forward 1024x512x512, so16, nt=500, no damping layer, 1 GPU",
+    3: "configs[3]: 3D acoustic forward 1024x512x512, so16, nt=500, no damping layer",
     4: "configs[4]: one shot of the multi-shot FWI gradient, 400^3, so12, nt=1500, save every 3",
 }
 
@@ -194,7 +271,14 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     cfg = args.config
-    p, m_loc, eta_loc, gshape = build_problem(args.nt, rank, world, cfg)
+    comm_info = None
+    if comm is not None:
+        n_c, r_c = sf.nccl_comm_info(comm)
+        comm_info = {"nranks": n_c, "rank": r_c, "ok": n_c == world}
+        log(f"[bench] NCCL communicator: nranks {n_c} (world {world}), rank {r_c}")
+        if n_c != world:
+            raise SystemExit(f"NCCL communicator spans {n_c} ranks, world is {world}")
+    p, m_loc, eta_loc, gshape = build_problem(args.nt, rank, world, cfg, args.strong)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
     m_d = dev(m_loc)
     # damping: the eta array (hoisted beta streamed, 20 B/pt) unless --sep regenerates beta
@@ -284,8 +368,11 @@ def run_ours(args):
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sf.nccl_check(comm)
     ms_max = float(t.item())
-    updates = npts_local * world * (p.nt - 1) * args.steps * passes
+    # points updated per step over all ranks: the global grid (slab: the ranks' owned planes
+    # partition it; shots: one full grid per rank)
+    updates = (int(np.prod(gshape)) if slab else npts_local * world) * (p.nt - 1) * args.steps * passes
     value = updates / (ms_max * 1e-3) / 1e9
 
     # roofline of the dominant kernel (stencil step): algorithmic bytes per launch
@@ -307,6 +394,13 @@ def run_ours(args):
     peak, peak_src = peaks()
     traffic, traffic_rel = ncu_traffic(cfg)
 
+    check = None
+    if slab and not args.no_check:
+        del u, rec
+        prop.close()
+        torch.cuda.empty_cache()
+        check = slab_bitwise_check(args, cfg, comm, rank, world)
+        log(f"[bench] slab check: {check}")
     result = None
     if rank == 0:
         # end to end through the public C-ABI with HOST buffers (pinned), N=1 form
@@ -321,11 +415,12 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
             "step_ms": {"median": round(statistics.median(step_ms), 3), "best": round(min(step_ms), 3),
                         "rank0_all": [round(x, 3) for x in step_ms]},
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if (slab and args.strong) else "weak",
+            "vs_baseline": None, "dtype": "f32",
             "data": f"synthetic (seeded {p.name} model of BASELINE configs[{cfg}], readings of "
                     "SURVEY 8.0; no dataset in the paper)",
-            "config": {"workload": WORKLOADS[cfg] + (f" (weak-scaled: {'x'.join(map(str, gshape))} "
-                                                     f"global, slab per GPU)" if slab else
+            "config": {"workload": WORKLOADS[cfg] + (f" ({'strong' if args.strong else 'weak'}-scaled: "
+                                                     f"{'x'.join(map(str, gshape))} global, x-slab per GPU)" if slab else
                                                      f" (weak-scaled: {world} shots, one per GPU, gradient "
                                                      f"all-reduce in every step)" if world > 1 else ""),
                        "grid": list(gshape), "space_order": p.space_order, "nt": p.nt,
@@ -362,6 +457,8 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": int(prof["launches"]),
             "clocks": clocks,
+            "comm": comm_info,
+            "slab_check": check,
         }
     if world > 1:
         dist.barrier()
@@ -480,6 +577,11 @@ def main():
     ap.add_argument("--snap-half", action="store_true",
                     help="gradient configs: fp16 snapshots (SF_OPT_SNAP_HALF, reading C23)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1, --config 3: split the literal 1024x512x512 grid over the GPUs "
+                         "(strong scaling) instead of 1024 planes per GPU (weak)")
+    ap.add_argument("--no-check", action="store_true",
+                    help="N > 1 slab runs: skip the bitwise slab-vs-single-domain check after the timed region")
     ap.add_argument("--sep", action="store_true",
                     help="damped configs: regenerate beta in-kernel from the separable damping "
                          "profiles (16 B/pt) instead of streaming the hoisted beta array (20 B/pt)")

@@ -246,6 +246,16 @@ SF_API sf_status sf_slab_halo_plan(int64_t n0, int space_order, int rank, int nr
 SF_API sf_status sf_nccl_unique_id(char id_out[128]);
 SF_API sf_status sf_nccl_comm_init(const char id[128], int nranks, int rank, void **comm_out);
 SF_API sf_status sf_nccl_comm_destroy(void *comm);
+/* Size and rank of an NCCL communicator (ncclCommCount / ncclCommUserRank), e.g. for a
+ * harness to verify the communicator spans every rank.  SF_ERR_NCCL on failure. */
+SF_API sf_status sf_nccl_comm_info(void *comm, int *nranks, int *rank);
+/* Asynchronous-error poll (ncclCommGetAsyncError, non-blocking): SF_ERR_NCCL with the NCCL
+ * message if the communicator has failed (a peer died, a link fault, ...).  The library also
+ * polls after every NCCL enqueue it makes (halo exchange, record / gradient all-reduce), so a
+ * failed exchange surfaces as SF_ERR_NCCL from the next sf_forward / sf_adjoint /
+ * sf_gradient / sf_allreduce_gradient call instead of a hang being the only symptom.
+ * An in-process group (sf_local_group_create) always reports SF_OK. */
+SF_API sf_status sf_nccl_check(void *comm);
 
 /* In-process transport (testing the slab path on ONE device): ranks are threads of one
  * process, each with its own handle and stream; a group created here is passed as the

@@ -25,7 +25,8 @@ EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint
            "sf_gradient_workspace_bytes", "sf_gradient", "sf_gradient_ckpt_workspace_bytes",
            "sf_gradient_ckpt", "sf_forward_host", "sf_set_profiling",
            "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
-           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_create_slab",
+           "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_nccl_comm_info",
+           "sf_nccl_check", "sf_create_slab",
            "sf_allreduce_gradient", "sf_local_group_create", "sf_local_group_destroy",
            "sf_convection2d", "sf_laplace2d", "sf_last_error", "sf_version"]
 
@@ -91,6 +92,8 @@ def lib():
             "sf_nccl_unique_id": [P],
             "sf_nccl_comm_init": [P, I, I, P],
             "sf_nccl_comm_destroy": [P],
+            "sf_nccl_comm_info": [P, P, P],
+            "sf_nccl_check": [P],
             "sf_create_slab": [P, P, I, I, P],
             "sf_allreduce_gradient": [P, P, P, Z, P, I, P],
             "sf_local_group_create": [I, P],

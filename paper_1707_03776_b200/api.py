@@ -82,6 +82,19 @@ def nccl_comm_destroy(comm: int):
     check(lib().sf_nccl_comm_destroy(ctypes.c_void_p(comm)))
 
 
+def nccl_comm_info(comm: int):
+    """sf_nccl_comm_info: (nranks, rank) of an NCCL communicator."""
+    n, r = ctypes.c_int(), ctypes.c_int()
+    check(lib().sf_nccl_comm_info(ctypes.c_void_p(comm), ctypes.byref(n), ctypes.byref(r)))
+    return n.value, r.value
+
+
+def nccl_check(comm: int):
+    """sf_nccl_check: raises SfError(SF_ERR_NCCL) if the communicator reported an
+    asynchronous error."""
+    check(lib().sf_nccl_check(ctypes.c_void_p(comm)))
+
+
 def _ondev(fn):
     """Run a Propagator method with the handle's device current: the library allocates,
     launches and creates streams on the current device."""

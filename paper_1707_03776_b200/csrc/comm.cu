@@ -35,6 +35,9 @@ struct NcclApi {
     decltype(&ncclAllReduce) AllReduce = nullptr;
     decltype(&ncclAllGather) AllGather = nullptr;
     decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    decltype(&ncclCommGetAsyncError) CommGetAsyncError = nullptr;
+    decltype(&ncclCommCount) CommCount = nullptr;
+    decltype(&ncclCommUserRank) CommUserRank = nullptr;
     bool ok = false;
 };
 
@@ -60,9 +63,13 @@ NcclApi &api()
         SF_SYM(AllReduce);
         SF_SYM(AllGather);
         SF_SYM(GetErrorString);
+        SF_SYM(CommGetAsyncError);
+        SF_SYM(CommCount);
+        SF_SYM(CommUserRank);
 #undef SF_SYM
         a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv &&
-               a.GroupStart && a.GroupEnd && a.AllReduce && a.AllGather && a.GetErrorString;
+               a.GroupStart && a.GroupEnd && a.AllReduce && a.AllGather && a.GetErrorString &&
+               a.CommGetAsyncError && a.CommCount && a.CommUserRank;
     });
     return a;
 }
@@ -106,6 +113,39 @@ extern "C" sf_status sf_nccl_comm_init(const char id[128], int nranks, int rank,
     ncclComm_t c = nullptr;
     SF_NCCL_TRY(api().CommInitRank(&c, nranks, uid, rank));
     *comm_out = c;
+    return SF_OK;
+}
+
+// Asynchronous NCCL errors (a peer died, a network/NVLink fault, ...) are not returned by
+// the enqueue calls: poll the communicator (non-blocking) and surface them as SF_ERR_NCCL.
+// Called after every NCCL enqueue of the library; ncclInProgress (a non-blocking
+// communicator still initialising) is not an error.
+sf_status sf_comm_check_async(void *comm)
+{
+    if (!comm || sf_comm_is_local(comm) || !api().ok) return SF_OK;
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = api().CommGetAsyncError(static_cast<ncclComm_t>(comm), &ar);
+    if (r != ncclSuccess) return nccl_err("ncclCommGetAsyncError", r);
+    if (ar != ncclSuccess && ar != ncclInProgress) return nccl_err("asynchronous NCCL error", ar);
+    return SF_OK;
+}
+
+extern "C" sf_status sf_nccl_check(void *comm)
+{
+    if (!comm) return sf_set_error(SF_ERR_INVALID_ARG, "comm is NULL");
+    return sf_comm_check_async(comm);
+}
+
+extern "C" sf_status sf_nccl_comm_info(void *comm, int *nranks, int *rank)
+{
+    sf_status s = need_nccl();
+    if (s) return s;
+    if (!comm) return sf_set_error(SF_ERR_INVALID_ARG, "comm is NULL");
+    int n = 0, r = 0;
+    SF_NCCL_TRY(api().CommCount(static_cast<ncclComm_t>(comm), &n));
+    SF_NCCL_TRY(api().CommUserRank(static_cast<ncclComm_t>(comm), &r));
+    if (nranks) *nranks = n;
+    if (rank) *rank = r;
     return SF_OK;
 }
 
@@ -282,7 +322,7 @@ sf_status sf_comm_halo_exchange(sf_handle *h, float *buf, cudaStream_t st)
     SF_NCCL_TRY(api().GroupEnd());
     h->n_all++;
     h->n_kind[3]++;
-    return SF_OK;
+    return sf_comm_check_async(h->comm);
 }
 
 sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st, int rank)
@@ -291,7 +331,7 @@ sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream
     sf_status s = need_nccl();
     if (s) return s;
     SF_NCCL_TRY(api().AllReduce(buf, buf, count, ncclFloat, ncclSum, static_cast<ncclComm_t>(comm), st));
-    return SF_OK;
+    return sf_comm_check_async(comm);
 }
 
 sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st, int rank)
@@ -300,7 +340,7 @@ sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStrea
     sf_status s = need_nccl();
     if (s) return s;
     SF_NCCL_TRY(api().AllReduce(buf, buf, count, ncclDouble, ncclSum, static_cast<ncclComm_t>(comm), st));
-    return SF_OK;
+    return sf_comm_check_async(comm);
 }
 
 extern "C" sf_status sf_allreduce_gradient(sf_handle *h, void *comm, float *grad, size_t count,

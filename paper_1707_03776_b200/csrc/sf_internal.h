@@ -139,3 +139,4 @@ sf_status sf_comm_p2p_local_step(sf_handle *h, cudaStream_t st, bool left, bool 
 sf_status sf_comm_allreduce_f32(void *comm, float *buf, size_t count, cudaStream_t st, int rank);
 sf_status sf_comm_allreduce_f64(void *comm, double *buf, size_t count, cudaStream_t st, int rank);
 bool sf_comm_is_local(void *comm);
+sf_status sf_comm_check_async(void *comm);

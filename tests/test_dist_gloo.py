@@ -227,3 +227,67 @@ def test_bench_multishot_ranks_get_distinct_shots():
         assert g == g0 and d is None
         assert np.array_equal(m, m0)
         assert np.array_equal(p.rec_coords, p0.rec_coords)
+
+
+def _c3_worker(rank, world, port, strong, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        sys.path.insert(0, ROOT)
+        import bench
+        p, m_loc, eta_loc, gshape = bench.build_problem(nt_override=4, rank=rank, nranks=world, cfg=3,
+                                                        strong=strong)
+        import paper_1707_03776_b200 as sf
+        r = p.space_order // 2
+        x0, nl = sf.slab_plan(gshape[0], p.space_order, rank, world)
+        assert m_loc.shape == (nl + 2 * r,) + tuple(gshape[1:]) and eta_loc is None
+        # fingerprint of the owned planes: the z profile of every owned plane (the model is
+        # x-invariant) and the planes' global indices
+        prof = torch.from_numpy(m_loc[r:r + nl, 7, :].astype(np.float64).copy())
+        idx = torch.arange(x0, x0 + nl, dtype=torch.int64)
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([nl]))
+        mx = int(max(s.item() for s in sizes))
+        pad = lambda t, fill: torch.cat([t, torch.full((mx - t.shape[0],) + t.shape[1:], fill, dtype=t.dtype)])
+        profs = [torch.zeros((mx, gshape[2]), dtype=torch.float64) for _ in range(world)]
+        idxs = [torch.zeros(mx, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(profs, pad(prof, -1.0))
+        dist.all_gather(idxs, pad(idx, -1))
+        if rank == 0:
+            q.put((gshape, [int(s.item()) for s in sizes], [t.numpy() for t in profs], [t.numpy() for t in idxs],
+                   p.src_coords.copy(), p.rec_coords.copy(), p.h))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("strong", [False, True])
+def test_bench_config3_slabs_gloo(strong):
+    """bench.py --gpus 2 --config 3 [--strong] (BASELINE configs[3], run at 1/2/4/8 GPUs):
+    two gloo ranks build their slabs with bench.build_problem; gathered, the owned planes
+    cover the global grid exactly once in order (weak: 1024 N planes, strong: the literal
+    1024), every plane carries the configs[3] layered profile, the source sits at the global
+    centre and the receivers are one per global plane along x."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c3_worker, args=(r, world, port, strong, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    gshape, sizes, profs, idxs, src, rec, h = out
+    ref = synth.make_config(3, nt=4)
+    assert gshape == ((1024,) if strong else (1024 * world,)) + (512, 512)
+    assert sum(sizes) == gshape[0]
+    allidx = np.concatenate([i[:n] for i, n in zip(idxs, sizes)])
+    assert np.array_equal(allidx, np.arange(gshape[0]))
+    zprof = ref.m[0, 7, :].astype(np.float64)
+    for pr_, n in zip(profs, sizes):
+        assert np.array_equal(pr_[:n], np.broadcast_to(zprof, (n, gshape[2])))
+    assert np.isclose(src[0, 0], (gshape[0] - 1) * h / 2.0)
+    assert rec.shape[0] == gshape[0] and np.array_equal(rec[:, 0], np.arange(gshape[0]) * np.float32(h))
