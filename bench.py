@@ -299,6 +299,8 @@ def run_ours(args):
         prop.set_option(8, 1)   # peer-store halo exchange instead of NCCL send/recv
     if args.snap_half:
         prop.set_option(7, 1)
+    if args.no_plane:
+        prop.set_option(10, 0)  # SF_OPT_PLANE_INJ off: standalone injection kernel
     wav = dev(p.wavelet)
     u = prop.zeros_state()
     rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
@@ -500,6 +502,22 @@ def run_e2e(p, args, sep=False):
                         "(coefficient hoist, tables, CFL), forward, D2H record"}
 
 
+def host_cpu():
+    """CPU model of this host (/proc/cpuinfo) and the OpenMP thread setting the oracle ran
+    with (record nproc, the CPU model and OMP_NUM_THREADS)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.lower().startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS", "unset (OpenMP default: all cores)")}
+
+
 def cpu_baseline(p, seconds):
     """The oracle as it stands (fp64, OpenMP over all host cores) on a bounded sample:
     the same grid and model, first `k` time steps, k sized to ~`seconds` of CPU work."""
@@ -519,7 +537,7 @@ def cpu_baseline(p, seconds):
     oracle.forward(p, nt=k, wavelet=p.wavelet[:k])
     t = time.perf_counter() - t0
     return {"value": round(N * (k - 1) / t / 1e9, 5), "unit": UNIT, "cores": oracle.num_threads(),
-            "kind": "oracle", "seconds": round(t, 2),
+            "kind": "oracle", "seconds": round(t, 2), **host_cpu(),
             "sample": f"{p.name}: full {'x'.join(map(str, p.shape))} grid, first {k} of {p.nt} time "
                       f"samples ({k - 1} forward updates), fp64 C oracle"}
 
@@ -547,7 +565,7 @@ def run_reference(args):
     v = N * (k - 1) * args.steps / t / 1e9
     sample = f"{p.name}: full {'x'.join(map(str, p.shape))} grid, {k} of {p.nt} time samples per step"
     cpu = {"value": round(v, 5), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-           "sample": sample}
+           "sample": sample, **host_cpu()}
     return {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t / args.steps * 1e3, 1), "higher_is_better": True,
@@ -577,6 +595,9 @@ def main():
     ap.add_argument("--snap-half", action="store_true",
                     help="gradient configs: fp16 snapshots (SF_OPT_SNAP_HALF, reading C23)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-plane", action="store_true",
+                    help="inject receiver surfaces with the standalone kernel instead of inside the "
+                         "stencil kernel (SF_OPT_PLANE_INJ 0; A/B of the adjoint)")
     ap.add_argument("--strong", action="store_true",
                     help="N > 1, --config 3: split the literal 1024x512x512 grid over the GPUs "
                          "(strong scaling) instead of 1024 planes per GPU (weak)")

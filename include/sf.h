@@ -218,6 +218,14 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   lanes); sources are then injected by the standalone kernel.
                                   Bitwise the same.  (Lower orders run at the HBM roofline, where
                                   the extra launch costs more than the idle lanes.)             */
+#define SF_OPT_PLANE_INJ 10    /* 3D TMA kernel, space order <= 12: 1 (default) injects a large point
+                                  set (> SF_OPT_FUSE_MAX targets) inside the stencil kernel when
+                                  every target lies on one z index and gets one contribution --
+                                  receivers on the nodes of a surface (configs[1..4]) -- from a
+                                  dense [n0][n1] table built at sf_create (point, coefficient),
+                                  its loads issued two planes ahead.  Replaces the standalone
+                                  injection kernel between two stencil steps; bitwise the same.
+                                  0: standalone kernel.                                           */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */

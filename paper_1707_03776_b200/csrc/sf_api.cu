@@ -460,9 +460,18 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         if (zrem && (s = build_maps(nmaps, NARROW_TZ, NARROW_BY))) return s;
     }
     L.maps = &maps;
-    // fuse only small point sets (a few shots' sources): large sets (receiver grids) would
-    // put dependent table loads on the stencil's critical path -> standalone kernels.  Not
-    // with the z split (the fused lists index the 128-column tiles only)
+    // large point sets on one z index (receiver surfaces): plane injection in the kernel, its
+    // dense-table loads pipelined two planes ahead (any mode, also across the z split)
+    if (L.variant == SF_VAR_TMA && h->plane_inj && h->r <= 6 && b.inj && b.inj->pl_tab && b.inj_vals &&
+        b.inj->ntgt > h->fuse_max) {
+        a.pl_tab = b.inj->pl_tab;
+        a.pl_vals = b.inj_vals;
+        a.pl_z = b.inj->pl_z;
+        *fused = true;
+    } else
+    // fuse only small point sets (a few shots' sources) as lists: large ones (receiver grids)
+    // would put dependent table loads on the stencil's critical path.  Not with the z split
+    // (the fused lists index the 128-column tiles only)
     if (L.variant == SF_VAR_TMA && !zrem && mode != SF_MODE_GRAD && b.inj && b.inj->ntgt > 0 &&
         b.inj->ntgt <= h->fuse_max && b.inj_vals) {
         sf_status s = ensure_inj_tiles(h, *b.inj, L.vy);
@@ -548,6 +557,7 @@ static void free_sparse(SfSparse &s)
     cudaFree(s.ej_coef);
     cudaFree(s.jl_bnd);
     cudaFree(s.jl_int);
+    cudaFree(s.pl_tab);
     s = SfSparse{};
 }
 
@@ -712,6 +722,22 @@ static sf_status commit_sparse(sf_handle *h, const SparsePlan &pl, const float *
                                                           out.ej_pt, out.ej_coef);
             SF_CUDA_TRY(cudaGetLastError());
             SF_CUDA_TRY(cudaDeviceSynchronize());
+        }
+        // plane-injection table: every target on one z index with one contribution
+        // (receivers on the nodes of a surface); only for sets the kernel would not fuse
+        // anyway as a list, and only where the TMA kernel carries the plane path (r <= 6)
+        bool plane = h->ndim == 3 && kmax == 1 && h->r <= 6 && !pl.tgt.empty();
+        const int64_t n2 = h->nb[2];
+        for (size_t t = 0; plane && t < pl.tgt.size(); ++t) plane = (pl.tgt[t] % n2) == (pl.tgt[0] % n2);
+        if (plane) {
+            const size_t rows = (size_t)h->nb[0] * (size_t)h->nb[1];
+            SF_CUDA_TRY(cudaMalloc(&out.pl_tab, sizeof(int2) * rows));
+            SF_CUDA_TRY(cudaMemset(out.pl_tab, 0xff, sizeof(int2) * rows));  // point -1: no target
+            k_plane_table<<<(out.ntgt + 255) / 256, 256>>>(out.j_tgt, out.ej_pt, out.ej_coef, out.ntgt, n2,
+                                                           out.pl_tab);
+            SF_CUDA_TRY(cudaGetLastError());
+            SF_CUDA_TRY(cudaDeviceSynchronize());
+            out.pl_z = (int)(pl.tgt[0] % n2);
         }
     }
     out.ik = pl.K;
@@ -1073,6 +1099,10 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         return SF_OK;
     case SF_OPT_ZSPLIT:
         h->zsplit = value != 0;
+        drop_graphs(h);
+        return SF_OK;
+    case SF_OPT_PLANE_INJ:
+        h->plane_inj = value != 0;
         drop_graphs(h);
         return SF_OK;
     case SF_OPT_SNAP_HALF:

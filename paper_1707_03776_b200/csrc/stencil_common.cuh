@@ -9,7 +9,16 @@
 //   X  = sum_{k=1..r} w_k * ( (x_-k + x_+k) - 2 u )
 //   Lap = P + X,  w_k = fp32(w_k^exact / h^2)
 // so that a constant field is annihilated exactly (4u and 2u are exact) and the fp32
-// weights never need to sum to zero.  Update (the paper's solve(), with a
+// weights never need to sum to zero.
+//
+// 3D, r <= 4 ("combined form", SF_CF): one chain over the three axes,
+//   Lap = sum_{k=1..r} w_k * ( (((y_-k + y_+k) + (z_-k + z_+k)) + (x_-k + x_+k)) + (-6u) ),
+//   -6u = fl(-6 u) formed once per point
+// -- 7 FP operations per radius instead of 8 (the TMA kernel unrolls its plane loop for
+// r <= 4, so the x neighbours are at hand next to the in-plane ones).  Still exact on a
+// constant field: ((2u + 2u) + 2u) rounds exactly like 6u, so every term is fl(6u) - fl(6u)
+// = 0 (same fp32 accuracy as the per-axis form).  Every 3D variant (TMA,
+// generic, slab boundary launches) uses the form its radius selects, so all agree bitwise.  Update (the paper's solve(), with a
 // centred u.dt, reading C1), beta/c3 hoisted per point at setup:
 //   out = u + beta (u - old) + c3 * Lap
 // Gradient term formed in-register (reading C13/C14; north_star "g += v u_tt"):
@@ -28,6 +37,20 @@ struct SfWeights {
 enum SfMode { SF_MODE_PLAIN = 0, SF_MODE_SAVE = 1, SF_MODE_GRAD = 2 };
 // damping representation: none (beta = 1), hoisted beta array, separable profiles
 enum SfDampMode { SF_DAMP_NONE = 0, SF_DAMP_ARRAY = 1, SF_DAMP_SEP = 2 };
+
+// 3D radii that use the combined form (SF_CF_MAXR: override for A/B builds only; must be
+// <= 4, the radii whose TMA plane loop is unrolled)
+#ifndef SF_CF_MAXR
+#define SF_CF_MAXR 4
+#endif
+#define SF_CF(R) ((R) <= SF_CF_MAXR)
+
+// combined-form term at radius k: (((ym + yp) + (zm + zp)) + (xm + xp)) + nu6, nu6 = fl(-6u)
+__device__ __forceinline__ float sf_cf_term(float ym, float yp, float zm, float zp, float xm, float xp,
+                                            float nu6)
+{
+    return __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(ym, yp), __fadd_rn(zm, zp)), __fadd_rn(xm, xp)), nu6);
+}
 
 // in-plane term at radius k for 3D: ((ym + yp) + (zm + zp)) - 4u, as one fma
 __device__ __forceinline__ float sf_inplane3(float ym, float yp, float zm, float zp, float u)
@@ -171,4 +194,14 @@ struct SfStepArgs {
     // out[t] += sum coef vals.  (Records are interpolated by a separate kernel.)
     const int *inj_beg, *inj_q, *inj_lj, *inj_t, *inj_rowptr, *inj_pt;
     const float *inj_coef, *inj_vals;
+    // Plane injection (TMA kernel, r <= 6; NULL pl_tab = none): every target of a large point
+    // set lies on the one z index pl_z and has a single contribution (receivers on the grid
+    // nodes of a surface).  pl_tab[x n1 + y] = {point, float bits of its coefficient}, point
+    // -1 where (x, y, pl_z) is not a target.  The lane owning column pl_z adds
+    // delta = fma(coef, pl_vals[point], 0) to its value before the store (and the save /
+    // gradient patches of k_inject_ell, bitwise), with the table and value loads issued two
+    // and one planes ahead so that no dependent load sits on the critical path.
+    const int2 *pl_tab;
+    const float *pl_vals;
+    int pl_z;
 };

@@ -32,6 +32,7 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <type_traits>
+#include <utility>
 #include "stencil_common.cuh"
 
 #ifndef SF_DC_MIN
@@ -57,6 +58,7 @@
 #endif
 
 namespace sftma {
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -252,6 +254,33 @@ __device__ __forceinline__ float hi2(f2_t v)
     return b;
 }
 
+// element e (runtime, 0 <= e < 2 NJ) of a row of fp32 pairs
+template <int NJ>
+__device__ __forceinline__ float get_el(const f2_t (&v)[NJ], int e)
+{
+    float r = 0.0f;
+#pragma unroll
+    for (int jp = 0; jp < NJ; ++jp) {
+        float lo, hi;
+        upk2(v[jp], lo, hi);
+        r = (e == 2 * jp) ? lo : r;
+        r = (e == 2 * jp + 1) ? hi : r;
+    }
+    return r;
+}
+template <int NJ>
+__device__ __forceinline__ void set_el(f2_t (&v)[NJ], int e, float x)
+{
+#pragma unroll
+    for (int jp = 0; jp < NJ; ++jp) {
+        float lo, hi;
+        upk2(v[jp], lo, hi);
+        lo = (e == 2 * jp) ? x : lo;
+        hi = (e == 2 * jp + 1) ? x : hi;
+        v[jp] = pk2(lo, hi);
+    }
+}
+
 // fp32x2 form of sf_beta_sep: sxy = sx + sy (both lanes), sz = the lanes' sigma_z
 __device__ __forceinline__ f2_t beta_sep2(f2_t sxy, f2_t sz, f2_t hdt2, f2_t one2, f2_t m1)
 {
@@ -428,7 +457,10 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
     for (int k = 1; k <= R; ++k) Wk[k] = pk2(a.w.w[k], a.w.w[k]);
     Wk[0] = 0ull;
-    const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f);
+    const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f), M6 = pk2(-6.f, -6.f);
+    // combined Laplacian form (stencil_common.cuh, sf_lap_cf): radii up to 4, where the plane
+    // loop is unrolled and the x queue can be read next to the in-plane neighbours
+    constexpr bool CMB = SF_CF(R);
     const f2_t NG = pk2(-a.gscale, -a.gscale), ONE2 = pk2(1.f, 1.f);
     const f2_t HDT2 = pk2(a.hdt, a.hdt);
     constexpr int QINF = 0x7fffffff;
@@ -462,6 +494,21 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
         for (int j = 0; j < VY; ++j) act[j] = zact && (yg + j < a.n1);
         const int qa = (int)sg.qa, qb = (int)sg.qb;
+        // plane injection (SfStepArgs::pl_tab): this lane owns column pl_z of its rows (element
+        // pe).  Pipeline over output planes: plane q applies (pC0, pV0), plane q + 1 has its
+        // coefficient and value load in flight (pC1, pV1), plane q + 2 its table load (pT2).
+        constexpr bool PLANE = (R <= 6);
+        const int pe = (PLANE && a.pl_tab) ? a.pl_z - zg : -1;
+        const bool plo = pe >= 0 && pe < VZ;
+        int2 pT2[VY];
+        int pR0[VY], pR1[VY];
+        float pC0[VY], pV0[VY], pC1[VY], pV1[VY];
+#pragma unroll
+        for (int j = 0; j < VY; ++j) {
+            pT2[j] = make_int2(-1, 0);
+            pR0[j] = pR1[j] = -1;
+            pC0[j] = pV0[j] = pC1[j] = pV1[j] = 0.0f;
+        }
         const int NP = (qb - qa) + 2 * R;
         float *optr = a.out + (int64_t)qa * plane + (int64_t)yg * a.n2 + zg;
         // snapshot row pointer (element offsets as the output; with fp16 snapshots it only
@@ -496,11 +543,28 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                     if (UNR == Q) sl = s2;
                     const int p = qa - R + i;
                     const bool outp = (i >= 2 * R);
+                    if (PLANE && plo) {
+                        // advance the plane-injection pipeline (output plane p - R)
+                        const int q2 = p - R + 2;
+#pragma unroll
+                        for (int j = 0; j < VY; ++j) {
+                            pR0[j] = pR1[j];
+                            pC0[j] = pC1[j];
+                            pV0[j] = pV1[j];
+                            pR1[j] = pT2[j].x;
+                            pC1[j] = __int_as_float(pT2[j].y);
+                            pV1[j] = pR1[j] >= 0 ? __ldg(a.pl_vals + pR1[j]) : 0.0f;
+                            pT2[j] = (q2 >= qa && q2 < qb && yg + j < a.n1)
+                                         ? __ldg(a.pl_tab + (int64_t)q2 * a.n1 + yg + j)
+                                         : make_int2(-1, 0);
+                        }
+                    }
                     // separable damping: sigma_x of the output plane q = p - R (issued early)
                     const float sxq = (DM == SF_DAMP_SEP && outp) ? __ldg(a.sigx + (p - R)) : 0.0f;
                     // ---- (1) in-plane partial of output plane q = p - R: its u tile is
                     // resident (arrived R planes ago), so this overlaps the wait for plane p
                     f2_t Pin[VY][NJ], Uq[VY][NJ];
+                    f2_t S4R[VY][NJ], NU6[VY][NJ];  // CMB: radius-R in-plane pair sums, -6u
                     if (outp) {
                         const float *uq = ubase + uo * UF;
                         // y rows rown - R .. rown + VY - 1 + R (own rows included)
@@ -526,6 +590,34 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                 ldp<VZ>(uq + own_off + j * W + VZ + VZ * c, ZR[j] + NJ * c);
                             }
                         }
+                        // CMB (r <= 4, unrolled loop): the combined form (stencil_common.cuh)
+                        //   t_k = (((y-k + y+k) + (z-k + z+k)) + (x-k + x+k)) + (-6u),  L = sum_k w_k t_k
+                        // -- radii 1..R-1 now, radius R (x+R = plane p, still in flight) after
+                        // the wait.  The x pair sums come from the register queue through a
+                        // slot switch that folds away in the unrolled loop.  Otherwise the
+                        // in-plane partial P = sum_k w_k (((y-k + y+k) + (z-k + z+k)) - 4u).
+                        constexpr int KX = (CMB && R > 1) ? R - 1 : 1;
+                        f2_t XS[VY][NJ][KX];
+                        if constexpr (CMB) {
+                            auto xpairs = [&](auto ic) {
+                                constexpr int SQ = (decltype(ic)::value - R + Q) % Q;  // slot of plane q
+#pragma unroll
+                                for (int j = 0; j < VY; ++j)
+#pragma unroll
+                                    for (int jp = 0; jp < NJ; ++jp)
+#pragma unroll
+                                        for (int k = 1; k < R; ++k)
+                                            XS[j][jp][k - 1] = add2(V[(SQ - k + Q) % Q][j][jp], V[(SQ + k) % Q][j][jp]);
+                            };
+                            switch (sl) {
+#define SF_XP(S_) \
+    case S_:      \
+        if constexpr (S_ < Q) xpairs(std::integral_constant<int, S_>{}); \
+        break;
+                                SF_XP(0) SF_XP(1) SF_XP(2) SF_XP(3) SF_XP(4) SF_XP(5) SF_XP(6) SF_XP(7) SF_XP(8)
+#undef SF_XP
+                            }
+                        }
 #pragma unroll
                         for (int j = 0; j < VY; ++j) {
                             // float at z offset e (relative to the own first column) of row j
@@ -549,7 +641,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                             for (int jp = 0; jp < NJ; ++jp) {
                                 const f2_t u = Uq[j][jp];
-                                // radius ascending (== sf_inplane3 per lane)
+                                if (CMB) NU6[j][jp] = mul2(M6, u);
+                                // radius ascending
                                 f2_t P = 0ull;
 #pragma unroll
                                 for (int k = 1; k <= R; ++k) {
@@ -560,7 +653,12 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                         zs = pk2(__fadd_rn(F(em), F(ep)), __fadd_rn(F(em + 1), F(ep + 1)));
                                     else
                                         zs = add2(PZ(em), PZ(ep));
-                                    P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
+                                    if (CMB) {
+                                        if (k < R) P = fma2(Wk[k], add2(add2(add2(ys, zs), XS[j][jp][k < R ? k - 1 : 0]), NU6[j][jp]), P);
+                                        else S4R[j][jp] = add2(ys, zs);
+                                    } else {
+                                        P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);  // == sf_inplane3
+                                    }
                                 }
                                 Pin[j][jp] = P;
                             }
@@ -578,7 +676,16 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             SF_CHK(ut + own_off + j * W, ut, ut + W * C::H);
                             ldp<VZ>(ut + own_off + j * W, V[S][j]);
                         }
-                        if (outp) {
+                        if (outp && CMB) {
+                            // radius R of the combined form: L = fma(w_R, ((s4_R + (x-R + x+R)) - 6u), L)
+#pragma unroll
+                            for (int j = 0; j < VY; ++j)
+#pragma unroll
+                                for (int jp = 0; jp < NJ; ++jp) {
+                                    const f2_t xs = add2(V[(SQ - R + Q) % Q][j][jp], V[S][j][jp]);
+                                    X[j][jp] = fma2(Wk[R], add2(add2(S4R[j][jp], xs), NU6[j][jp]), Pin[j][jp]);
+                                }
+                        } else if (outp) {
 #pragma unroll
                             for (int j = 0; j < VY; ++j)
 #pragma unroll
@@ -661,7 +768,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                             for (int jp = 0; jp < NJ; ++jp) {
                                 const f2_t u = Uq[j][jp];
-                                const f2_t lap = add2(Pin[j][jp], X[j][jp]);
+                                const f2_t lap = CMB ? X[j][jp] : add2(Pin[j][jp], X[j][jp]);
                                 // out = u + beta (u - old) + c3 lap   (== sf_update per lane)
                                 const f2_t d = fma2(M1, ov[j][jp], u);
                                 res2[j][jp] = fma2(cv[j][jp], lap, fma2(bv[j][jp], d, u));
@@ -683,6 +790,21 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                         if (++cs == DC) {
                             cs = 0;
                             cph ^= 1u;
+                        }
+                        if (PLANE && plo) {
+                            // plane injection: the operations of
+                            // k_inject_ell for a one-contribution target, bitwise
+#pragma unroll
+                            for (int j = 0; j < VY; ++j) {
+                                if (pR0[j] >= 0) {
+                                    const float d = (pC0[j] != 0.0f) ? __fmaf_rn(pC0[j], pV0[j], 0.0f) : 0.0f;
+                                    set_el<NJ>(res2[j], pe, __fadd_rn(get_el<NJ>(res2[j], pe), d));
+                                    if (MODE == SF_MODE_GRAD)
+                                        set_el<NJ>(gres2[j], pe,
+                                                   __fmaf_rn(-a.gscale, __fmul_rn(get_el<NJ>(sv[j], pe), d),
+                                                             get_el<NJ>(gres2[j], pe)));
+                                }
+                            }
                         }
                         if (MODE != SF_MODE_GRAD && cq == q) {
                             // fused injection, rare path: res[t] += sum_e coef_e vals[pt_e]

@@ -1020,3 +1020,121 @@ def test_gradient_high_order_damped_tma(so):
     assert np.array_equal(sr[0][0], sr[1][0]) and np.array_equal(sr[0][1], sr[1][1])
     assert rel(sr[0][0], go["srca"]) <= TOL, rel(sr[0][0], go["srca"])
     assert rel(sr[0][1], go["grad"]) <= TOL
+
+
+# ------------------------------------------------------------------- plane injection
+def _surface_problem(shape, so, nt, zs, seed, nbl=4, damp=True):
+    """Receivers on every grid node of the plane z = zs inside an absorbing ring (> 256
+    targets, one contribution each: the plane-injection case), one off-node source."""
+    p = synth.random_problem(3, shape, so, nt, seed=seed, nbl=nbl if damp else 0, nsrc=1, nrec=4,
+                             damp=damp)
+    h = p.h
+    lo = nbl + 1 if damp else 1
+    ii, jj = np.meshgrid(np.arange(lo, shape[0] - lo), np.arange(lo, shape[1] - lo), indexing="ij")
+    p.rec_coords = np.stack([ii.ravel() * h, jj.ravel() * h, np.full(ii.size, zs * h)], 1).astype(np.float32)
+    return p
+
+
+@pytest.mark.parametrize("shape,so,zs,damp", [((30, 44, 64), 8, 9, True), ((26, 30, 144), 12, 7, False),
+                                              ((26, 30, 144), 12, 135, False), ((22, 26, 132), 4, 131, True)])
+def test_plane_injection_adjoint_gradient(shape, so, zs, damp):
+    """Adjoint injection of a receiver surface (every node of z = zs) inside the TMA kernel
+    (SF_OPT_PLANE_INJ, the one-contribution dense table pipelined two planes ahead): the
+    adjoint source records, final levels and the fused gradient (GRAD mode: the injected
+    increment's correlation patch) are bitwise those of the standalone injection kernel
+    (option off) and of the generic kernel, and match the oracle.  Covers r = 4 (unrolled
+    loop) and r = 6 with the narrow-tile z split (zs in the 128-column tiles and in the
+    remainder), ragged tiles and the last z column."""
+    p = _surface_problem(shape, so, 50, zs, seed=41, damp=damp)
+    nrec = p.rec_coords.shape[0]
+    assert nrec > 256
+    rng = np.random.default_rng(2)
+    p.m_true = (p.m * rng.uniform(0.9, 1.1, p.m.shape)).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    go = oracle.gradient(p, d_obs, save_every=2)
+    outs = []
+    for variant, plane in ((2, 1), (2, 0), (1, 1)):
+        prop = make_prop(p)
+        prop.set_tuning(variant, 0, 0)
+        prop.set_option(sf().SF_OPT_PLANE_INJ, plane)
+        _, _, snaps = prop.forward(dev(p.wavelet), save_every=2)
+        srca, v, g = prop.adjoint(dev(go["res"]), snaps=snaps, save_every=2,
+                                  grad=torch.zeros(p.shape, device="cuda"))
+        srca0, v0, _ = prop.adjoint(dev(go["res"]))          # PLAIN-mode adjoint
+        gg, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
+        torch.cuda.synchronize()
+        outs.append([x.cpu().numpy() for x in (srca, v, g, srca0, v0, gg)] + [J])
+        prop.close()
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+    assert rel(outs[0][0], go["srca"]) <= TOL
+    assert rel(outs[0][2], go["grad"]) <= TOL and rel(outs[0][5], go["grad"]) <= TOL
+    assert abs(outs[0][6] - go["J"]) <= 1e-4 * go["J"]
+
+
+def test_plane_injection_forward_save_sources():
+    """Forward injection of a large SOURCE surface (300+ sources on the nodes of z = 5) in
+    SAVE mode: the snapshots hold the post-injection values, bitwise equal between the
+    plane path, the standalone kernel and the generic kernel, and the records match the
+    oracle."""
+    p = synth.random_problem(3, (24, 28, 64), 8, 40, seed=5, nbl=3, nsrc=1, nrec=6)
+    h = p.h
+    ii, jj = np.meshgrid(np.arange(4, 20), np.arange(4, 24), indexing="ij")
+    p.src_coords = np.stack([ii.ravel() * h, jj.ravel() * h, np.full(ii.size, 5 * h)], 1).astype(np.float32)
+    ns = p.src_coords.shape[0]
+    p.wavelet = np.random.default_rng(3).standard_normal((p.nt, ns)).astype(np.float32)
+    ro, uo, so_ = oracle_forward(p, save_every=3)
+    outs = []
+    for variant, plane in ((2, 1), (2, 0), (1, 1)):
+        prop = make_prop(p)
+        prop.set_tuning(variant, 0, 0)
+        prop.set_option(sf().SF_OPT_PLANE_INJ, plane)
+        rec, u, snaps = prop.forward(dev(p.wavelet), save_every=3)
+        torch.cuda.synchronize()
+        outs.append((rec.cpu().numpy(), u.cpu().numpy(), snaps.cpu().numpy()))
+        prop.close()
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+    assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
+    for k in range(1, so_.shape[0]):
+        assert rel(outs[0][2][k], so_[k]) <= TOL
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_plane_injection_slab_bitwise(nranks):
+    """Slab path (split boundary / interior TMA launches, local transport) with a receiver
+    surface injected by the plane path in both launches: gradient, J and the owned planes
+    bitwise equal to the single-domain run."""
+    S = sf()
+    p = _surface_problem((41, 30, 64), 8, 40, 9, seed=44)
+    p.m_true = (p.m * 0.93).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    prop = make_prop(p)
+    g1, J1 = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+    torch.cuda.synchronize()
+    g1 = g1.cpu().numpy()
+    prop.close()
+    group = S.local_group_create(nranks)
+    r = p.space_order // 2
+
+    def rank_fn(rank):
+        x0, nl, m, eta = _slab_inputs(p, rank, nranks)
+        pr = S.Propagator(dev(m), None if eta is None else dev(eta), shape=p.shape, h=p.h,
+                          space_order=p.space_order, nt=p.nt, dt=p.dt,
+                          src_coords=p.src_coords.astype(np.float64),
+                          rec_coords=p.rec_coords.astype(np.float64), comm=group, rank=rank, nranks=nranks)
+        g, J = pr.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+        torch.cuda.current_stream().synchronize()
+        res = (x0, nl, g.cpu().numpy()[r:r + nl], J)
+        pr.close()
+        return res
+
+    try:
+        outs = _run_ranks(nranks, rank_fn)
+    finally:
+        S.local_group_destroy(group)
+    for x0, nl, g, J in outs:
+        assert np.array_equal(g, g1[x0:x0 + nl]), (x0, nl)
+        assert J == J1
