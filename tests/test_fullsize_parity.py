@@ -129,15 +129,28 @@ def _gradient_case(ci, shot=0):
     del g, d_obs_g
     torch.cuda.empty_cache()
     t1 = time.time()
-    # oracle: its own d_obs, checkpointed gradient
-    d_obs_o = oracle.forward(p, m=p.m_true)["rec"]
-    S = ckpt_segment(p.nt, k)
-    go = oracle.gradient(p, d_obs_o, save_every=k, checkpoint=S)
-    t2 = time.time()
+    exp_dir = os.path.join(os.environ.get("SF_EXPECTED_DIR", "gpurun_data"), f"c{ci}")
+    meta_path = os.path.join(exp_dir, "meta.json")
+    if os.path.exists(meta_path):
+        # the oracle's outputs written beforehand by scripts/oracle_expected.py (oracle/ only:
+        # its runtime exceeds one GPU-box call); d_obs and grad stored rounded to fp32
+        with open(meta_path) as f:
+            meta = json.load(f)
+        assert (meta["shape"], meta["nt"], meta["save_every"], meta["shot"]) == (list(p.shape), p.nt, k, shot)
+        d_obs_o = np.load(os.path.join(exp_dir, "d_obs.npy")).astype(np.float64)
+        go = {"grad": np.load(os.path.join(exp_dir, "grad.npy")), "J": meta["J"]}
+        S, rres, src = meta["checkpoint_segment"], meta["rel_residual"], "scripts/oracle_expected.py"
+        t2 = t1 + meta["d_obs_s"] + meta["gradient_s"]
+    else:
+        # oracle: its own d_obs, checkpointed gradient
+        d_obs_o = oracle.forward(p, m=p.m_true)["rec"]
+        S = ckpt_segment(p.nt, k)
+        go = oracle.gradient(p, d_obs_o, save_every=k, checkpoint=S)
+        rres, src = float(np.linalg.norm(go["res"]) / np.linalg.norm(d_obs_o)), "in-process"
+        t2 = time.time()
     out = {"kind": "gradient", "shape": list(p.shape), "space_order": p.space_order, "nt": p.nt,
-           "save_every": k, "checkpoint_segment": S, "shot": shot, "tuning": tun,
-           "d_obs": trace_stats(dg, d_obs_o), "d_syn_oracle_rel_residual":
-               float(np.linalg.norm(go["res"]) / np.linalg.norm(d_obs_o)),
+           "save_every": k, "checkpoint_segment": S, "shot": shot, "tuning": tun, "oracle_run": src,
+           "d_obs": trace_stats(dg, d_obs_o), "d_syn_oracle_rel_residual": rres,
            "grad_rel_l2": rel(gg, go["grad"]), "J_gpu": J, "J_oracle": go["J"],
            "J_rel_err": abs(J - go["J"]) / go["J"], "gpu_s": t1 - t0, "oracle_s": t2 - t1}
     _dump(ci, out)
