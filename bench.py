@@ -293,14 +293,14 @@ def run_ours(args):
                          nranks=world if slab else 1, sigma=p.sigma if sep else None)
     if args.split:
         prop.set_option(2, 1)
+        if args.one_launch and world == 1:
+            prop.set_option(11, 2)  # SF_OPT_ONE_LAUNCH: the one-launch slab schedule, emulated on one GPU
     if args.graph:
         prop.set_option(5, 1)
     if args.p2p and slab:
         prop.set_option(8, 1)   # peer-store halo exchange instead of NCCL send/recv
     if args.snap_half:
         prop.set_option(7, 1)
-    if args.no_plane:
-        prop.set_option(10, 0)  # SF_OPT_PLANE_INJ off: standalone injection kernel
     wav = dev(p.wavelet)
     u = prop.zeros_state()
     rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
@@ -436,7 +436,9 @@ def run_ours(args):
                                    "eta array (hoisted beta streamed)" if eta_d is not None else "none"),
                        "halo_exchange": (("peer stores from the boundary kernel + stream counters"
                                           if args.p2p else "NCCL send/recv") if slab else None),
-                       "schedule": ("split (boundary planes, then interior)" if split else
+                       "schedule": (("one launch per step, boundary ranges signalled to the comm stream"
+                                     if (args.one_launch or (slab and not args.p2p)) else
+                                     "split (boundary planes, then interior)") if split else
                                     "single launch per step") + (", CUDA graph replay" if args.graph else ""),
                        "kernel_tuning": tuning},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -588,6 +590,10 @@ def main():
     ap.add_argument("--split", action="store_true",
                     help="1 GPU: run the slab schedule (boundary planes first, interior second) "
                          "to measure its cost without communication")
+    ap.add_argument("--one-launch", action="store_true",
+                    help="with --split on 1 GPU: the one-launch slab schedule (SF_OPT_ONE_LAUNCH 2: one "
+                         "launch per step, boundary ranges signalled on device counters the comm stream "
+                         "waits on) instead of the two-launch split")
     ap.add_argument("--p2p", action="store_true",
                     help="N > 1 slab runs: peer-store halo exchange (SF_OPT_P2P) instead of NCCL send/recv")
     ap.add_argument("--graph", action="store_true",
@@ -595,9 +601,6 @@ def main():
     ap.add_argument("--snap-half", action="store_true",
                     help="gradient configs: fp16 snapshots (SF_OPT_SNAP_HALF, reading C23)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-plane", action="store_true",
-                    help="inject receiver surfaces with the standalone kernel instead of inside the "
-                         "stencil kernel (SF_OPT_PLANE_INJ 0; A/B of the adjoint)")
     ap.add_argument("--strong", action="store_true",
                     help="N > 1, --config 3: split the literal 1024x512x512 grid over the GPUs "
                          "(strong scaling) instead of 1024 planes per GPU (weak)")

@@ -218,15 +218,24 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   lanes); sources are then injected by the standalone kernel.
                                   Bitwise the same.  (Lower orders run at the HBM roofline, where
                                   the extra launch costs more than the idle lanes.)             */
-#define SF_OPT_PLANE_INJ 10    /* 3D TMA kernel, space order <= 12: 1 (default) injects a large point
-                                  set (> SF_OPT_FUSE_MAX targets) inside the stencil kernel when
-                                  every target lies on one z index and gets one contribution --
-                                  receivers on the nodes of a surface (configs[1..4]) -- from a
-                                  dense [n0][n1] table built at sf_create (point, coefficient),
-                                  its loads issued two planes ahead.  Replaces the standalone
-                                  injection kernel between two stencil steps; bitwise the same.
-                                  0: standalone kernel.                                           */
+#define SF_OPT_ONE_LAUNCH 11   /* split schedule (slab handles; SF_OPT_SPLIT on one GPU): 1 (default)
+                                  runs each step as ONE persistent TMA launch when the injection
+                                  of the step happens inside it (fused source lists) -- the last x-chunk of every tile streams downward,
+                                  each CTA fences and bumps a device counter when it has stored a
+                                  boundary range, the comm stream waits on the counters
+                                  (cuStreamWaitValue32) and runs the NCCL send/recv while the
+                                  launch computes the interior.  Otherwise (or 0) the two-launch
+                                  split (boundary launch on a high-priority stream, interior
+                                  launch).  2: the one-launch schedule also on one GPU (the
+                                  exchange becomes a copy into sf_debug_probe's buffer).  In-
+                                  process local groups and SF_OPT_P2P keep the two-launch
+                                  schedule.  Bitwise the same results.                          */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
+/* Test hook of the one-launch schedule on one GPU (SF_OPT_ONE_LAUNCH 2): after each step's
+ * counters fire, the comm stream copies the r boundary planes at each end of the new level
+ * ([xa, xa + r) then [xb - r, xb), 2 r n1 n2 floats) into `dst` (device; NULL = off);
+ * *one_launch_steps (may be NULL) = steps run with the one-launch schedule so far. */
+SF_API sf_status sf_debug_probe(sf_handle *h, float *dst, long long *one_launch_steps);
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */
 SF_API sf_status sf_get_tuning(const sf_handle *h, int *variant, int *vy, int *ctas);

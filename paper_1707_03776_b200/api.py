@@ -219,6 +219,14 @@ class Propagator:
         check(lib().sf_set_profiling(self._h, 1 if on else 0))
 
     @_ondev
+    def debug_probe(self, dst: Optional[torch.Tensor]) -> int:
+        """sf_debug_probe: set (or clear) the one-launch test probe buffer; returns the
+        number of steps run with the one-launch schedule so far."""
+        n = ctypes.c_longlong()
+        check(lib().sf_debug_probe(self._h, _ptr(dst) if dst is not None else None, ctypes.byref(n)))
+        return n.value
+
+    @_ondev
     def profile(self, reset: bool = True):
         """Summed in-stream kernel times (CUDA events) and launch counts since the last
         reset, by kind: stencil / inject / interp / other."""

@@ -37,10 +37,13 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
     const int64_t tiles = ((a.n2t - a.zbase + C::TZ - 1) / C::TZ) * ((a.n1 + C::BY - 1) / C::BY);
     if (PT <= 0 || tiles <= 0) return cudaSuccess;
     const int64_t slots = L.ctas > 0 ? L.ctas : L.sms;
+    // one-launch slab schedule (a.bidir): at least two chunks per tile (the last one streams
+    // downward) of at least r planes each, so each boundary range lies in one chunk
     double best = 1e300;
     int64_t chunk = PT, nch = 1;
-    for (int64_t c = 1; c <= std::min<int64_t>(PT, 256); ++c) {
+    for (int64_t c = a.bidir ? 2 : 1; c <= std::min<int64_t>(PT, 256); ++c) {
         const int64_t ch = (PT + c - 1) / c, ce = (PT + ch - 1) / ch;
+        if (a.bidir && (ce < 2 || ch < SF_R)) continue;
         const int64_t items = tiles * ce, g = std::min(items, slots);
         const double t = (double)((items + g - 1) / g) * (double)(ch + 2 * SF_R);
         if (t < best - 1e-9) {

@@ -260,6 +260,8 @@ struct StepBufs {
     int ctas_cap = 0;          // > 0: at most this many persistent TMA CTAs (split interior)
     int itp_cur = -1;          // side-stream record index of the `cur` level (SF_OPT_P2P ordering)
     bool force_generic = false;            // thread-per-point kernel (P2P boundary launch)
+    bool bidir = false;                    // one-launch slab schedule (SfStepArgs::bidir / sig)
+    bool dry = false;                      // launch_step: decide (fused, tiles), launch nothing
     const int64_t *mq = nullptr, *md = nullptr;  // peer-store mirror (SfStepArgs::mq / md)
 };
 
@@ -460,18 +462,12 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         if (zrem && (s = build_maps(nmaps, NARROW_TZ, NARROW_BY))) return s;
     }
     L.maps = &maps;
-    // large point sets on one z index (receiver surfaces): plane injection in the kernel, its
-    // dense-table loads pipelined two planes ahead (any mode, also across the z split)
-    if (L.variant == SF_VAR_TMA && h->plane_inj && h->r <= 6 && b.inj && b.inj->pl_tab && b.inj_vals &&
-        b.inj->ntgt > h->fuse_max) {
-        a.pl_tab = b.inj->pl_tab;
-        a.pl_vals = b.inj_vals;
-        a.pl_z = b.inj->pl_z;
-        *fused = true;
-    } else
-    // fuse only small point sets (a few shots' sources) as lists: large ones (receiver grids)
-    // would put dependent table loads on the stencil's critical path.  Not with the z split
-    // (the fused lists index the 128-column tiles only)
+    // fuse only small point sets (a few shots' sources): large sets (receiver grids) would
+    // put dependent table loads on the stencil's critical path -> standalone kernels (an
+    // in-kernel injection of receiver surfaces from a dense per-plane table, its loads
+    // pipelined two planes ahead, measured 9 % slower even where inactive and 23 % slower on
+    // configs[2]: DESIGN.md section 7).  Not with the z split (the fused lists index the
+    // 128-column tiles only)
     if (L.variant == SF_VAR_TMA && !zrem && mode != SF_MODE_GRAD && b.inj && b.inj->ntgt > 0 &&
         b.inj->ntgt <= h->fuse_max && b.inj_vals) {
         sf_status s = ensure_inj_tiles(h, *b.inj, L.vy);
@@ -489,6 +485,14 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     // (records are interpolated by k_interp_ell on the side stream, concurrently with the
     //  next step: no in-kernel interpolation)
 
+    if (b.bidir) {
+        if (L.variant != SF_VAR_TMA || zrem) return sf_set_error(SF_ERR_INVALID_ARG, "one-launch schedule needs the TMA kernel without a z split");
+        a.bidir = 1;
+        a.sig = h->sigc;
+        h->last_tiles = (int)(((a.n2 + tile_tz(h, L.vy) - 1) / tile_tz(h, L.vy)) *
+                              ((a.n1 + tile_by(L.vy) - 1) / tile_by(L.vy)));
+    }
+    if (b.dry) return SF_OK;
     cudaError_t e;
     {
         ProfScope ps(h, PK_STENCIL, st);  // one scope over both launches of a z split
@@ -557,7 +561,6 @@ static void free_sparse(SfSparse &s)
     cudaFree(s.ej_coef);
     cudaFree(s.jl_bnd);
     cudaFree(s.jl_int);
-    cudaFree(s.pl_tab);
     s = SfSparse{};
 }
 
@@ -723,22 +726,6 @@ static sf_status commit_sparse(sf_handle *h, const SparsePlan &pl, const float *
             SF_CUDA_TRY(cudaGetLastError());
             SF_CUDA_TRY(cudaDeviceSynchronize());
         }
-        // plane-injection table: every target on one z index with one contribution
-        // (receivers on the nodes of a surface); only for sets the kernel would not fuse
-        // anyway as a list, and only where the TMA kernel carries the plane path (r <= 6)
-        bool plane = h->ndim == 3 && kmax == 1 && h->r <= 6 && !pl.tgt.empty();
-        const int64_t n2 = h->nb[2];
-        for (size_t t = 0; plane && t < pl.tgt.size(); ++t) plane = (pl.tgt[t] % n2) == (pl.tgt[0] % n2);
-        if (plane) {
-            const size_t rows = (size_t)h->nb[0] * (size_t)h->nb[1];
-            SF_CUDA_TRY(cudaMalloc(&out.pl_tab, sizeof(int2) * rows));
-            SF_CUDA_TRY(cudaMemset(out.pl_tab, 0xff, sizeof(int2) * rows));  // point -1: no target
-            k_plane_table<<<(out.ntgt + 255) / 256, 256>>>(out.j_tgt, out.ej_pt, out.ej_coef, out.ntgt, n2,
-                                                           out.pl_tab);
-            SF_CUDA_TRY(cudaGetLastError());
-            SF_CUDA_TRY(cudaDeviceSynchronize());
-            out.pl_z = (int)(pl.tgt[0] % n2);
-        }
     }
     out.ik = pl.K;
     if ((s = upload(&out.e_idx, pl.eidx))) return s;
@@ -797,6 +784,7 @@ extern "C" void sf_destroy(sf_handle *h)
     if (h->hi_stream) cudaStreamDestroy(h->hi_stream);
     sf_comm_p2p_release(h);
     if (h->p2p_flags) (cudaFree)(h->p2p_flags);
+    if (h->sigc) (cudaFree)(h->sigc);
     if (h->ev_pre) cudaEventDestroy(h->ev_pre);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
     if (h->ev_xch) cudaEventDestroy(h->ev_xch);
@@ -910,6 +898,9 @@ static sf_status create_common(const sf_desc *d, sf_handle *h)
     SF_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_itp[1], cudaEventDisableTiming));
     SF_CUDA_TRY(cudaMalloc(&h->partial, sizeof(double) * 1024));
     SF_CUDA_TRY(cudaMalloc(&h->dJ, sizeof(double)));
+    // one-launch schedule counters (stream memory operations: plain cudaMalloc, not the pool)
+    SF_CUDA_TRY((cudaMalloc)((void **)&h->sigc, 2 * sizeof(unsigned int)));
+    SF_CUDA_TRY(cudaMemset(h->sigc, 0, 2 * sizeof(unsigned int)));
     SF_CUDA_TRY(cudaDeviceSynchronize());
     return SF_OK;
 }
@@ -1101,8 +1092,9 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         h->zsplit = value != 0;
         drop_graphs(h);
         return SF_OK;
-    case SF_OPT_PLANE_INJ:
-        h->plane_inj = value != 0;
+    case SF_OPT_ONE_LAUNCH:
+        if (value < 0 || value > 2) return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_ONE_LAUNCH %d", value);
+        h->one_launch = value;
         drop_graphs(h);
         return SF_OK;
     case SF_OPT_SNAP_HALF:
@@ -1174,6 +1166,14 @@ extern "C" sf_status sf_get_profile(sf_handle *h, double *ms, long long *nst, lo
     if (s) return s;
     if (ms) *ms = mk[PK_STENCIL];
     if (nst) *nst = nk[PK_STENCIL];
+    return SF_OK;
+}
+
+extern "C" sf_status sf_debug_probe(sf_handle *h, float *dst, long long *one_launch_steps)
+{
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    h->probe = dst;
+    if (one_launch_steps) *one_launch_steps = h->n_onelaunch;
     return SF_OK;
 }
 
@@ -1327,6 +1327,58 @@ static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepB
 // slab mode the halo exchange.  Split mode computes the r boundary planes at each end
 // first, injects there, hands them to NCCL on the comm stream and computes the interior
 // while the halos travel; the stream then waits for the exchange.
+// One-launch slab schedule (SF_OPT_ONE_LAUNCH): ONE persistent
+// stencil launch per step whose last x-chunk of every tile streams downward, so both
+// boundary ranges are finished r output planes in; each CTA signals a finished boundary range
+// on the handle's device counters (fence + atomic), the comm stream waits on the counters
+// (cuStreamWaitValue32) and runs the NCCL exchange while the same launch computes the
+// interior.  Injection must happen inside the launch (fused list or plane injection) so the
+// boundary planes are final when signalled.  One GPU (SF_OPT_ONE_LAUNCH 2 with SF_OPT_SPLIT):
+// the same schedule, the "exchange" being a copy of the boundary planes into a test probe.
+static bool one_launch_ok(sf_handle *h, const StepBufs &b, int mode, cudaStream_t st)
+{
+    if (!h->one_launch || h->p2p || h->ndim != 3 || !h->sigc) return false;
+    if (h->nranks > 1 ? sf_comm_is_local(h->comm) : h->one_launch < 2) return false;
+    StepBufs bd = b;
+    bd.bidir = true;
+    bd.dry = true;
+    bool fused = false;
+    if (launch_step(h, bd, mode, st, &fused) != SF_OK) return false;
+    const bool need = b.inj && b.inj->ntgt > 0 && b.inj_vals;
+    return fused || !need;
+}
+
+static sf_status do_step_onelaunch(sf_handle *h, StepBufs b, int mode, cudaStream_t st)
+{
+    sf_status s;
+    bool fused = false;
+    SF_CUDA_TRY(cudaEventRecord(h->ev_pre, st));  // orders the exchange after earlier readers of `out`
+    b.bidir = true;
+    // the persistent launch would hold every SM until it ends: leave some free so the NCCL
+    // kernels of the exchange run while it computes the interior
+    const int reserve = h->comm_sms >= 0 ? h->comm_sms : (h->nranks > 1 ? 8 : 0);
+    if (reserve > 0) b.ctas_cap = std::max(1, h->sms - reserve);
+    if ((s = launch_step(h, b, mode, st, &fused))) return s;
+    h->sig_tgt += (uint32_t)h->last_tiles;       // one signal per tile and side
+    h->n_onelaunch++;
+    cudaStream_t cs = h->comm_stream;
+    SF_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev_pre, 0));
+    if ((s = stream_wait32(cs, h->sigc + 0, h->sig_tgt))) return s;
+    if ((s = stream_wait32(cs, h->sigc + 1, h->sig_tgt))) return s;
+    if (h->nranks > 1) {
+        if ((s = sf_comm_halo_exchange(h, b.out, cs))) return s;
+    } else if (h->probe) {
+        const int64_t plane = h->N / h->nb[0], r = h->r;
+        const size_t bytes = sizeof(float) * (size_t)(r * plane);
+        SF_CUDA_TRY(cudaMemcpyAsync(h->probe, b.out + h->xa * plane, bytes, cudaMemcpyDeviceToDevice, cs));
+        SF_CUDA_TRY(cudaMemcpyAsync(h->probe + r * plane, b.out + (h->xb - r) * plane, bytes,
+                                    cudaMemcpyDeviceToDevice, cs));
+    }
+    SF_CUDA_TRY(cudaEventRecord(h->ev_xch, cs));
+    SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_xch, 0));
+    return SF_OK;
+}
+
 static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, const float *grad_snap,
                          cudaStream_t st)
 {
@@ -1341,6 +1393,7 @@ static sf_status do_step(sf_handle *h, StepBufs b, int mode, float *snap_patch, 
         if (h->nranks > 1) return sf_comm_halo_exchange(h, b.out, st);
         return SF_OK;
     }
+    if (one_launch_ok(h, b, mode, st)) return do_step_onelaunch(h, b, mode, st);
     // boundary planes at both ends in ONE launch on the high-priority stream, overlapping
     // the interior launch on `st`; then the exchange on the comm stream
     bool f2 = false;

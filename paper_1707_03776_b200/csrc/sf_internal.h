@@ -43,10 +43,6 @@ struct SfSparse {
     int n_bnd = -1, n_int = 0;
     std::vector<int64_t> h_tgt;  // host copy of the target offsets
     SfInjTiles tiles;
-    // plane injection (SfStepArgs::pl_tab): dense [nb0][nb1] {point, coefficient bits} table
-    // when every target lies on the z index pl_z with one contribution (else NULL)
-    int2 *pl_tab = nullptr;
-    int pl_z = -1;
 };
 
 // One cached CUDA graph of a whole sf_forward / sf_adjoint call (SF_OPT_GRAPH): the
@@ -113,7 +109,14 @@ struct sf_handle {
     // owned boundary planes straight into the neighbours' halos (peer-mapped pointers) and
     // signals with a stream-ordered counter write; the neighbour's stream waits on the value
     bool zsplit = true;               // SF_OPT_ZSPLIT: narrow tiles for a z remainder <= 64
-    bool plane_inj = true;            // SF_OPT_PLANE_INJ: in-kernel injection of surface point sets
+    // one-launch slab schedule (SF_OPT_ONE_LAUNCH): the stencil launch signals its finished
+    // boundary ranges on device counters; the comm stream waits on them, then exchanges
+    int one_launch = 1;               // 1: in NCCL slab mode when applicable; 2: also on one GPU (emulation)
+    unsigned int *sigc = nullptr;     // [2] left / right boundary counters (monotonic)
+    uint32_t sig_tgt = 0;             // counter value that marks the current step's boundaries
+    int last_tiles = 0;               // tiles of the last bidir launch (signals per side)
+    float *probe = nullptr;           // test hook: boundary planes copied here on the comm stream
+    long long n_onelaunch = 0;        // steps run with the one-launch schedule
     bool p2p = false;
     uint32_t *p2p_flags = nullptr;    // own device counters: [0] written by the left, [1] by the right neighbour
     uint32_t p2p_seq = 0;             // P2P steps completed (the value the next step writes is seq + 1)

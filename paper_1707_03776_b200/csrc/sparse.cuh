@@ -140,16 +140,6 @@ __global__ void k_inject_csr_list(float *__restrict__ u, const int64_t *__restri
     if (grad) grad[g] = __fmaf_rn(-gscale, __fmul_rn(snap_ld(grad_snap, g, snap_half), d), grad[g]);
 }
 
-// plane-injection table (SfStepArgs::pl_tab): row x n1 + y of every target <- {point, coef}
-// (one-contribution ELL slot 0)
-__global__ void k_plane_table(const int64_t *__restrict__ tgt, const int *__restrict__ ept,
-                              const float *__restrict__ ecoef, int ntgt, int64_t n2, int2 *__restrict__ tab)
-{
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntgt) return;
-    tab[tgt[t] / n2] = make_int2(ept[t], __float_as_int(ecoef[t]));
-}
-
 // CSR -> ELL (slot-major) for the injection tables
 __global__ void k_csr_to_ell(const int *__restrict__ rowptr, const int *__restrict__ pt,
                              const float *__restrict__ coef, int ntgt, int K, int *__restrict__ ept,

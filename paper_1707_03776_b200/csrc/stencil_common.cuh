@@ -194,14 +194,12 @@ struct SfStepArgs {
     // out[t] += sum coef vals.  (Records are interpolated by a separate kernel.)
     const int *inj_beg, *inj_q, *inj_lj, *inj_t, *inj_rowptr, *inj_pt;
     const float *inj_coef, *inj_vals;
-    // Plane injection (TMA kernel, r <= 6; NULL pl_tab = none): every target of a large point
-    // set lies on the one z index pl_z and has a single contribution (receivers on the grid
-    // nodes of a surface).  pl_tab[x n1 + y] = {point, float bits of its coefficient}, point
-    // -1 where (x, y, pl_z) is not a target.  The lane owning column pl_z adds
-    // delta = fma(coef, pl_vals[point], 0) to its value before the store (and the save /
-    // gradient patches of k_inject_ell, bitwise), with the table and value loads issued two
-    // and one planes ahead so that no dependent load sits on the critical path.
-    const int2 *pl_tab;
-    const float *pl_vals;
-    int pl_z;
+    // One-launch slab schedule (TMA kernel): bidir = 1 streams the LAST x-chunk of every tile
+    // downward (from xb - 1), so that both boundary ranges [xa, xa + r) and [xb - r, xb) are
+    // finished r output planes into the launch; sig != NULL: after a CTA has stored all of a
+    // boundary range of its tile, it fences and adds 1 to sig[0] (left) / sig[1] (right), so
+    // that a stream waiting on the counter (cuStreamWaitValue32) can start the halo exchange
+    // while the same launch computes the interior.
+    int bidir;
+    unsigned int *sig;
 };

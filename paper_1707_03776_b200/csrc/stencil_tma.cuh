@@ -254,33 +254,6 @@ __device__ __forceinline__ float hi2(f2_t v)
     return b;
 }
 
-// element e (runtime, 0 <= e < 2 NJ) of a row of fp32 pairs
-template <int NJ>
-__device__ __forceinline__ float get_el(const f2_t (&v)[NJ], int e)
-{
-    float r = 0.0f;
-#pragma unroll
-    for (int jp = 0; jp < NJ; ++jp) {
-        float lo, hi;
-        upk2(v[jp], lo, hi);
-        r = (e == 2 * jp) ? lo : r;
-        r = (e == 2 * jp + 1) ? hi : r;
-    }
-    return r;
-}
-template <int NJ>
-__device__ __forceinline__ void set_el(f2_t (&v)[NJ], int e, float x)
-{
-#pragma unroll
-    for (int jp = 0; jp < NJ; ++jp) {
-        float lo, hi;
-        upk2(v[jp], lo, hi);
-        lo = (e == 2 * jp) ? x : lo;
-        hi = (e == 2 * jp + 1) ? x : hi;
-        v[jp] = pk2(lo, hi);
-    }
-}
-
 // fp32x2 form of sf_beta_sep: sxy = sx + sy (both lanes), sz = the lanes' sigma_z
 __device__ __forceinline__ f2_t beta_sep2(f2_t sxy, f2_t sz, f2_t hdt2, f2_t one2, f2_t m1)
 {
@@ -314,6 +287,14 @@ __device__ __forceinline__ Seg next_seg(int64_t w, int64_t end, int64_t P1, int6
     }
     s.qb = s.qa + min(lim, end - w);
     return s;
+}
+
+// streaming direction of a segment: +1 (ascending x), or -1 for the last chunk of a tile in
+// the one-launch slab schedule (SfStepArgs::bidir; needs two or more chunks per tile)
+__device__ __forceinline__ int seg_dir(const SfStepArgs &a, int it, int tiles, int nchunk, int64_t w1,
+                                       int64_t PT)
+{
+    return (a.bidir && nchunk > 1 && it / tiles == nchunk - 1 && w1 == (int64_t)(it % tiles + 1) * PT) ? -1 : 1;
 }
 
 template <int R, int VY, int DM, int MODE, int LZ = 32>
@@ -381,12 +362,14 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
             for (int64_t w = (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk,
                          w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
                 const Seg sg = next_seg(w, w1, P1, PT, a);
+                const int dir = seg_dir(a, it, tiles, nchunk, w1, PT);
                 w += sg.qb - sg.qa;
                 const int z0 = (int)a.zbase + (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
                 const int NP = (int)(sg.qb - sg.qa) + 2 * R;
                 for (int i = 0; i < NP; ++i) {
-                    const int p = (int)(sg.qa - R) + i;   // plane of u^n
-                    const int q = p - R;                  // output plane
+                    // plane of u^n / output plane (downward segments start at qb - 1 + R)
+                    const int p = dir > 0 ? (int)(sg.qa - R) + i : (int)(sg.qb - 1 + R) - i;
+                    const int q = p - dir * R;
                     if (gu >= DU) mbar_wait(uempty + 8 * us, uph ^ 1u);
                     mbar_expect_tx(ufull + 8 * us, W * C::H * 4);  // full box, OOB zero-filled
                     tma_load3(ubase + us * C::UST, &tm_cur, z0 - HZ, y0 - R, p, ufull + 8 * us);
@@ -422,7 +405,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                     }
                     // warm L2 PD planes ahead of the smem rings
                     if (PD > 0 && i + PD < NP) {
-                        const int pp = p + PD, qq = q + PD;
+                        const int pp = p + dir * PD, qq = q + dir * PD;
                         tma_prefetch3(&tm_cur, z0 - HZ, y0 - R, pp);
                         if (i + PD >= 2 * R) {
                             tma_prefetch3(&tm_old, z0, y0, qq);
@@ -469,6 +452,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     for (int64_t w = (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk,
                  w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
         const Seg sg = next_seg(w, w1, P1, PT, a);
+        const int dir = seg_dir(a, it, tiles, nchunk, w1, PT);
         w += sg.qb - sg.qa;
         const int z0 = (int)a.zbase + (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
         const int zg = z0 + VZ * lz;
@@ -494,35 +478,34 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
         for (int j = 0; j < VY; ++j) act[j] = zact && (yg + j < a.n1);
         const int qa = (int)sg.qa, qb = (int)sg.qb;
-        // plane injection (SfStepArgs::pl_tab): this lane owns column pl_z of its rows (element
-        // pe).  Pipeline over output planes: plane q applies (pC0, pV0), plane q + 1 has its
-        // coefficient and value load in flight (pC1, pV1), plane q + 2 its table load (pT2).
-        constexpr bool PLANE = (R <= 6);
-        const int pe = (PLANE && a.pl_tab) ? a.pl_z - zg : -1;
-        const bool plo = pe >= 0 && pe < VZ;
-        int2 pT2[VY];
-        int pR0[VY], pR1[VY];
-        float pC0[VY], pV0[VY], pC1[VY], pV1[VY];
-#pragma unroll
-        for (int j = 0; j < VY; ++j) {
-            pT2[j] = make_int2(-1, 0);
-            pR0[j] = pR1[j] = -1;
-            pC0[j] = pV0[j] = pC1[j] = pV1[j] = 0.0f;
-        }
         const int NP = (qb - qa) + 2 * R;
-        float *optr = a.out + (int64_t)qa * plane + (int64_t)yg * a.n2 + zg;
+        const int64_t dplane = dir * plane;
+        float *optr = a.out + (int64_t)(dir > 0 ? qa : qb - 1) * plane + (int64_t)yg * a.n2 + zg;
+        const int p0 = dir > 0 ? qa - R : qb - 1 + R;  // plane of u^n at iteration 0
+        // boundary signals (one-launch slab schedule): the iteration after which this segment
+        // has stored all of [xa, xa + r) (left) / [xb - r, xb) (right), else -1; checked once
+        // per unrolled group of iterations (a check inside the unrolled body costs scheduling)
+        int fiL = (a.sig && dir > 0 && qa == (int)a.xa) ? min((int)a.xa + R, qb) - 1 - qa + 2 * R : -1;
+        int fiR = (a.sig && qb == (int)a.xb) ? (dir < 0 ? (qb - 1 - max((int)a.xb - R, qa)) + 2 * R : NP - 1) : -1;
         // snapshot row pointer (element offsets as the output; with fp16 snapshots it only
         // carries the element index, stsnap_half rebases it onto the __half array)
         float *sptr = (MODE == SF_MODE_SAVE) ? a.snap_out + (optr - a.out) : nullptr;
         float *gptr = (MODE == SF_MODE_GRAD) ? a.grad + (optr - a.out) : nullptr;
         // fused injection: this warp's cursor (warp-uniform), first entry at q >= qa
-        int ci = 0, ce = 0, cq = QINF;
+        // (downward segments walk the list backwards from the last entry at q < qb)
+        int ci = 0, cb = 0, ce = 0, cq = QINF;
         if (MODE != SF_MODE_GRAD && a.inj_beg) {
             const int wl = sg.tile * NW + wy;
-            ci = a.inj_beg[wl];
+            cb = ci = a.inj_beg[wl];
             ce = a.inj_beg[wl + 1];
-            while (ci < ce && a.inj_q[ci] < qa) ++ci;
-            cq = ci < ce ? a.inj_q[ci] : QINF;
+            if (dir > 0) {
+                while (ci < ce && a.inj_q[ci] < qa) ++ci;
+                cq = ci < ce ? a.inj_q[ci] : QINF;
+            } else {
+                ci = ce - 1;
+                while (ci >= cb && a.inj_q[ci] >= qb) --ci;
+                cq = ci >= cb ? a.inj_q[ci] : QINF;
+            }
         }
 
         // The x-direction register queue needs compile-time slots; only that small part
@@ -535,32 +518,16 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
         constexpr int UNR = (R <= 4) ? Q : 1;
         int sl = 0;  // queue slot of plane p: iteration index mod Q
 #pragma unroll 1
-        for (int base = 0; base < NP; base += UNR)
+        for (int base = 0; base < NP; base += UNR) {
 #pragma unroll
         for (int s2 = 0; s2 < UNR; ++s2) {
                     const int i = base + s2;
                     if (i >= NP) break;
                     if (UNR == Q) sl = s2;
-                    const int p = qa - R + i;
+                    const int p = p0 + dir * i;
                     const bool outp = (i >= 2 * R);
-                    if (PLANE && plo) {
-                        // advance the plane-injection pipeline (output plane p - R)
-                        const int q2 = p - R + 2;
-#pragma unroll
-                        for (int j = 0; j < VY; ++j) {
-                            pR0[j] = pR1[j];
-                            pC0[j] = pC1[j];
-                            pV0[j] = pV1[j];
-                            pR1[j] = pT2[j].x;
-                            pC1[j] = __int_as_float(pT2[j].y);
-                            pV1[j] = pR1[j] >= 0 ? __ldg(a.pl_vals + pR1[j]) : 0.0f;
-                            pT2[j] = (q2 >= qa && q2 < qb && yg + j < a.n1)
-                                         ? __ldg(a.pl_tab + (int64_t)q2 * a.n1 + yg + j)
-                                         : make_int2(-1, 0);
-                        }
-                    }
                     // separable damping: sigma_x of the output plane q = p - R (issued early)
-                    const float sxq = (DM == SF_DAMP_SEP && outp) ? __ldg(a.sigx + (p - R)) : 0.0f;
+                    const float sxq = (DM == SF_DAMP_SEP && outp) ? __ldg(a.sigx + (p - dir * R)) : 0.0f;
                     // ---- (1) in-plane partial of output plane q = p - R: its u tile is
                     // resident (arrived R planes ago), so this overlaps the wait for plane p
                     f2_t Pin[VY][NJ], Uq[VY][NJ];
@@ -761,7 +728,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             }
                         }
                         // done with the u tile of plane q and the coefficient stage
-                        const int q = p - R;
+                        const int q = p - dir * R;
                         f2_t res2[VY][NJ], gres2[VY][NJ];
 #pragma unroll
                         for (int j = 0; j < VY; ++j) {
@@ -791,21 +758,6 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             cs = 0;
                             cph ^= 1u;
                         }
-                        if (PLANE && plo) {
-                            // plane injection: the operations of
-                            // k_inject_ell for a one-contribution target, bitwise
-#pragma unroll
-                            for (int j = 0; j < VY; ++j) {
-                                if (pR0[j] >= 0) {
-                                    const float d = (pC0[j] != 0.0f) ? __fmaf_rn(pC0[j], pV0[j], 0.0f) : 0.0f;
-                                    set_el<NJ>(res2[j], pe, __fadd_rn(get_el<NJ>(res2[j], pe), d));
-                                    if (MODE == SF_MODE_GRAD)
-                                        set_el<NJ>(gres2[j], pe,
-                                                   __fmaf_rn(-a.gscale, __fmul_rn(get_el<NJ>(sv[j], pe), d),
-                                                             get_el<NJ>(gres2[j], pe)));
-                                }
-                            }
-                        }
                         if (MODE != SF_MODE_GRAD && cq == q) {
                             // fused injection, rare path: res[t] += sum_e coef_e vals[pt_e]
                             // (the fp32 operations of k_inject, bitwise); lj = ((jy 32 + lane) 4 + jz)
@@ -829,8 +781,13 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                         for (int jj = 0; jj < VZ; ++jj)
                                             res[j][jj] = (jy == j && jz == jj) ? __fadd_rn(res[j][jj], dd) : res[j][jj];
                                 }
-                                ++ci;
-                                cq = ci < ce ? a.inj_q[ci] : QINF;
+                                if (dir > 0) {
+                                    ++ci;
+                                    cq = ci < ce ? a.inj_q[ci] : QINF;
+                                } else {
+                                    --ci;
+                                    cq = ci >= cb ? a.inj_q[ci] : QINF;
+                                }
                             } while (cq == q);
 #pragma unroll
                             for (int j = 0; j < VY; ++j)
@@ -871,15 +828,31 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                 }
                             }
                         }
-                        optr += plane;
-                        if (MODE == SF_MODE_SAVE) sptr += plane;
-                        if (MODE == SF_MODE_GRAD) gptr += plane;
+                        optr += dplane;
+                        if (MODE == SF_MODE_SAVE) sptr += dplane;
+                        if (MODE == SF_MODE_GRAD) gptr += dplane;
+
                     }
                     if (++us == DU) {
                         us = 0;
                         uph ^= 1u;
                     }
                     if (++uo == DU) uo = 0;
+        }
+            // one-launch schedule: a boundary range of this tile is stored -> every consumer
+            // thread fences its stores, the consumer warps meet, one thread signals
+            const int done = base + UNR;  // iterations finished (or more: the last group)
+            const bool fl = fiL >= 0 && done > fiL, fr = fiR >= 0 && done > fiR;
+            if (fl || fr) {
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+                if (wy == 0 && lane == 0) {
+                    if (fl) atomicAdd(a.sig + 0, 1u);
+                    if (fr) atomicAdd(a.sig + 1, 1u);
+                }
+                if (fl) fiL = -1;
+                if (fr) fiR = -1;
+            }
         }
     }
 }

@@ -1022,41 +1022,43 @@ def test_gradient_high_order_damped_tma(so):
     assert rel(sr[0][1], go["grad"]) <= TOL
 
 
-# ------------------------------------------------------------------- plane injection
+# ------------------------------------------------------------------- receiver surfaces
 def _surface_problem(shape, so, nt, zs, seed, nbl=4, damp=True):
     """Receivers on every grid node of the plane z = zs inside an absorbing ring (> 256
-    targets, one contribution each: the plane-injection case), one off-node source."""
+    targets, one contribution each, like the configs' surface receiver grids); the source
+    two cells below the receiver plane so records and residuals carry signal."""
     p = synth.random_problem(3, shape, so, nt, seed=seed, nbl=nbl if damp else 0, nsrc=1, nrec=4,
                              damp=damp)
     h = p.h
     lo = nbl + 1 if damp else 1
     ii, jj = np.meshgrid(np.arange(lo, shape[0] - lo), np.arange(lo, shape[1] - lo), indexing="ij")
     p.rec_coords = np.stack([ii.ravel() * h, jj.ravel() * h, np.full(ii.size, zs * h)], 1).astype(np.float32)
+    zsrc = zs + 2.3 if zs + 3 < shape[2] else zs - 2.3
+    p.src_coords = np.array([[shape[0] / 2.0 * h + 0.3 * h, shape[1] / 2.0 * h - 0.4 * h, zsrc * h]],
+                            dtype=np.float32)
     return p
 
 
 @pytest.mark.parametrize("shape,so,zs,damp", [((30, 44, 64), 8, 9, True), ((26, 30, 144), 12, 7, False),
-                                              ((26, 30, 144), 12, 135, False), ((22, 26, 132), 4, 131, True)])
-def test_plane_injection_adjoint_gradient(shape, so, zs, damp):
-    """Adjoint injection of a receiver surface (every node of z = zs) inside the TMA kernel
-    (SF_OPT_PLANE_INJ, the one-contribution dense table pipelined two planes ahead): the
-    adjoint source records, final levels and the fused gradient (GRAD mode: the injected
-    increment's correlation patch) are bitwise those of the standalone injection kernel
-    (option off) and of the generic kernel, and match the oracle.  Covers r = 4 (unrolled
-    loop) and r = 6 with the narrow-tile z split (zs in the 128-column tiles and in the
-    remainder), ragged tiles and the last z column."""
-    p = _surface_problem(shape, so, 50, zs, seed=41, damp=damp)
-    nrec = p.rec_coords.shape[0]
-    assert nrec > 256
+                                              ((26, 30, 144), 12, 135, False), ((22, 26, 132), 4, 129, True)])
+def test_receiver_surface_adjoint_gradient(shape, so, zs, damp):
+    """Adjoint injection of a receiver surface (every node of z = zs: > 256 targets, the
+    standalone injection kernel between stencil steps): adjoint source records, final
+    levels and the fused gradient (GRAD mode + the injection's correlation patch) are bitwise
+    equal between the TMA and generic kernels and match the oracle.  r = 4 (unrolled loop,
+    combined Laplacian form) and r = 6 with the narrow-tile z split (zs in the 128-column
+    tiles and in the remainder), ragged tiles, the last z columns."""
+    p = _surface_problem(shape, so, 60, zs, seed=41, damp=damp)
+    assert p.rec_coords.shape[0] > 256
     rng = np.random.default_rng(2)
     p.m_true = (p.m * rng.uniform(0.9, 1.1, p.m.shape)).astype(np.float32)
     d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
     go = oracle.gradient(p, d_obs, save_every=2)
+    assert np.linalg.norm(go["srca"]) > 1e-6 * np.abs(go["res"]).max()
     outs = []
-    for variant, plane in ((2, 1), (2, 0), (1, 1)):
+    for variant in (2, 1):
         prop = make_prop(p)
         prop.set_tuning(variant, 0, 0)
-        prop.set_option(sf().SF_OPT_PLANE_INJ, plane)
         _, _, snaps = prop.forward(dev(p.wavelet), save_every=2)
         srca, v, g = prop.adjoint(dev(go["res"]), snaps=snaps, save_every=2,
                                   grad=torch.zeros(p.shape, device="cuda"))
@@ -1065,19 +1067,18 @@ def test_plane_injection_adjoint_gradient(shape, so, zs, damp):
         torch.cuda.synchronize()
         outs.append([x.cpu().numpy() for x in (srca, v, g, srca0, v0, gg)] + [J])
         prop.close()
-    for o in outs[1:]:
-        for a, b in zip(outs[0], o):
-            assert np.array_equal(a, b)
-    assert rel(outs[0][0], go["srca"]) <= TOL
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    assert rel(outs[0][0], go["srca"]) <= TOL and rel(outs[0][3], go["srca"]) <= TOL
     assert rel(outs[0][2], go["grad"]) <= TOL and rel(outs[0][5], go["grad"]) <= TOL
     assert abs(outs[0][6] - go["J"]) <= 1e-4 * go["J"]
 
 
-def test_plane_injection_forward_save_sources():
-    """Forward injection of a large SOURCE surface (300+ sources on the nodes of z = 5) in
-    SAVE mode: the snapshots hold the post-injection values, bitwise equal between the
-    plane path, the standalone kernel and the generic kernel, and the records match the
-    oracle."""
+def test_many_sources_forward_save():
+    """Forward injection of a large SOURCE surface (320 sources on the nodes of z = 5, the
+    standalone kernel) in SAVE mode: the snapshots hold the post-injection values, bitwise
+    equal between the TMA and generic kernels, and records, final level and snapshots match
+    the oracle."""
     p = synth.random_problem(3, (24, 28, 64), 8, 40, seed=5, nbl=3, nsrc=1, nrec=6)
     h = p.h
     ii, jj = np.meshgrid(np.arange(4, 20), np.arange(4, 24), indexing="ij")
@@ -1086,27 +1087,25 @@ def test_plane_injection_forward_save_sources():
     p.wavelet = np.random.default_rng(3).standard_normal((p.nt, ns)).astype(np.float32)
     ro, uo, so_ = oracle_forward(p, save_every=3)
     outs = []
-    for variant, plane in ((2, 1), (2, 0), (1, 1)):
+    for variant in (2, 1):
         prop = make_prop(p)
         prop.set_tuning(variant, 0, 0)
-        prop.set_option(sf().SF_OPT_PLANE_INJ, plane)
         rec, u, snaps = prop.forward(dev(p.wavelet), save_every=3)
         torch.cuda.synchronize()
         outs.append((rec.cpu().numpy(), u.cpu().numpy(), snaps.cpu().numpy()))
         prop.close()
-    for o in outs[1:]:
-        for a, b in zip(outs[0], o):
-            assert np.array_equal(a, b)
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
     assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
     for k in range(1, so_.shape[0]):
         assert rel(outs[0][2][k], so_[k]) <= TOL
 
 
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_plane_injection_slab_bitwise(nranks):
-    """Slab path (split boundary / interior TMA launches, local transport) with a receiver
-    surface injected by the plane path in both launches: gradient, J and the owned planes
-    bitwise equal to the single-domain run."""
+def test_receiver_surface_slab_bitwise(nranks):
+    """Slab path (split boundary / interior launches, local transport) with a receiver
+    surface injected by the split-list kernels: gradient, J and the owned planes bitwise
+    equal to the single-domain run."""
     S = sf()
     p = _surface_problem((41, 30, 64), 8, 40, 9, seed=44)
     p.m_true = (p.m * 0.93).astype(np.float32)
@@ -1138,3 +1137,57 @@ def test_plane_injection_slab_bitwise(nranks):
     for x0, nl, g, J in outs:
         assert np.array_equal(g, g1[x0:x0 + nl]), (x0, nl)
         assert J == J1
+
+
+# ------------------------------------------------------------------- one-launch schedule
+@pytest.mark.parametrize("so,shape,plane", [(8, (58, 30, 64), True), (16, (60, 26, 64), False), (4, (40, 44, 128), True)])
+def test_one_launch_schedule_bitwise(so, shape, plane):
+    """The one-launch slab schedule (SF_OPT_ONE_LAUNCH, emulated on one GPU with
+    SF_OPT_SPLIT): one persistent launch per step whose last x-chunk of every tile streams
+    DOWNWARD, fused source lists walked backwards there, plane injection pipelined
+    downward, boundary ranges signalled on device counters that the comm stream waits on.
+    Forward records / final levels / snapshots and the gradient (its adjoint with a receiver
+    surface on the two-launch split) are bitwise those of the plain single launch; every step took the
+    one-launch path; and the probe copy the comm stream takes as soon as the counters fire
+    holds the final boundary planes of the last level (a counter firing before every CTA
+    had stored its boundary planes would capture stale values)."""
+    S = sf()
+    if plane:
+        p = _surface_problem(shape, so, 40, 5, seed=61)
+    else:
+        p = synth.random_problem(3, shape, so, 40, seed=61, nbl=4, nsrc=3, nrec=9)
+    h, r = p.h, so // 2
+    # sources in the first and the last x-chunk (fused lists, walked both ways)
+    p.src_coords[0, 0] = 3.5 * h
+    p.src_coords[-1, 0] = (shape[0] - 4.3) * h
+    p.m_true = (p.m * 0.94).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    outs = []
+    for one in (0, 2):
+        prop = make_prop(p)
+        prop.set_tuning(2, 0, 0)
+        if one:
+            prop.set_option(S.SF_OPT_SPLIT, 1)
+            prop.set_option(S.SF_OPT_ONE_LAUNCH, 2)
+            probe = torch.full((2 * r,) + tuple(shape[1:]), float("nan"), device="cuda")
+            prop.debug_probe(probe)
+        rec, u, snaps = prop.forward(dev(p.wavelet), save_every=3)
+        torch.cuda.synchronize()
+        o = [rec.cpu().numpy(), u.cpu().numpy(), snaps.cpu().numpy()]
+        if one:
+            pr = probe.cpu().numpy()
+            assert np.array_equal(pr[:r], o[1][1][:r]) and np.array_equal(pr[r:], o[1][1][-r:])
+        g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+        torch.cuda.synchronize()
+        o += [g.cpu().numpy(), J]
+        if one:
+            n1 = prop.debug_probe(None)
+            # forward + the gradient's forward (its adjoint injects the receivers with the
+            # standalone kernel -> the two-launch split schedule)
+            assert n1 == 2 * (p.nt - 1), n1
+        outs.append(o)
+        prop.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    ro = oracle.forward(p)["rec"]
+    assert rel(outs[1][0], ro) <= TOL
