@@ -13,7 +13,8 @@ import subprocess
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # SF_LIB_PATH: load another build of the same C-ABI (A/B timing of kernel variants only;
 # the tests, smoke() and bench.py use the in-tree build)
-LIB_PATH = os.environ.get("SF_LIB_PATH") or os.path.join(_HERE, "libsf.so")
+_DEFAULT_LIB = os.path.join(_HERE, "libsf.so")
+LIB_PATH = os.environ.get("SF_LIB_PATH") or _DEFAULT_LIB
 CSRC = os.path.join(_HERE, "csrc")
 
 STATUS = {0: "SF_OK", 1: "SF_ERR_INVALID_ARG", 2: "SF_ERR_SHAPE", 3: "SF_ERR_ORDER",
@@ -104,7 +105,13 @@ def lib():
             "sf_local_group_destroy": [P],
         }
         for name, at in sig.items():
-            f = getattr(L, name)
+            try:
+                f = getattr(L, name)
+            except AttributeError:
+                # an A/B build of an older revision (SF_LIB_PATH) may lack newer entry points
+                if LIB_PATH != _DEFAULT_LIB:
+                    continue
+                raise
             f.argtypes = at
             f.restype = ctypes.c_int
         L.sf_destroy.argtypes = [P]

@@ -9,16 +9,11 @@
 //   X  = sum_{k=1..r} w_k * ( (x_-k + x_+k) - 2 u )
 //   Lap = P + X,  w_k = fp32(w_k^exact / h^2)
 // so that a constant field is annihilated exactly (4u and 2u are exact) and the fp32
-// weights never need to sum to zero.
-//
-// 3D, r <= 4 ("combined form", SF_CF): one chain over the three axes,
-//   Lap = sum_{k=1..r} w_k * ( (((y_-k + y_+k) + (z_-k + z_+k)) + (x_-k + x_+k)) + (-6u) ),
-//   -6u = fl(-6 u) formed once per point
-// -- 7 FP operations per radius instead of 8 (the TMA kernel unrolls its plane loop for
-// r <= 4, so the x neighbours are at hand next to the in-plane ones).  Still exact on a
-// constant field: ((2u + 2u) + 2u) rounds exactly like 6u, so every term is fl(6u) - fl(6u)
-// = 0 (same fp32 accuracy as the per-axis form).  Every 3D variant (TMA,
-// generic, slab boundary launches) uses the form its radius selects, so all agree bitwise.  Update (the paper's solve(), with a
+// weights never need to sum to zero.  (A single chain over the three axes with one
+// -fl(6u) term costs 7 instead of 8 FP operations per radius and is also exact on constants,
+// but fl(6u) adds a rounding error per point that the exact 4u / 2u avoid: measured twice the
+// fp32 error, configs[2] gradient 1.9e-4 vs 3.8e-5 -- DESIGN.md section 7.)  Update (the
+// paper's solve(), with a
 // centred u.dt, reading C1), beta/c3 hoisted per point at setup:
 //   out = u + beta (u - old) + c3 * Lap
 // Gradient term formed in-register (reading C13/C14; north_star "g += v u_tt"):
@@ -37,20 +32,6 @@ struct SfWeights {
 enum SfMode { SF_MODE_PLAIN = 0, SF_MODE_SAVE = 1, SF_MODE_GRAD = 2 };
 // damping representation: none (beta = 1), hoisted beta array, separable profiles
 enum SfDampMode { SF_DAMP_NONE = 0, SF_DAMP_ARRAY = 1, SF_DAMP_SEP = 2 };
-
-// 3D radii that use the combined form (SF_CF_MAXR: override for A/B builds only; must be
-// <= 4, the radii whose TMA plane loop is unrolled)
-#ifndef SF_CF_MAXR
-#define SF_CF_MAXR 4
-#endif
-#define SF_CF(R) ((R) <= SF_CF_MAXR)
-
-// combined-form term at radius k: (((ym + yp) + (zm + zp)) + (xm + xp)) + nu6, nu6 = fl(-6u)
-__device__ __forceinline__ float sf_cf_term(float ym, float yp, float zm, float zp, float xm, float xp,
-                                            float nu6)
-{
-    return __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(ym, yp), __fadd_rn(zm, zp)), __fadd_rn(xm, xp)), nu6);
-}
 
 // in-plane term at radius k for 3D: ((ym + yp) + (zm + zp)) - 4u, as one fma
 __device__ __forceinline__ float sf_inplane3(float ym, float yp, float zm, float zp, float u)

@@ -22,22 +22,7 @@ k_generic3d(SfStepArgs a)
     const float *__restrict__ c = a.cur;
     const float u = __ldg(c + idx);
     float lap;
-    if (SF_CF(R)) {
-        // combined form (stencil_common.cuh)
-        const float nu6 = __fmul_rn(-6.0f, u);
-        float L = 0.0f;
-#pragma unroll
-        for (int k = 1; k <= R; ++k) {
-            const float ym = (y - k >= 0) ? __ldg(c + idx - k * sy) : 0.0f;
-            const float yp = (y + k < a.n1) ? __ldg(c + idx + k * sy) : 0.0f;
-            const float zm = (z - k >= 0) ? __ldg(c + idx - k) : 0.0f;
-            const float zp = (z + k < a.n2) ? __ldg(c + idx + k) : 0.0f;
-            const float xm = (x - k >= 0) ? __ldg(c + idx - k * sx) : 0.0f;
-            const float xp = (x + k < a.n0b) ? __ldg(c + idx + k * sx) : 0.0f;
-            L = __fmaf_rn(a.w.w[k], sf_cf_term(ym, yp, zm, zp, xm, xp, nu6), L);
-        }
-        lap = L;
-    } else {
+    {
         float P = 0.0f, X = 0.0f;
 #pragma unroll
         for (int k = 1; k <= R; ++k) {

@@ -440,10 +440,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
     for (int k = 1; k <= R; ++k) Wk[k] = pk2(a.w.w[k], a.w.w[k]);
     Wk[0] = 0ull;
-    const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f), M6 = pk2(-6.f, -6.f);
-    // combined Laplacian form (stencil_common.cuh, sf_lap_cf): radii up to 4, where the plane
-    // loop is unrolled and the x queue can be read next to the in-plane neighbours
-    constexpr bool CMB = SF_CF(R);
+    const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f);
     const f2_t NG = pk2(-a.gscale, -a.gscale), ONE2 = pk2(1.f, 1.f);
     const f2_t HDT2 = pk2(a.hdt, a.hdt);
     constexpr int QINF = 0x7fffffff;
@@ -531,7 +528,6 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                     // ---- (1) in-plane partial of output plane q = p - R: its u tile is
                     // resident (arrived R planes ago), so this overlaps the wait for plane p
                     f2_t Pin[VY][NJ], Uq[VY][NJ];
-                    f2_t S4R[VY][NJ], NU6[VY][NJ];  // CMB: radius-R in-plane pair sums, -6u
                     if (outp) {
                         const float *uq = ubase + uo * UF;
                         // y rows rown - R .. rown + VY - 1 + R (own rows included)
@@ -557,34 +553,6 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                 ldp<VZ>(uq + own_off + j * W + VZ + VZ * c, ZR[j] + NJ * c);
                             }
                         }
-                        // CMB (r <= 4, unrolled loop): the combined form (stencil_common.cuh)
-                        //   t_k = (((y-k + y+k) + (z-k + z+k)) + (x-k + x+k)) + (-6u),  L = sum_k w_k t_k
-                        // -- radii 1..R-1 now, radius R (x+R = plane p, still in flight) after
-                        // the wait.  The x pair sums come from the register queue through a
-                        // slot switch that folds away in the unrolled loop.  Otherwise the
-                        // in-plane partial P = sum_k w_k (((y-k + y+k) + (z-k + z+k)) - 4u).
-                        constexpr int KX = (CMB && R > 1) ? R - 1 : 1;
-                        f2_t XS[VY][NJ][KX];
-                        if constexpr (CMB) {
-                            auto xpairs = [&](auto ic) {
-                                constexpr int SQ = (decltype(ic)::value - R + Q) % Q;  // slot of plane q
-#pragma unroll
-                                for (int j = 0; j < VY; ++j)
-#pragma unroll
-                                    for (int jp = 0; jp < NJ; ++jp)
-#pragma unroll
-                                        for (int k = 1; k < R; ++k)
-                                            XS[j][jp][k - 1] = add2(V[(SQ - k + Q) % Q][j][jp], V[(SQ + k) % Q][j][jp]);
-                            };
-                            switch (sl) {
-#define SF_XP(S_) \
-    case S_:      \
-        if constexpr (S_ < Q) xpairs(std::integral_constant<int, S_>{}); \
-        break;
-                                SF_XP(0) SF_XP(1) SF_XP(2) SF_XP(3) SF_XP(4) SF_XP(5) SF_XP(6) SF_XP(7) SF_XP(8)
-#undef SF_XP
-                            }
-                        }
 #pragma unroll
                         for (int j = 0; j < VY; ++j) {
                             // float at z offset e (relative to the own first column) of row j
@@ -608,8 +576,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                             for (int jp = 0; jp < NJ; ++jp) {
                                 const f2_t u = Uq[j][jp];
-                                if (CMB) NU6[j][jp] = mul2(M6, u);
-                                // radius ascending
+                                // radius ascending (== sf_inplane3 per lane)
                                 f2_t P = 0ull;
 #pragma unroll
                                 for (int k = 1; k <= R; ++k) {
@@ -620,12 +587,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                         zs = pk2(__fadd_rn(F(em), F(ep)), __fadd_rn(F(em + 1), F(ep + 1)));
                                     else
                                         zs = add2(PZ(em), PZ(ep));
-                                    if (CMB) {
-                                        if (k < R) P = fma2(Wk[k], add2(add2(add2(ys, zs), XS[j][jp][k < R ? k - 1 : 0]), NU6[j][jp]), P);
-                                        else S4R[j][jp] = add2(ys, zs);
-                                    } else {
-                                        P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);  // == sf_inplane3
-                                    }
+                                    P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
                                 }
                                 Pin[j][jp] = P;
                             }
@@ -643,16 +605,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             SF_CHK(ut + own_off + j * W, ut, ut + W * C::H);
                             ldp<VZ>(ut + own_off + j * W, V[S][j]);
                         }
-                        if (outp && CMB) {
-                            // radius R of the combined form: L = fma(w_R, ((s4_R + (x-R + x+R)) - 6u), L)
-#pragma unroll
-                            for (int j = 0; j < VY; ++j)
-#pragma unroll
-                                for (int jp = 0; jp < NJ; ++jp) {
-                                    const f2_t xs = add2(V[(SQ - R + Q) % Q][j][jp], V[S][j][jp]);
-                                    X[j][jp] = fma2(Wk[R], add2(add2(S4R[j][jp], xs), NU6[j][jp]), Pin[j][jp]);
-                                }
-                        } else if (outp) {
+                        if (outp) {
 #pragma unroll
                             for (int j = 0; j < VY; ++j)
 #pragma unroll
@@ -735,7 +688,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                             for (int jp = 0; jp < NJ; ++jp) {
                                 const f2_t u = Uq[j][jp];
-                                const f2_t lap = CMB ? X[j][jp] : add2(Pin[j][jp], X[j][jp]);
+                                const f2_t lap = add2(Pin[j][jp], X[j][jp]);
                                 // out = u + beta (u - old) + c3 lap   (== sf_update per lane)
                                 const f2_t d = fma2(M1, ov[j][jp], u);
                                 res2[j][jp] = fma2(cv[j][jp], lap, fma2(bv[j][jp], d, u));

@@ -1040,7 +1040,7 @@ def _surface_problem(shape, so, nt, zs, seed, nbl=4, damp=True):
 
 
 @pytest.mark.parametrize("shape,so,zs,damp", [((30, 44, 64), 8, 9, True), ((26, 30, 144), 12, 7, False),
-                                              ((26, 30, 144), 12, 135, False), ((22, 26, 132), 4, 129, True)])
+                                              ((26, 30, 144), 12, 135, False), ((30, 30, 132), 4, 129, True)])
 def test_receiver_surface_adjoint_gradient(shape, so, zs, damp):
     """Adjoint injection of a receiver surface (every node of z = zs: > 256 targets, the
     standalone injection kernel between stencil steps): adjoint source records, final
@@ -1182,9 +1182,11 @@ def test_one_launch_schedule_bitwise(so, shape, plane):
         o += [g.cpu().numpy(), J]
         if one:
             n1 = prop.debug_probe(None)
-            # forward + the gradient's forward (its adjoint injects the receivers with the
-            # standalone kernel -> the two-launch split schedule)
-            assert n1 == 2 * (p.nt - 1), n1
+            # the forward and the gradient's forward; the gradient's adjoint only on its non-
+            # correlation steps with a small receiver set (GRAD-mode injection stays standalone
+            # -> the two-launch split there; a receiver surface is never fused)
+            na = 0 if plane else (p.nt - 1) - (p.nt - 1) // 3
+            assert n1 == 2 * (p.nt - 1) + na, n1
         outs.append(o)
         prop.close()
     for a, b in zip(outs[0], outs[1]):
