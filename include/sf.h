@@ -155,6 +155,9 @@ SF_API sf_status sf_gradient_ckpt(sf_handle *h, const float *wavelet, const floa
  * Synchronises `stream`. */
 SF_API sf_status sf_forward_host(const sf_desc *host_desc, const float *wavelet_host, float *rec_host,
                           float *u_final_host, void *stream);
+/* SURVEY 8(b)'s name for the same flat form (sf_create + sf_forward + sf_destroy). */
+SF_API sf_status sf_forward_once(const sf_desc *host_desc, const float *wavelet_host, float *rec_host,
+                          float *u_final_host, void *stream);
 
 /* Profiling: when on, the library records CUDA events around every stencil launch on
  * the launch stream; sf_get_profile synchronises and returns the summed stencil-kernel

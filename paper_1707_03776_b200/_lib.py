@@ -24,7 +24,7 @@ STATUS = {0: "SF_OK", 1: "SF_ERR_INVALID_ARG", 2: "SF_ERR_SHAPE", 3: "SF_ERR_ORD
 # every symbol include/sf.h declares
 EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint", "sf_residual",
            "sf_gradient_workspace_bytes", "sf_gradient", "sf_gradient_ckpt_workspace_bytes",
-           "sf_gradient_ckpt", "sf_forward_host", "sf_set_profiling",
+           "sf_gradient_ckpt", "sf_forward_host", "sf_forward_once", "sf_set_profiling",
            "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_nccl_comm_info",
            "sf_nccl_check", "sf_create_slab",
@@ -82,6 +82,7 @@ def lib():
             "sf_gradient": [P, P, P, P, P, P, Z, I, P],
             "sf_gradient_ckpt": [P, P, P, P, P, P, Z, I, I, P],
             "sf_forward_host": [P, P, P, P, P],
+            "sf_forward_once": [P, P, P, P, P],
             "sf_set_profiling": [P, I],
             "sf_get_profile": [P, P, P, P, I],
             "sf_get_profile_detail": [P, P, P, I],

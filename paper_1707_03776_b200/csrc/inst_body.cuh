@@ -14,11 +14,16 @@
 
 namespace {
 
-template <int VY, int DM, int MODE, int LZ>
+template <int VY, int DM, int MODE, int LZ, bool BIDIR = false>
 cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
+    if constexpr (!BIDIR && LZ == 32) {
+        // the one-launch slab schedule has its own instances (direction and boundary-signal
+        // code compiled out of the plain ones: it cost up to 7 % at r = 8 when only inactive)
+        if (a.bidir) return launch_tma<VY, DM, MODE, LZ, true>(L, a, st);
+    }
     using C = sftma::Cfg<SF_R, VY, DM, MODE, LZ>;
-    auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE, LZ>;
+    auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE, LZ, BIDIR>;
     // the dynamic shared-memory limit is a per-device function attribute: cached per device
     // in an atomic bitmask (handles on several GPUs, concurrent rank threads)
     static std::atomic<uint64_t> attr{0};

@@ -336,6 +336,8 @@ static int64_t n_warp_lists(const sf_handle *h, int vy)
 }
 
 // Per-(tile, warp) lists of the injection targets for the TMA kernel's fused injection.
+static sf_status ensure_split_lists(sf_handle *h, SfSparse &sp);
+
 static sf_status ensure_inj_tiles(sf_handle *h, SfSparse &sp, int by)
 {
     SfInjTiles &T = sp.tiles;
@@ -901,6 +903,17 @@ static sf_status create_common(const sf_desc *d, sf_handle *h)
     // one-launch schedule counters (stream memory operations: plain cudaMalloc, not the pool)
     SF_CUDA_TRY((cudaMalloc)((void **)&h->sigc, 2 * sizeof(unsigned int)));
     SF_CUDA_TRY(cudaMemset(h->sigc, 0, 2 * sizeof(unsigned int)));
+    // the tables the time loops would otherwise build on first use (no per-call
+    // allocation): fused-injection lists for the default tile shape, split-schedule lists in
+    // slab mode.  (A later sf_set_tuning to another tile shape rebuilds the lists once.)
+    if (resolve_variant(h) == SF_VAR_TMA) {
+        if (h->src.ntgt > 0 && h->src.ntgt <= h->fuse_max && (s = ensure_inj_tiles(h, h->src, resolve_vy(h)))) return s;
+        if (h->rec.ntgt > 0 && h->rec.ntgt <= h->fuse_max && (s = ensure_inj_tiles(h, h->rec, resolve_vy(h)))) return s;
+    }
+    if (h->split) {
+        if (h->src.ntgt > 0 && (s = ensure_split_lists(h, h->src))) return s;
+        if (h->rec.ntgt > 0 && (s = ensure_split_lists(h, h->rec))) return s;
+    }
     SF_CUDA_TRY(cudaDeviceSynchronize());
     return SF_OK;
 }
@@ -1838,6 +1851,12 @@ sf_status ensure(float **p, size_t *cap, size_t n)
     return SF_OK;
 }
 }  // namespace
+
+extern "C" sf_status sf_forward_once(const sf_desc *hd, const float *wavelet_host, float *rec_host,
+                                     float *u_final_host, void *stream)
+{
+    return sf_forward_host(hd, wavelet_host, rec_host, u_final_host, stream);
+}
 
 extern "C" sf_status sf_forward_host(const sf_desc *hd, const float *wavelet_host, float *rec_host,
                                      float *u_final_host, void *stream)

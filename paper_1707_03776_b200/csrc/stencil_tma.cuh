@@ -297,7 +297,7 @@ __device__ __forceinline__ int seg_dir(const SfStepArgs &a, int it, int tiles, i
     return (a.bidir && nchunk > 1 && it / tiles == nchunk - 1 && w1 == (int64_t)(it % tiles + 1) * PT) ? -1 : 1;
 }
 
-template <int R, int VY, int DM, int MODE, int LZ = 32>
+template <int R, int VY, int DM, int MODE, int LZ = 32, bool BIDIR = false>
 __global__ void __launch_bounds__(Cfg<R, VY, DM, MODE, LZ>::THREADS, 1)
 k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_old,
         const __grid_constant__ CUtensorMap tm_c3, const __grid_constant__ CUtensorMap tm_beta,
@@ -362,7 +362,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
             for (int64_t w = (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk,
                          w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
                 const Seg sg = next_seg(w, w1, P1, PT, a);
-                const int dir = seg_dir(a, it, tiles, nchunk, w1, PT);
+                // (BIDIR instances only: the one-launch slab schedule; elsewhere dir == 1 folds)
+                const int dir = BIDIR ? seg_dir(a, it, tiles, nchunk, w1, PT) : 1;
                 w += sg.qb - sg.qa;
                 const int z0 = (int)a.zbase + (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
                 const int NP = (int)(sg.qb - sg.qa) + 2 * R;
@@ -449,7 +450,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     for (int64_t w = (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk,
                  w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
         const Seg sg = next_seg(w, w1, P1, PT, a);
-        const int dir = seg_dir(a, it, tiles, nchunk, w1, PT);
+        const int dir = BIDIR ? seg_dir(a, it, tiles, nchunk, w1, PT) : 1;
         w += sg.qb - sg.qa;
         const int z0 = (int)a.zbase + (sg.tile % ntz) * TZ, y0 = (sg.tile / ntz) * BY;
         const int zg = z0 + VZ * lz;
@@ -482,8 +483,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
         // boundary signals (one-launch slab schedule): the iteration after which this segment
         // has stored all of [xa, xa + r) (left) / [xb - r, xb) (right), else -1; checked once
         // per unrolled group of iterations (a check inside the unrolled body costs scheduling)
-        int fiL = (a.sig && dir > 0 && qa == (int)a.xa) ? min((int)a.xa + R, qb) - 1 - qa + 2 * R : -1;
-        int fiR = (a.sig && qb == (int)a.xb) ? (dir < 0 ? (qb - 1 - max((int)a.xb - R, qa)) + 2 * R : NP - 1) : -1;
+        int fiL = (BIDIR && a.sig && dir > 0 && qa == (int)a.xa) ? min((int)a.xa + R, qb) - 1 - qa + 2 * R : -1;
+        int fiR = (BIDIR && a.sig && qb == (int)a.xb) ? (dir < 0 ? (qb - 1 - max((int)a.xb - R, qa)) + 2 * R : NP - 1) : -1;
         // snapshot row pointer (element offsets as the output; with fp16 snapshots it only
         // carries the element index, stsnap_half rebases it onto the __half array)
         float *sptr = (MODE == SF_MODE_SAVE) ? a.snap_out + (optr - a.out) : nullptr;
@@ -795,8 +796,8 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
             // one-launch schedule: a boundary range of this tile is stored -> every consumer
             // thread fences its stores, the consumer warps meet, one thread signals
             const int done = base + UNR;  // iterations finished (or more: the last group)
-            const bool fl = fiL >= 0 && done > fiL, fr = fiR >= 0 && done > fiR;
-            if (fl || fr) {
+            const bool fl = BIDIR && fiL >= 0 && done > fiL, fr = BIDIR && fiR >= 0 && done > fiR;
+            if (BIDIR && (fl || fr)) {
                 __threadfence();
                 asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
                 if (wy == 0 && lane == 0) {
