@@ -50,7 +50,7 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-NCU_ROUND = "r01"
+NCU_ROUND = "r02"
 
 
 def ncu_traffic(cfg):

@@ -30,7 +30,20 @@ def main():
     ap.add_argument("--shot", type=int, default=0)
     ap.add_argument("--nt", type=int, default=None)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--subsample", type=int, default=0,
+                    help="only write d_obs_sub.npy = every N-th trace of an existing d_obs.npy "
+                         "(the upload to the GPU box is capped at 512 MiB) and record it in meta.json")
     a = ap.parse_args()
+    if a.subsample:
+        d = np.load(os.path.join(a.out, "d_obs.npy"))
+        np.save(os.path.join(a.out, "d_obs_sub.npy"), np.ascontiguousarray(d[:, ::a.subsample]))
+        with open(os.path.join(a.out, "meta.json")) as f:
+            meta = json.load(f)
+        meta["d_obs_stride"] = a.subsample
+        with open(os.path.join(a.out, "meta.json"), "w") as f:
+            json.dump(meta, f, indent=1)
+        print(json.dumps(meta))
+        return
     p = synth.make_config(a.config, nt=a.nt, shot=a.shot) if a.config == 4 else synth.make_config(a.config, nt=a.nt)
     k = p.save_every
     S = max(k, int(round(math.sqrt(2.0 * (p.nt - 1) * k) / k)) * k)

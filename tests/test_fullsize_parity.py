@@ -137,7 +137,11 @@ def _gradient_case(ci, shot=0):
         with open(meta_path) as f:
             meta = json.load(f)
         assert (meta["shape"], meta["nt"], meta["save_every"], meta["shot"]) == (list(p.shape), p.nt, k, shot)
-        d_obs_o = np.load(os.path.join(exp_dir, "d_obs.npy")).astype(np.float64)
+        # d_obs.npy (every trace) or d_obs_sub.npy (every `d_obs_stride`-th trace: the GPU box
+        # takes at most 512 MiB of upload per call, configs[4]'s record alone is 960 MB)
+        st = int(meta.get("d_obs_stride", 1))
+        d_obs_o = np.load(os.path.join(exp_dir, "d_obs.npy" if st == 1 else "d_obs_sub.npy")).astype(np.float64)
+        dg = dg[:, ::st]
         go = {"grad": np.load(os.path.join(exp_dir, "grad.npy")), "J": meta["J"]}
         S, rres, src = meta["checkpoint_segment"], meta["rel_residual"], "scripts/oracle_expected.py"
         t2 = t1 + meta["d_obs_s"] + meta["gradient_s"]
