@@ -38,6 +38,9 @@
 #ifndef SF_DC_MIN
 #define SF_DC_MIN 3
 #endif
+#ifndef SF_DC_MIN_HI
+#define SF_DC_MIN_HI 2
+#endif
 #ifndef SF_MBAR_SUSPEND_NS
 #define SF_MBAR_SUSPEND_NS 0x100000
 #endif
@@ -184,7 +187,7 @@ struct Cfg {
     // below SF_DC_MIN only when even DU = R + 2 leaves no more, e.g. r = 8 GRAD + damping)
     // r >= 7: two coefficient stages are enough and the freed stage deepens the u ring's
     // lead from 1 to 2 planes (configs[3]: -1.1 %, A/B)
-    static constexpr int DC_MIN = R >= 7 ? 2 : SF_DC_MIN;
+    static constexpr int DC_MIN = R >= 7 ? SF_DC_MIN_HI : SF_DC_MIN;
     static constexpr int DU_WANT = R + 5;
     static constexpr int DU_FIT = (BUDGET - DC_MIN * CST) / UST;
     static constexpr int DU = DU_FIT >= DU_WANT ? DU_WANT : (DU_FIT >= R + 2 ? DU_FIT : R + 2);
