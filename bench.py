@@ -301,6 +301,12 @@ def run_ours(args):
         prop.set_option(8, 1)   # peer-store halo exchange instead of NCCL send/recv
     if args.snap_half:
         prop.set_option(7, 1)
+    if args.no_pdl:
+        prop.set_option(12, 0)  # SF_OPT_PDL off: plain launches
+    # time every 16th kernel launch of each kind inside the timed steps (an event pair around
+    # every launch costs 1-3 % of a step and defeats PDL; the average over ~60 timed stencil
+    # launches per step is the kernel's average launch time)
+    prop.set_option(13, args.prof_every)
     wav = dev(p.wavelet)
     u = prop.zeros_state()
     rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
@@ -341,7 +347,7 @@ def run_ours(args):
     # per-launch kernel times come from in-stream events recorded by the library; with
     # --graph the timed steps replay CUDA graphs (no events) and one extra profiled eager
     # step after the timed region provides the kernel times
-    prop.set_profiling(not args.graph)
+    prop.set_profiling(not (args.graph or args.no_prof))
     prop.profile(reset=True)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -357,7 +363,7 @@ def run_ours(args):
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
     step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
-    if args.graph:
+    if args.graph or args.no_prof:
         prop.set_profiling(True)
         prop.profile(reset=True)
         step()
@@ -456,7 +462,12 @@ def run_ours(args):
                          "bytes_per_point": round(alg_bytes / npts_local, 3), "avg_launch_ms": round(launch_ms, 5),
                          "stencil_share_of_step": round(prof["stencil_ms"] / max(ms, 1e-9), 4),
                          "per_update_us": {k: round(prof[f"{k}_ms"] * 1e3 / (args.steps * (p.nt - 1)), 2)
-                                           for k in ("stencil", "inject", "interp", "other")}},
+                                           for k in ("stencil", "inject", "interp", "other")},
+                         "per_update_note": "event time per kind on its own stream: 'interp' is the record "
+                                            "kernel on the side stream, overlapped with the next stencil step, "
+                                            "and includes its queueing behind the persistent stencil CTAs (its "
+                                            "own cost, serialised and cold, is in the ncu launch list: "
+                                            "profiles/r02_bench_launches.json)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(prof["launches"]),
@@ -601,6 +612,13 @@ def main():
     ap.add_argument("--snap-half", action="store_true",
                     help="gradient configs: fp16 snapshots (SF_OPT_SNAP_HALF, reading C23)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true",
+                    help="plain launches instead of programmatic dependent launches (SF_OPT_PDL 0)")
+    ap.add_argument("--prof-every", type=int, default=16,
+                    help="time every n-th kernel launch of each kind inside the timed region (default 16)")
+    ap.add_argument("--no-prof", action="store_true",
+                    help="A/B runs only: no per-kernel events inside the timed steps (kernel times from "
+                         "one extra profiled step after them)")
     ap.add_argument("--strong", action="store_true",
                     help="N > 1, --config 3: split the literal 1024x512x512 grid over the GPUs "
                          "(strong scaling) instead of 1024 planes per GPU (weak)")

@@ -159,8 +159,8 @@ SF_API sf_status sf_forward_host(const sf_desc *host_desc, const float *wavelet_
 SF_API sf_status sf_forward_once(const sf_desc *host_desc, const float *wavelet_host, float *rec_host,
                           float *u_final_host, void *stream);
 
-/* Profiling: when on, the library records CUDA events around every stencil launch on
- * the launch stream; sf_get_profile synchronises and returns the summed stencil-kernel
+/* Profiling: when on, the library records CUDA events around every (SF_OPT_PROF_EVERY:
+ * every n-th) stencil launch on the launch stream; sf_get_profile synchronises and returns the summed stencil-kernel
  * time, the number of stencil launches and of all kernel launches since the last reset. */
 SF_API sf_status sf_set_profiling(sf_handle *h, int on);
 SF_API sf_status sf_get_profile(sf_handle *h, double *stencil_ms, long long *stencil_launches,
@@ -233,6 +233,15 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   exchange becomes a copy into sf_debug_probe's buffer).  In-
                                   process local groups and SF_OPT_P2P keep the two-launch
                                   schedule.  Bitwise the same results.                          */
+#define SF_OPT_PDL 12          /* 1 (default): launch the stencil and the standalone injection kernels with
+                                  programmatic stream serialisation (PDL): each kernel's launch and
+                                  prologue overlap the previous kernel's tail, and it waits
+                                  (griddepcontrol.wait) for that kernel's writes before its first
+                                  global access.  Bitwise the same results.  0: plain launches.  */
+#define SF_OPT_PROF_EVERY 13   /* profiling (sf_set_profiling): time every n-th launch of each kind
+                                  (default 1 = every launch); sf_get_profile* scale the timed sum by
+                                  launches / timed launches.  An event pair between two kernels
+                                  costs 1-3 % of a step and defeats PDL.                          */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 /* Test hook of the one-launch schedule on one GPU (SF_OPT_ONE_LAUNCH 2): after each step's
  * counters fire, the comm stream copies the r boundary planes at each end of the new level

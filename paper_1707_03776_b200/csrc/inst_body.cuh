@@ -59,10 +59,21 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
     }
     const int64_t g = std::min(tiles * nch, slots);
     dim3 block(32, C::NW + 1);  // NW consumer warps + 1 TMA producer warp
-    kern<<<(unsigned)g, block, C::SMEM, st>>>(L.maps->cur, L.maps->old, L.maps->c3, L.maps->beta,
-                                              L.maps->snap, L.maps->grad, a, L.snap_slot, (int)chunk,
-                                              (int)nch);
-    return cudaGetLastError();
+    // programmatic dependent launch (SF_OPT_PDL): the CTAs' prologue (barrier init, tensor-map
+    // prefetch) overlaps the previous kernel's tail; they wait (griddepcontrol.wait) before
+    // their first global access
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = L.pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, L.maps->cur, L.maps->old, L.maps->c3, L.maps->beta, L.maps->snap,
+                              L.maps->grad, a, L.snap_slot, (int)chunk, (int)nch);
 }
 
 template <int MODE>

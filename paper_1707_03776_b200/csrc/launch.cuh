@@ -21,6 +21,7 @@ struct SfLaunch {
     int mode;         // SfMode
     int snap_slot;    // GRAD: snapshot slot for the 4D snapshot tensor map
     int lz;           // TMA lane layout: 32 (128-column tiles) or 8 (narrow 32-column tiles)
+    int pdl;          // launch with programmatic stream serialisation (SF_OPT_PDL)
     const SfTmaMaps *maps;
 };
 

@@ -228,13 +228,16 @@ struct ProfScope {
     ProfScope(sf_handle *h_, int kind, cudaStream_t st_) : h(h_), st(st_)
     {
         h->n_all++;
-        h->n_kind[kind]++;
-        if (h->prof) {
+        // SF_OPT_PROF_EVERY = n: time every n-th launch of each kind (the event pair between
+        // two kernels costs ~1-3 % and defeats PDL); totals are scaled by launches / timed
+        if (h->prof && (h->n_kind[kind] % h->prof_every) == 0) {
             cudaEvent_t e0 = next_event(h);
             e1 = next_event(h);
             h->ev_kind.push_back(kind);
+            h->n_samp[kind]++;
             cudaEventRecord(e0, st);
         }
+        h->n_kind[kind]++;
     }
     ~ProfScope()
     {
@@ -426,6 +429,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     L.mode = mode;
     L.snap_slot = b.snap_slot;
     L.lz = 32;
+    L.pdl = h->pdl ? 1 : 0;
     // z remainder (SF_OPT_ZSPLIT): n2 = 128 k + rem with 0 < rem <= 64 -> the 128-column tiles
     // cover [0, 128 k) and a second launch of narrow 56 x 32 tiles covers the rem columns
     // (the 128-column tiles there would be mostly idle lanes; configs[4]: 400 = 3 x 128 + 16).
@@ -536,15 +540,26 @@ static sf_status launch_inject(sf_handle *h, const SfSparse &sp, float *u, const
 {
     if (sp.ntgt == 0 || !vals) return SF_OK;
     ProfScope ps(h, PK_INJECT, st);
+    // (SF_OPT_PDL: launched with programmatic stream serialisation -- its launch overlaps the
+    // stencil's tail; the kernel waits for the stencil's writes before touching them)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((sp.ntgt + 127) / 128));
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = h->pdl ? 1 : 0;
+    const int half = h->snap_half ? 1 : 0;
     if (sp.jk > 0)
-        k_inject_ell<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.jk, sp.ej_pt, sp.ej_coef, sp.ntgt,
-                                                             vals, snap_patch, grad_snap, grad, gscale,
-                                                             h->snap_half ? 1 : 0);
+        SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_inject_ell, u, (const int64_t *)sp.j_tgt, sp.jk, (const int *)sp.ej_pt,
+                                       (const float *)sp.ej_coef, sp.ntgt, vals, (void *)snap_patch,
+                                       (const void *)grad_snap, grad, gscale, half));
     else
-        k_inject<<<(sp.ntgt + 127) / 128, 128, 0, st>>>(u, sp.j_tgt, sp.j_rowptr, sp.j_pt, sp.j_coef,
-                                                         sp.ntgt, vals, snap_patch, grad_snap, grad, gscale,
-                                                         h->snap_half ? 1 : 0);
-    SF_CUDA_TRY(cudaGetLastError());
+        SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_inject, u, (const int64_t *)sp.j_tgt, (const int *)sp.j_rowptr,
+                                       (const int *)sp.j_pt, (const float *)sp.j_coef, sp.ntgt, vals,
+                                       (void *)snap_patch, (const void *)grad_snap, grad, gscale, half));
     return SF_OK;
 }
 
@@ -1105,6 +1120,14 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         h->zsplit = value != 0;
         drop_graphs(h);
         return SF_OK;
+    case SF_OPT_PROF_EVERY:
+        if (value < 1) return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_PROF_EVERY %d < 1", value);
+        h->prof_every = value;
+        return SF_OK;
+    case SF_OPT_PDL:
+        h->pdl = value != 0;
+        drop_graphs(h);
+        return SF_OK;
     case SF_OPT_ONE_LAUNCH:
         if (value < 0 || value > 2) return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_ONE_LAUNCH %d", value);
         h->one_launch = value;
@@ -1157,14 +1180,14 @@ static sf_status collect_profile(sf_handle *h, double *ms_kind, long long *n_kin
         tot[h->ev_kind[i / 2]] += t;
     }
     for (int k = 0; k < PK_N; ++k) {
-        if (ms_kind) ms_kind[k] = tot[k];
+        if (ms_kind) ms_kind[k] = h->n_samp[k] ? tot[k] * (double)h->n_kind[k] / (double)h->n_samp[k] : 0.0;
         if (n_kind) n_kind[k] = h->n_kind[k];
     }
     if (nall) *nall = h->n_all;
     if (reset) {
         h->ev_used = 0;
         h->ev_kind.clear();
-        for (int k = 0; k < PK_N; ++k) h->n_kind[k] = 0;
+        for (int k = 0; k < PK_N; ++k) h->n_kind[k] = h->n_samp[k] = 0;
         h->n_all = 0;
     }
     return SF_OK;

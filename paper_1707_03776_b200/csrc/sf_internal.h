@@ -87,6 +87,8 @@ struct sf_handle {
     std::vector<int> ev_kind;       // kind of event pair i (stencil / inject / interp / other)
     size_t ev_used = 0;
     long long n_kind[4] = {0, 0, 0, 0};
+    long long n_samp[4] = {0, 0, 0, 0};  // launches actually timed per kind
+    int prof_every = 1;                   // SF_OPT_PROF_EVERY
     long long n_all = 0;
     int sms = 148;                  // multiprocessors of the device (set at create)
     // side stream for records (overlap with the next stencil step)
@@ -111,6 +113,7 @@ struct sf_handle {
     bool zsplit = true;               // SF_OPT_ZSPLIT: narrow tiles for a z remainder <= 64
     // one-launch slab schedule (SF_OPT_ONE_LAUNCH): the stencil launch signals its finished
     // boundary ranges on device counters; the comm stream waits on them, then exchanges
+    bool pdl = true;                  // SF_OPT_PDL: programmatic dependent launches (stencil, injection)
     int one_launch = 1;               // 1: in NCCL slab mode when applicable; 2: also on one GPU (emulation)
     unsigned int *sigc = nullptr;     // [2] left / right boundary counters (monotonic)
     uint32_t sig_tgt = 0;             // counter value that marks the current step's boundaries

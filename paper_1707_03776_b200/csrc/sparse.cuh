@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include "stencil_common.cuh"
 
 // snapshot element access: fp32, or fp16 (SF_OPT_SNAP_HALF, reading C23: round to nearest
 // even on store, exact widening on load)
@@ -67,6 +68,7 @@ __global__ void k_inject_ell(float *__restrict__ u, const int64_t *__restrict__ 
                              const void *__restrict__ grad_snap, float *__restrict__ grad, float gscale,
                              int snap_half)
 {
+    sf_pdl_wait();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntgt) return;
     const int64_t g = tgt[t];
@@ -161,6 +163,7 @@ __global__ void k_inject(float *__restrict__ u, const int64_t *__restrict__ tgt,
                          const void *__restrict__ grad_snap, float *__restrict__ grad, float gscale,
                          int snap_half)
 {
+    sf_pdl_wait();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= ntgt) return;
     float d = 0.0f;

@@ -33,6 +33,15 @@ enum SfMode { SF_MODE_PLAIN = 0, SF_MODE_SAVE = 1, SF_MODE_GRAD = 2 };
 // damping representation: none (beta = 1), hoisted beta array, separable profiles
 enum SfDampMode { SF_DAMP_NONE = 0, SF_DAMP_ARRAY = 1, SF_DAMP_SEP = 2 };
 
+// Programmatic dependent launch (SF_OPT_PDL): a kernel launched with the programmatic-
+// serialisation attribute may start while the previous kernel of the stream drains; it waits
+// here, before its first global-memory access, until that kernel has completed and its
+// writes are visible.  A no-op when the kernel was launched without the attribute.
+__device__ __forceinline__ void sf_pdl_wait()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // in-plane term at radius k for 3D: ((ym + yp) + (zm + zp)) - 4u, as one fma
 __device__ __forceinline__ float sf_inplane3(float ym, float yp, float zm, float zp, float u)
 {

@@ -349,6 +349,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
+    sf_pdl_wait();  // (PDL) the prologue above overlapped the previous kernel's tail
 
     if (wy == NW) {
         // ------------------------------------------------ producer warp (TMA issue)

@@ -1193,3 +1193,27 @@ def test_one_launch_schedule_bitwise(so, shape, plane):
         assert np.array_equal(a, b)
     ro = oracle.forward(p)["rec"]
     assert rel(outs[1][0], ro) <= TOL
+
+
+def test_pdl_launches_bitwise():
+    """SF_OPT_PDL (programmatic dependent launches of the stencil and standalone injection
+    kernels: each launch overlaps the previous kernel's tail and waits for its writes with
+    griddepcontrol.wait): forward records, final levels and the gradient with a receiver
+    surface (standalone injection between every adjoint step) are bitwise those of plain
+    launches, for r = 4 and r = 6 (narrow-tile z split: two launches per step)."""
+    for shape, so in (((30, 44, 64), 8), ((26, 30, 144), 12)):
+        p = _surface_problem(shape, so, 40, 7, seed=52, damp=(so == 8))
+        p.m_true = (p.m * 0.95).astype(np.float32)
+        d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+        outs = []
+        for pdl in (0, 1):
+            prop = make_prop(p)
+            prop.set_option(sf().SF_OPT_PDL, pdl)
+            assert prop.tuning()["variant"] == 2
+            rec, u, _ = prop.forward(dev(p.wavelet))
+            g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
+            torch.cuda.synchronize()
+            outs.append((rec.cpu().numpy(), u.cpu().numpy(), g.cpu().numpy(), J))
+            prop.close()
+        for a, b in zip(outs[0], outs[1]):
+            assert np.array_equal(a, b)
