@@ -233,11 +233,14 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   exchange becomes a copy into sf_debug_probe's buffer).  In-
                                   process local groups and SF_OPT_P2P keep the two-launch
                                   schedule.  Bitwise the same results.                          */
-#define SF_OPT_PDL 12          /* 1 (default): launch the stencil and the standalone injection kernels with
-                                  programmatic stream serialisation (PDL): each kernel's launch and
-                                  prologue overlap the previous kernel's tail, and it waits
-                                  (griddepcontrol.wait) for that kernel's writes before its first
-                                  global access.  Bitwise the same results.  0: plain launches.  */
+#define SF_OPT_PDL 12          /* 1 (default): launch the standalone injection kernel, and the stencil
+                                  launch that follows it, with programmatic stream serialisation
+                                  (PDL): the kernel's launch and prologue overlap the previous
+                                  kernel's tail and it waits (griddepcontrol.wait) for that
+                                  kernel's writes before its first global access (adjoints with a
+                                  receiver set: +1-2 %).  Stencil -> stencil stays plain (no gain:
+                                  a persistent launch cannot co-reside with the previous one).
+                                  Bitwise the same results.  0: plain launches.                 */
 #define SF_OPT_PROF_EVERY 13   /* profiling (sf_set_profiling): time every n-th launch of each kind
                                   (default 1 = every launch); sf_get_profile* scale the timed sum by
                                   launches / timed launches.  An event pair between two kernels

@@ -429,7 +429,11 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     L.mode = mode;
     L.snap_slot = b.snap_slot;
     L.lz = 32;
-    L.pdl = h->pdl ? 1 : 0;
+    // PDL only after a standalone injection kernel: stencil -> stencil gains nothing measurable
+    // (a persistent launch cannot co-reside with the previous one), and plain launches keep
+    // the sampled event timing of the stencil exact
+    L.pdl = (h->pdl && h->prev_inject) ? 1 : 0;
+    h->prev_inject = false;
     // z remainder (SF_OPT_ZSPLIT): n2 = 128 k + rem with 0 < rem <= 64 -> the 128-column tiles
     // cover [0, 128 k) and a second launch of narrow 56 x 32 tiles covers the rem columns
     // (the 128-column tiles there would be mostly idle lanes; configs[4]: 400 = 3 x 128 + 16).
@@ -551,6 +555,7 @@ static sf_status launch_inject(sf_handle *h, const SfSparse &sp, float *u, const
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = h->pdl ? 1 : 0;
+    h->prev_inject = true;
     const int half = h->snap_half ? 1 : 0;
     if (sp.jk > 0)
         SF_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_inject_ell, u, (const int64_t *)sp.j_tgt, sp.jk, (const int *)sp.ej_pt,
