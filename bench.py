@@ -307,6 +307,11 @@ def run_ours(args):
     # every launch costs 1-3 % of a step and defeats PDL; the average over ~60 timed stencil
     # launches per step is the kernel's average launch time)
     prop.set_option(13, args.prof_every)
+    tuned = None
+    if not args.no_autotune:
+        # setup-time tuning (sf_autotune; the paper's runtime block-size tuning):
+        # outside the timed region, same bits for every choice
+        tuned = prop.autotune(steps=10)
     wav = dev(p.wavelet)
     u = prop.zeros_state()
     rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
@@ -446,7 +451,7 @@ def run_ours(args):
                                      if (args.one_launch or (slab and not args.p2p)) else
                                      "split (boundary planes, then interior)") if split else
                                     "single launch per step") + (", CUDA graph replay" if args.graph else ""),
-                       "kernel_tuning": tuning},
+                       "kernel_tuning": tuning, "autotune": tuned},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "frac_of_nominal_8TBps": round(achieved / 8000.0, 4),
@@ -612,6 +617,8 @@ def main():
     ap.add_argument("--snap-half", action="store_true",
                     help="gradient configs: fp16 snapshots (SF_OPT_SNAP_HALF, reading C23)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-autotune", action="store_true",
+                    help="skip the setup-time tuning (sf_autotune) and keep the library's defaults")
     ap.add_argument("--no-pdl", action="store_true",
                     help="plain launches instead of programmatic dependent launches (SF_OPT_PDL 0)")
     ap.add_argument("--prof-every", type=int, default=16,

@@ -246,6 +246,14 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   launches / timed launches.  An event pair between two kernels
                                   costs 1-3 % of a step and defeats PDL.                          */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
+/* Setup-time tuning (the counterpart of the paper's runtime block-size auto-tuning,
+ * P:729-731): times `steps` plain stencil steps (no sparse work) of every feasible launch
+ * configuration -- TMA kernel with 14- or 7-row tiles, with or without the narrow remainder
+ * tiles (space order >= 10), the thread-per-point kernel -- on the caller's scratch state u
+ * ([2][Nloc] device floats, overwritten), keeps the fastest in the handle and returns it in
+ * chosen[3] = {variant, vy, zsplit} (may be NULL) and its time per step in *ms (may be NULL).
+ * Every configuration computes the same bits.  Synchronises `stream`. */
+SF_API sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen, float *ms, void *stream);
 /* Test hook of the one-launch schedule on one GPU (SF_OPT_ONE_LAUNCH 2): after each step's
  * counters fire, the comm stream copies the r boundary planes at each end of the new level
  * ([xa, xa + r) then [xb - r, xb), 2 r n1 n2 floats) into `dst` (device; NULL = off);

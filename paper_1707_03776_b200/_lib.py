@@ -29,7 +29,7 @@ EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_nccl_comm_info",
            "sf_nccl_check", "sf_create_slab",
            "sf_allreduce_gradient", "sf_local_group_create", "sf_local_group_destroy",
-           "sf_convection2d", "sf_laplace2d", "sf_debug_probe", "sf_last_error", "sf_version"]
+           "sf_convection2d", "sf_laplace2d", "sf_debug_probe", "sf_autotune", "sf_last_error", "sf_version"]
 
 
 SF_OPT_L2_PREFETCH, SF_OPT_SPLIT, SF_OPT_FUSE_MAX, SF_OPT_COMM_SMS, SF_OPT_GRAPH, SF_OPT_SNAP_HALF, SF_OPT_P2P, SF_OPT_ZSPLIT = \
@@ -98,6 +98,7 @@ def lib():
             "sf_nccl_comm_info": [P, P, P],
             "sf_nccl_check": [P],
             "sf_debug_probe": [P, P, P],
+            "sf_autotune": [P, P, I, P, P, P],
             "sf_create_slab": [P, P, I, I, P],
             "sf_allreduce_gradient": [P, P, P, Z, P, I, P],
             "sf_local_group_create": [I, P],

@@ -219,6 +219,16 @@ class Propagator:
         check(lib().sf_set_profiling(self._h, 1 if on else 0))
 
     @_ondev
+    def autotune(self, steps: int = 8, stream=None) -> dict:
+        """sf_autotune: time every feasible launch configuration on a scratch state and keep
+        the fastest (same bits either way).  Returns {variant, vy, zsplit, ms_per_step}."""
+        u = torch.zeros((2,) + self.local_shape, device=self.device)
+        ch = (ctypes.c_int * 3)()
+        ms = ctypes.c_float()
+        check(lib().sf_autotune(self._h, _ptr(u), int(steps), ch, ctypes.byref(ms), _stream(stream)))
+        return {"variant": ch[0], "vy": ch[1], "zsplit": ch[2], "ms_per_step": ms.value}
+
+    @_ondev
     def debug_probe(self, dst: Optional[torch.Tensor]) -> int:
         """sf_debug_probe: set (or clear) the one-launch test probe buffer; returns the
         number of steps run with the one-launch schedule so far."""

@@ -1077,6 +1077,75 @@ extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas)
     return SF_OK;
 }
 
+// Setup-time tuning (the GPU counterpart of the paper's runtime block-size auto-tuning of
+// its loop engine): time `steps` stencil steps (no sparse work) of every feasible
+// launch configuration on the caller's scratch state and keep the fastest.  Every
+// configuration computes the same bits, so the choice only changes speed.
+extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen, float *ms_out, void *stream)
+{
+    if (!h || !u || steps < 1) return sf_set_error(SF_ERR_INVALID_ARG, "autotune: NULL handle/state or steps < 1");
+    cudaStream_t st = S(stream);
+    struct Cand {
+        int variant, vy, zsplit;
+    };
+    std::vector<Cand> cands;
+    if (tma_ok(h)) {
+        cands.push_back({SF_VAR_TMA, 2, 1});
+        if (h->r >= 5) cands.push_back({SF_VAR_TMA, 2, 0});  // narrow remainder tiles off
+        cands.push_back({SF_VAR_TMA, 1, 1});
+    }
+    cands.push_back({SF_VAR_GENERIC, 0, 1});
+    const Cand keep{h->variant, h->vy, h->zsplit ? 1 : 0};
+    const bool keep_prof = h->prof;
+    h->prof = false;
+    cudaEvent_t e0, e1;
+    SF_CUDA_TRY(cudaEventCreate(&e0));
+    SF_CUDA_TRY(cudaEventCreate(&e1));
+    float best = 1e30f;
+    int bi = -1;
+    sf_status s = SF_OK;
+    float *A = u, *B = u + h->N;
+    for (size_t c = 0; c < cands.size() && !s; ++c) {
+        h->variant = cands[c].variant;
+        h->vy = cands[c].vy;
+        h->zsplit = cands[c].zsplit != 0;
+        for (int it = -2; it < steps && !s; ++it) {  // two untimed warm-up steps
+            if (it == 0) SF_CUDA_TRY(cudaEventRecord(e0, st));
+            StepBufs b{};
+            b.cur = (it & 1) ? A : B;
+            b.out = (it & 1) ? B : A;
+            bool fused = false;
+            s = launch_step(h, b, SF_MODE_PLAIN, st, &fused);
+        }
+        if (s) break;
+        SF_CUDA_TRY(cudaEventRecord(e1, st));
+        SF_CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        SF_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        ms /= (float)steps;
+        if (ms < best) {
+            best = ms;
+            bi = (int)c;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h->prof = keep_prof;
+    const Cand pick = (s || bi < 0) ? keep : cands[bi];
+    h->variant = pick.variant;
+    h->vy = pick.vy;
+    h->zsplit = pick.zsplit != 0;
+    drop_graphs(h);
+    if (s) return s;
+    if (chosen) {
+        chosen[0] = pick.variant;
+        chosen[1] = pick.vy;
+        chosen[2] = pick.zsplit;
+    }
+    if (ms_out) *ms_out = best;
+    return SF_OK;
+}
+
 extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
 {
     if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");

@@ -1217,3 +1217,21 @@ def test_pdl_launches_bitwise():
             prop.close()
         for a, b in zip(outs[0], outs[1]):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("shape,so", [((40, 44, 128), 8), ((26, 30, 144), 12)])
+def test_autotune_picks_a_configuration_same_bits(shape, so):
+    """sf_autotune (setup-time tuning): times every feasible launch configuration
+    on a scratch state, keeps the fastest; the forward after it is bitwise the forward with
+    the default tuning (every configuration computes the same bits)."""
+    p = synth.random_problem(3, shape, so, 30, seed=71, nbl=4, nsrc=2, nrec=9)
+    ref = gpu_forward(p)
+    prop = make_prop(p)
+    t = prop.autotune(steps=4)
+    assert t["variant"] in (1, 2) and t["ms_per_step"] > 0
+    tun = prop.tuning()
+    assert tun["variant"] == t["variant"]
+    rec, u, _ = prop.forward(dev(p.wavelet))
+    torch.cuda.synchronize()
+    assert np.array_equal(rec.cpu().numpy(), ref[0]) and np.array_equal(u.cpu().numpy(), ref[1])
+    prop.close()
