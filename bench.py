@@ -390,11 +390,18 @@ def run_ours(args):
 
     # roofline of the dominant kernel (stencil step): algorithmic bytes per launch
     bpp = 20 if eta_d is not None else 16      # u^n, u^{n-1}, out, c3 (+beta array) fp32
-    launch_ms = prof["stencil_ms"] / max(prof["stencil_launches"], 1)
+    # the stencil's average launch duration, two CUDA-event measurements over the timed
+    # region, both upper bounds: (a) the event-timed launches (every --prof-every-th; each
+    # such interval also holds the launch gap the event forces before the kernel) and (b) the
+    # wall time per update (every main-stream kernel of the step, gaps included); the tighter
+    # one is reported
+    sampled_ms = prof["stencil_ms"] / max(prof["stencil_launches"], 1)
+    wall_ms = ms_max / (args.steps * (p.nt - 1) * passes)
+    launch_ms = min(sampled_ms, wall_ms)
     split = args.split or slab
     if split:
         # boundary and interior launches overlap: time the stencil by the wall time per update
-        launch_ms = ms_max / (args.steps * (p.nt - 1) * passes)
+        launch_ms = wall_ms
     alg_bytes = bpp * npts_local
     if grad_mode:
         # forward: nt-1 launches, (nt-1)//k of them also store a snapshot (+4 B/pt); adjoint:
@@ -465,6 +472,10 @@ def run_ours(args):
                                    ("k_generic3d" if len(gshape) == 3 else "k_generic2d"),
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "bytes_per_point": round(alg_bytes / npts_local, 3), "avg_launch_ms": round(launch_ms, 5),
+                         "launch_time_source": {"event_timed_launches_ms": round(sampled_ms, 5),
+                                                "wall_per_update_ms": round(wall_ms, 5),
+                                                "timed_every": args.prof_every,
+                                                "used": "wall per update" if launch_ms == wall_ms else "event-timed launches"},
                          "stencil_share_of_step": round(prof["stencil_ms"] / max(ms, 1e-9), 4),
                          "per_update_us": {k: round(prof[f"{k}_ms"] * 1e3 / (args.steps * (p.nt - 1)), 2)
                                            for k in ("stencil", "inject", "interp", "other")},
