@@ -82,7 +82,7 @@ def _dump(ci, out):
     d = os.environ.get("SF_PARITY_OUT", os.path.join("gpurun_out", "parity"))
     os.makedirs(d, exist_ok=True)
     out["config"] = ci
-    out["oracle_threads"] = oracle.num_threads()
+    out.setdefault("oracle_threads", oracle.num_threads())
     with open(os.path.join(d, f"parity_c{ci}.json"), "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out))
@@ -144,6 +144,7 @@ def _gradient_case(ci, shot=0):
         dg = dg[:, ::st]
         go = {"grad": np.load(os.path.join(exp_dir, "grad.npy")), "J": meta["J"]}
         S, rres, src = meta["checkpoint_segment"], meta["rel_residual"], "scripts/oracle_expected.py"
+        pre = {"oracle_threads": meta.get("oracle_threads"), "d_obs_trace_stride": st}
         t2 = t1 + meta["d_obs_s"] + meta["gradient_s"]
     else:
         # oracle: its own d_obs, checkpointed gradient
@@ -152,11 +153,12 @@ def _gradient_case(ci, shot=0):
         go = oracle.gradient(p, d_obs_o, save_every=k, checkpoint=S)
         rres, src = float(np.linalg.norm(go["res"]) / np.linalg.norm(d_obs_o)), "in-process"
         t2 = time.time()
+        pre = {}
     out = {"kind": "gradient", "shape": list(p.shape), "space_order": p.space_order, "nt": p.nt,
            "save_every": k, "checkpoint_segment": S, "shot": shot, "tuning": tun, "oracle_run": src,
            "d_obs": trace_stats(dg, d_obs_o), "d_syn_oracle_rel_residual": rres,
            "grad_rel_l2": rel(gg, go["grad"]), "J_gpu": J, "J_oracle": go["J"],
-           "J_rel_err": abs(J - go["J"]) / go["J"], "gpu_s": t1 - t0, "oracle_s": t2 - t1}
+           "J_rel_err": abs(J - go["J"]) / go["J"], "gpu_s": t1 - t0, "oracle_s": t2 - t1, **pre}
     _dump(ci, out)
     assert out["d_obs"]["rel_l2"] <= TOL
     assert out["grad_rel_l2"] <= TOL and out["J_rel_err"] <= TOL
