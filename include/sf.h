@@ -172,7 +172,9 @@ SF_API sf_status sf_get_profile_detail(sf_handle *h, double *ms_by_kind, long lo
                                        int reset);
 
 /* Tuning: kernel variant (0 auto, 1 generic thread-per-point, 2 TMA 2.5D streaming),
- * TMA rows per thread `vy` (0 auto = 2: 14-row tiles; 1: 7-row tiles) and the number of
+ * TMA layout `vy` (0 auto = 2: 2 rows x 4 z per thread, 7 consumer warps, 14 x 128 tiles;
+ * 1: one row per thread, 7-row tiles; 3, space order >= 10: 2 rows x 2 z per thread, 11
+ * consumer warps, 22 x 64 tiles -- otherwise read as 2) and the number of
  * persistent TMA CTAs `ctas` (0 auto = one per SM; the (tile, plane) work is split into
  * `ctas` equal runs; every setting gives the same bits).  SF_ERR_INVALID_ARG for other
  * values. */

@@ -14,16 +14,16 @@
 
 namespace {
 
-template <int VY, int DM, int MODE, int LZ, bool BIDIR = false>
+template <int VY, int DM, int MODE, int LZ, bool BIDIR = false, int LAY = 0>
 cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    if constexpr (!BIDIR && LZ == 32) {
+    if constexpr (!BIDIR && LZ == 32 && LAY == 0) {
         // the one-launch slab schedule has its own instances (direction and boundary-signal
         // code compiled out of the plain ones: it cost up to 7 % at r = 8 when only inactive)
         if (a.bidir) return launch_tma<VY, DM, MODE, LZ, true>(L, a, st);
     }
-    using C = sftma::Cfg<SF_R, VY, DM, MODE, LZ>;
-    auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE, LZ, BIDIR>;
+    using C = sftma::Cfg<SF_R, VY, DM, MODE, LZ, LAY>;
+    auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE, LZ, BIDIR, LAY>;
     // the dynamic shared-memory limit is a per-device function attribute: cached per device
     // in an atomic bitmask (handles on several GPUs, concurrent rank threads)
     static std::atomic<uint64_t> attr{0};
@@ -91,39 +91,39 @@ cudaError_t launch_generic(const SfLaunch &L, const SfStepArgs &a, cudaStream_t 
     return cudaGetLastError();
 }
 
-template <int VY, int DM, int LZ>
+template <int VY, int DM, int LZ, int LAY = 0>
 cudaError_t launch_tma_dm(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     switch (L.mode) {
-    case SF_MODE_PLAIN: return launch_tma<VY, DM, SF_MODE_PLAIN, LZ>(L, a, st);
-    case SF_MODE_SAVE: return launch_tma<VY, DM, SF_MODE_SAVE, LZ>(L, a, st);
-    default: return launch_tma<VY, DM, SF_MODE_GRAD, LZ>(L, a, st);
+    case SF_MODE_PLAIN: return launch_tma<VY, DM, SF_MODE_PLAIN, LZ, false, LAY>(L, a, st);
+    case SF_MODE_SAVE: return launch_tma<VY, DM, SF_MODE_SAVE, LZ, false, LAY>(L, a, st);
+    default: return launch_tma<VY, DM, SF_MODE_GRAD, LZ, false, LAY>(L, a, st);
     }
 }
 
-template <int VY, int LZ>
+template <int VY, int LZ, int LAY = 0>
 cudaError_t launch_tma_vy(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    if (L.damp == SF_DAMP_ARRAY) return launch_tma_dm<VY, SF_DAMP_ARRAY, LZ>(L, a, st);
-    if (L.damp == SF_DAMP_SEP) return launch_tma_dm<VY, SF_DAMP_SEP, LZ>(L, a, st);
-    return launch_tma_dm<VY, SF_DAMP_NONE, LZ>(L, a, st);
+    if (L.damp == SF_DAMP_ARRAY) return launch_tma_dm<VY, SF_DAMP_ARRAY, LZ, LAY>(L, a, st);
+    if (L.damp == SF_DAMP_SEP) return launch_tma_dm<VY, SF_DAMP_SEP, LZ, LAY>(L, a, st);
+    return launch_tma_dm<VY, SF_DAMP_NONE, LZ, LAY>(L, a, st);
 }
 
-template <int VY, int DM, int MODE>
-int smem_of() { return sftma::Cfg<SF_R, VY, DM, MODE>::SMEM; }
+template <int VY, int DM, int MODE, int LAY>
+int smem_of() { return sftma::Cfg<SF_R, VY, DM, MODE, 32, LAY>::SMEM; }
 
-template <int VY, int DM>
+template <int VY, int DM, int LAY>
 int smem_dm(int mode)
 {
-    return mode == 0 ? smem_of<VY, DM, 0>() : mode == 1 ? smem_of<VY, DM, 1>() : smem_of<VY, DM, 2>();
+    return mode == 0 ? smem_of<VY, DM, 0, LAY>() : mode == 1 ? smem_of<VY, DM, 1, LAY>() : smem_of<VY, DM, 2, LAY>();
 }
 
-template <int VY>
+template <int VY, int LAY = 0>
 int smem_vy(int damp, int mode)
 {
-    if (damp == SF_DAMP_ARRAY) return smem_dm<VY, SF_DAMP_ARRAY>(mode);
-    if (damp == SF_DAMP_SEP) return smem_dm<VY, SF_DAMP_SEP>(mode);
-    return smem_dm<VY, SF_DAMP_NONE>(mode);
+    if (damp == SF_DAMP_ARRAY) return smem_dm<VY, SF_DAMP_ARRAY, LAY>(mode);
+    if (damp == SF_DAMP_SEP) return smem_dm<VY, SF_DAMP_SEP, LAY>(mode);
+    return smem_dm<VY, SF_DAMP_NONE, LAY>(mode);
 }
 
 }  // namespace
@@ -135,6 +135,9 @@ cudaError_t SF_CAT(sf_launch_step_r, SF_R)(const SfLaunch &L, const SfStepArgs &
     if (L.variant == SF_VAR_TMA) {
         if (L.lz == 8) return launch_tma_vy<2, 8>(L, a, st);
         if (L.vy == 1) return launch_tma_vy<1, 32>(L, a, st);
+#if SF_R >= 5
+        if (L.vy == 3) return launch_tma_vy<2, 32, 1>(L, a, st);  // wide layout (Geo LAY = 1)
+#endif
         return launch_tma_vy<2, 32>(L, a, st);
     }
     switch (L.mode) {
@@ -147,5 +150,6 @@ cudaError_t SF_CAT(sf_launch_step_r, SF_R)(const SfLaunch &L, const SfStepArgs &
 int SF_CAT(sf_tma_smem_r, SF_R)(int vy, int damp, int mode)
 {
     if (vy == 1) return smem_vy<1>(damp, mode);
+    if (vy == 3) return SF_R >= 5 ? smem_vy<2, 1>(damp, mode) : 0;
     return smem_vy<2>(damp, mode);
 }

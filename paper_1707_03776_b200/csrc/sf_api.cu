@@ -193,15 +193,20 @@ static int resolve_variant(const sf_handle *h)
 
 static int resolve_vy(const sf_handle *h)
 {
-    return h->vy == 1 ? 1 : 2;
+    if (h->vy == 1) return 1;
+    if (h->vy == 3 && h->r >= 5) return 3;  // the wide layout exists for r >= 5 only
+    return 2;
 }
 
 // TMA kernel tile geometry (stencil_tma.cuh Geo): VY rows per thread (tuning `vy`, auto
 // 2), 7 consumer warps -> BY = 7 VY tile rows; 4 z per lane -> 128-column tiles.
-static const int TILE_NW = 7;
-static int tile_vz(const sf_handle *, int) { return 4; }
+// vy = 3: the wide layout (Geo LAY = 1, r >= 5): 11 consumer warps x 2 rows, 2 z per lane ->
+// 22 x 64 tiles.
+static int tile_nw(int vy) { return vy == 3 ? 11 : 7; }
+static int tile_rows(int vy) { return vy == 3 ? 2 : vy; }  // rows per thread
+static int tile_vz(const sf_handle *, int vy) { return vy == 3 ? 2 : 4; }
 static int tile_tz(const sf_handle *h, int vy) { return 32 * tile_vz(h, vy); }
-static int tile_by(int vy) { return TILE_NW * vy; }
+static int tile_by(int vy) { return tile_nw(vy) * tile_rows(vy); }
 // narrow tiles of the z remainder (Geo<R, 2, 8>): 8 lanes x 4 z, 4 lane rows x 2 rows x 7 warps
 static const int NARROW_TZ = 32, NARROW_BY = 56;
 
@@ -328,14 +333,15 @@ static TileLoc tile_loc(const sf_handle *h, int vy, int64_t off)
     const int64_t ntz = (n2 + tz - 1) / tz;
     const int64_t x = off / (n1 * n2), y = (off / n2) % n1, z = off % n2;
     const int64_t tile = (y / by) * ntz + z / tz;
-    return {(int)(tile * TILE_NW + (y % by) / vy), (int)x, (int)((z % tz) / vz), (int)((y % by) % vy),
+    const int ry = tile_rows(vy);
+    return {(int)(tile * tile_nw(vy) + (y % by) / ry), (int)x, (int)((z % tz) / vz), (int)((y % by) % ry),
             (int)(z % vz)};
 }
 
 static int64_t n_warp_lists(const sf_handle *h, int vy)
 {
     const int tz = tile_tz(h, vy), by = tile_by(vy);
-    return ((h->nb[2] + tz - 1) / tz) * ((h->nb[1] + by - 1) / by) * TILE_NW;
+    return ((h->nb[2] + tz - 1) / tz) * ((h->nb[1] + by - 1) / by) * tile_nw(vy);
 }
 
 // Per-(tile, warp) lists of the injection targets for the TMA kernel's fused injection.
@@ -496,7 +502,8 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     //  next step: no in-kernel interpolation)
 
     if (b.bidir) {
-        if (L.variant != SF_VAR_TMA || zrem) return sf_set_error(SF_ERR_INVALID_ARG, "one-launch schedule needs the TMA kernel without a z split");
+        if (L.variant != SF_VAR_TMA || zrem || L.vy == 3)
+            return sf_set_error(SF_ERR_INVALID_ARG, "one-launch schedule needs the TMA kernel (7-warp layout) without a z split");
         a.bidir = 1;
         a.sig = h->sigc;
         h->last_tiles = (int)(((a.n2 + tile_tz(h, L.vy) - 1) / tile_tz(h, L.vy)) *
@@ -1066,7 +1073,7 @@ extern "C" sf_status sf_create_slab(const sf_desc *d, void *comm, int rank, int 
 extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas)
 {
     if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
-    if (variant < 0 || variant > 2 || vy < 0 || vy > 2 || ctas < 0)
+    if (variant < 0 || variant > 2 || vy < 0 || vy > 3 || ctas < 0)
         return sf_set_error(SF_ERR_INVALID_ARG, "bad tuning (%d, %d, %d)", variant, vy, ctas);
     if (variant == SF_VAR_TMA && !tma_ok(h))
         return sf_set_error(SF_ERR_INVALID_ARG, "TMA variant needs 3D and n2 %% 4 == 0");
@@ -1093,6 +1100,7 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
         cands.push_back({SF_VAR_TMA, 2, 1});
         if (h->r >= 5) cands.push_back({SF_VAR_TMA, 2, 0});  // narrow remainder tiles off
         cands.push_back({SF_VAR_TMA, 1, 1});
+        if (h->r >= 5 && h->ndim == 3) cands.push_back({SF_VAR_TMA, 3, 1});  // wide layout
     }
     cands.push_back({SF_VAR_GENERIC, 0, 1});
     const Cand keep{h->variant, h->vy, h->zsplit ? 1 : 0};

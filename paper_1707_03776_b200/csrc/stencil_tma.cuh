@@ -158,20 +158,24 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
 // remainder of grids whose n2 is not a multiple of 128 (configs[4]: 400 = 3 x 128 + 16),
 // where 128-column tiles would be mostly idle lanes.  8 lanes x 16 B = one 128-B shared-
 // memory wavefront per row, so the lane rows never share a bank phase (conflict-free).
-template <int R, int VY, int LZ = 32>
+// LAY = 1 ("wide", tuning vy = 3, r >= 5): 2 z per lane and 11 consumer warps -- 4 points per
+// thread halve the register queue (2r+1 planes x points) so that 12 warps (3 per SM sub-
+// partition) fit the register file: more warps to hide the FP latency that bounds the
+// 7-warp layout at high order.  Tiles 22 x 64.
+template <int R, int VY, int LZ = 32, int LAY = 0>
 struct Geo {
-    static constexpr int VZ = 4;
-    static constexpr int NW = 7;                        // consumer warps
+    static constexpr int VZ = LAY == 1 ? 2 : 4;
+    static constexpr int NW = LAY == 1 ? 11 : 7;        // consumer warps
     static constexpr int LY = 32 / LZ;                  // lane rows per warp
     static constexpr int BY = NW * LY * VY;             // rows per tile
     static constexpr int TZ = LZ * VZ;                  // columns per tile
     static constexpr int HZ = ((R + 3) / 4) * 4;        // z halo rounded up to 16 B
 };
 
-template <int R, int VY, int DM, int MODE, int LZ = 32>
+template <int R, int VY, int DM, int MODE, int LZ = 32, int LAY = 0>
 struct Cfg {
     static constexpr bool DAMP = (DM == SF_DAMP_ARRAY);  // beta array streamed
-    using G = Geo<R, VY, LZ>;
+    using G = Geo<R, VY, LZ, LAY>;
     static constexpr int VZ = G::VZ, NW = G::NW, BY = G::BY, TZ = G::TZ, HZ = G::HZ;
     static constexpr int W = TZ + 2 * HZ;               // smem row pitch of the u tile
     static constexpr int H = BY + 2 * R;                // rows of the u tile
@@ -300,14 +304,14 @@ __device__ __forceinline__ int seg_dir(const SfStepArgs &a, int it, int tiles, i
     return (a.bidir && nchunk > 1 && it / tiles == nchunk - 1 && w1 == (int64_t)(it % tiles + 1) * PT) ? -1 : 1;
 }
 
-template <int R, int VY, int DM, int MODE, int LZ = 32, bool BIDIR = false>
-__global__ void __launch_bounds__(Cfg<R, VY, DM, MODE, LZ>::THREADS, 1)
+template <int R, int VY, int DM, int MODE, int LZ = 32, bool BIDIR = false, int LAY = 0>
+__global__ void __launch_bounds__(Cfg<R, VY, DM, MODE, LZ, LAY>::THREADS, 1)
 k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_old,
         const __grid_constant__ CUtensorMap tm_c3, const __grid_constant__ CUtensorMap tm_beta,
         const __grid_constant__ CUtensorMap tm_snap, const __grid_constant__ CUtensorMap tm_grad,
         const SfStepArgs a, const int snap_slot, const int chunk, const int nchunk)
 {
-    using C = Cfg<R, VY, DM, MODE, LZ>;
+    using C = Cfg<R, VY, DM, MODE, LZ, LAY>;
     constexpr bool DAMP = C::DAMP;
     constexpr int VZ = C::VZ, NJ = VZ / 2, NW = C::NW, BY = C::BY, TZ = C::TZ, HZ = C::HZ;
     constexpr int Q = C::Q, W = C::W, DU = C::DU, DC = C::DC;

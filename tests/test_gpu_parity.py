@@ -1235,3 +1235,29 @@ def test_autotune_picks_a_configuration_same_bits(shape, so):
     torch.cuda.synchronize()
     assert np.array_equal(rec.cpu().numpy(), ref[0]) and np.array_equal(u.cpu().numpy(), ref[1])
     prop.close()
+
+
+@pytest.mark.parametrize("so", [10, 12, 14, 16])
+def test_wide_layout_bitwise(so):
+    """The wide TMA layout (tuning vy = 3, r >= 5: 2 rows x 2 z per thread, 11 consumer warps,
+    22 x 64 tiles): forward records / final levels / snapshots (SAVE), the gradient (GRAD, with
+    the fused source lists in the forward) are bitwise those of the default layout and of the
+    generic kernel, and match the oracle.  Ragged tiles in y (45 rows) and z (132 columns)."""
+    p = synth.random_problem(3, (37, 45, 132), so, 40, seed=83, nbl=5, nsrc=2, nrec=9)
+    p.m_true = (p.m * 0.93).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    outs = []
+    for variant, vy in ((2, 3), (2, 2), (1, 0)):
+        prop = make_prop(p)
+        prop.set_tuning(variant, vy, 0)
+        assert prop.tuning()["vy"] == (vy if variant == 2 else 0)
+        rec, u, snaps = prop.forward(dev(p.wavelet), save_every=3)
+        g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+        torch.cuda.synchronize()
+        outs.append((rec.cpu().numpy(), u.cpu().numpy(), snaps.cpu().numpy(), g.cpu().numpy(), J))
+        prop.close()
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+    ro, uo, _ = oracle_forward(p)
+    assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
