@@ -269,6 +269,7 @@ struct StepBufs {
     int itp_cur = -1;          // side-stream record index of the `cur` level (SF_OPT_P2P ordering)
     bool force_generic = false;            // thread-per-point kernel (P2P boundary launch)
     bool bidir = false;                    // one-launch slab schedule (SfStepArgs::bidir / sig)
+    bool nosig = false;                    // bidir without the device counters (peer-store form)
     bool dry = false;                      // launch_step: decide (fused, tiles), launch nothing
     const int64_t *mq = nullptr, *md = nullptr;  // peer-store mirror (SfStepArgs::mq / md)
 };
@@ -505,7 +506,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
         if (L.variant != SF_VAR_TMA || zrem || L.vy == 3)
             return sf_set_error(SF_ERR_INVALID_ARG, "one-launch schedule needs the TMA kernel (7-warp layout) without a z split");
         a.bidir = 1;
-        a.sig = h->sigc;
+        a.sig = b.nosig ? nullptr : h->sigc;
         h->last_tiles = (int)(((a.n2 + tile_tz(h, L.vy) - 1) / tile_tz(h, L.vy)) *
                               ((a.n1 + tile_by(L.vy) - 1) / tile_by(L.vy)));
     }
@@ -1455,8 +1456,10 @@ static sf_status do_step_p2p(sf_handle *h, const StepBufs &b, StepBufs bb, StepB
 // the same schedule, the "exchange" being a copy of the boundary planes into a test probe.
 static bool one_launch_ok(sf_handle *h, const StepBufs &b, int mode, cudaStream_t st)
 {
-    if (!h->one_launch || h->p2p || h->ndim != 3 || !h->sigc) return false;
-    if (h->nranks > 1 ? sf_comm_is_local(h->comm) : h->one_launch < 2) return false;
+    if (!h->one_launch || h->ndim != 3 || !h->sigc) return false;
+    // NCCL exchange: separate processes only (local groups keep the two-launch split);
+    // peer stores (SF_OPT_P2P): local groups and processes alike
+    if (h->nranks > 1 ? (!h->p2p && sf_comm_is_local(h->comm)) : h->one_launch < 2) return false;
     StepBufs bd = b;
     bd.bidir = true;
     bd.dry = true;
@@ -1466,8 +1469,64 @@ static bool one_launch_ok(sf_handle *h, const StepBufs &b, int mode, cudaStream_
     return fused || !need;
 }
 
+// Peer-store form of the one-launch schedule (SF_OPT_P2P + SF_OPT_ONE_LAUNCH): the single
+// persistent launch stores its boundary planes a second time, straight into the neighbours'
+// halos of the same level (peer-mapped; the transfer overlaps the stencil tile by tile), then
+// -- in stream order after the launch and after the side-stream record of the level it read
+// (the neighbour overwrites that buffer's halo at its next step: write-after-read) -- bumps
+// the neighbours' counters and waits on its own (RAW: the neighbours' planes have landed).
+static sf_status do_step_onelaunch_p2p(sf_handle *h, StepBufs b, int mode, cudaStream_t st)
+{
+    sf_status s;
+    const int64_t r = h->r;
+    const int ob = b.out == h->p2p_own[0] ? 0 : b.out == h->p2p_own[1] ? 1 : -1;
+    if (ob < 0) return sf_set_error(SF_ERR_INVALID_ARG, "P2P step on a buffer outside the published state");
+    int64_t plan[7], qp[7];
+    if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank, h->nranks, plan))) return s;
+    const int64_t plane = h->N / h->nb[0];
+    auto delta = [](const float *to, const float *from) {
+        return (int64_t)(reinterpret_cast<uintptr_t>(to) - reinterpret_cast<uintptr_t>(from));
+    };
+    int64_t mq[4] = {0, 0, 0, 0}, md[2] = {0, 0};
+    if (plan[5]) {  // owned [r, 2r) -> left neighbour's right halo
+        if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank - 1, h->nranks, qp))) return s;
+        mq[0] = plan[0];
+        mq[1] = plan[0] + r;
+        md[0] = delta(h->p2p_nbr[0][ob] + qp[3] * plane, b.out + plan[0] * plane);
+    }
+    if (plan[6]) {  // owned [nl, nl + r) -> right neighbour's left halo
+        if ((s = sf_slab_halo_plan(h->gshape[0], h->so, h->rank + 1, h->nranks, qp))) return s;
+        mq[2] = plan[2];
+        mq[3] = plan[2] + r;
+        md[1] = delta(h->p2p_nbr[1][ob] + qp[1] * plane, b.out + plan[2] * plane);
+    }
+    StepBufs bm = b;
+    bm.bidir = true;
+    bm.nosig = true;
+    bm.mq = mq;
+    bm.md = md;
+    bool fused = false;
+    if ((s = launch_step(h, bm, mode, st, &fused))) return s;
+    h->n_onelaunch++;
+    if (b.itp_cur >= 0 && h->itp_pending[b.itp_cur & 1])
+        SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_itp[b.itp_cur & 1], 0));
+    SF_CUDA_TRY(cudaEventRecord(h->ev_bnd, st));
+    const uint32_t seq = h->p2p_seq + 1;
+    if (sf_comm_p2p_local(h)) {
+        if ((s = sf_comm_p2p_local_step(h, st, plan[5] != 0, plan[6] != 0))) return s;
+    } else {
+        for (int side = 0; side < 2; ++side)
+            if (h->p2p_nflag[side] && (s = stream_write32(st, h->p2p_nflag[side], seq))) return s;
+        if (plan[5] && (s = stream_wait32(st, h->p2p_flags + 0, seq))) return s;
+        if (plan[6] && (s = stream_wait32(st, h->p2p_flags + 1, seq))) return s;
+    }
+    h->p2p_seq = seq;
+    return SF_OK;
+}
+
 static sf_status do_step_onelaunch(sf_handle *h, StepBufs b, int mode, cudaStream_t st)
 {
+    if (h->p2p && h->nranks > 1) return do_step_onelaunch_p2p(h, b, mode, st);
     sf_status s;
     bool fused = false;
     SF_CUDA_TRY(cudaEventRecord(h->ev_pre, st));  // orders the exchange after earlier readers of `out`

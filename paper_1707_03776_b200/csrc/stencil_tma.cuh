@@ -790,6 +790,15 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                 }
                             }
                         }
+                        if (BIDIR && ((q >= a.mq[0] && q < a.mq[1]) || (q >= a.mq[2] && q < a.mq[3]))) {
+                            // peer-store halo exchange (SF_OPT_P2P): a boundary plane
+                            // is also stored straight into the neighbour's halo of the same level
+                            // (peer-mapped buffer at byte offset md from its own address)
+                            const int64_t db = (q < a.mq[1]) ? a.md[0] : a.md[1];
+#pragma unroll
+                            for (int j = 0; j < VY; ++j)
+                                if (act[j]) stp<VZ>(sf_mirror(optr + j * a.n2, db), res2[j]);
+                        }
                         optr += dplane;
                         if (MODE == SF_MODE_SAVE) sptr += dplane;
                         if (MODE == SF_MODE_GRAD) gptr += dplane;

@@ -591,7 +591,8 @@ def test_slab_decomposition_bitwise_local_transport(nranks, variant, p2p, dense)
     records, the owned planes of both final levels and of the gradient, and J are bitwise
     those of the single-domain run (reading C18).  Sources and receivers straddle the slab
     boundaries.  p2p = 1: SF_OPT_P2P -- the boundary kernel stores the boundary planes
-    straight into the neighbours' halos and the streams order on counters; the
+    straight into the neighbours' halos and the streams order on counters -- with
+    the TMA kernel, from the single persistent launch of each step (one-launch schedule); the
     transport then only runs once per call (the initial halo).  dense = 1: 20 receivers
     inside one grid cell at a rank boundary, so their 8 corners get 20 contributions each
     and the adjoint injection takes the CSR path (no ELL table) in the split launches."""
@@ -633,6 +634,11 @@ def test_slab_decomposition_bitwise_local_transport(nranks, variant, p2p, dense)
         pr.set_profiling(False)
         # transport exchanges: one per step, or only the initial one with peer stores
         assert (other <= 2) if p2p else (other >= p.nt - 1), other
+        if p2p and variant == 2:
+            # peer stores from the ONE persistent TMA launch per step (SF_OPT_ONE_LAUNCH +
+            # SF_OPT_P2P: boundary planes stored into the neighbours' halos by the stencil
+            # kernel itself) on every forward step
+            assert pr.debug_probe(None) == p.nt - 1
         g, J = pr.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
         torch.cuda.current_stream().synchronize()
         res = (x0, nl, rec.cpu().numpy(), u.cpu().numpy()[:, r:r + nl], g.cpu().numpy()[r:r + nl], J)
