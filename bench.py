@@ -454,8 +454,10 @@ def run_ours(args):
                                    "eta array (hoisted beta streamed)" if eta_d is not None else "none"),
                        "halo_exchange": (("peer stores from the boundary kernel + stream counters"
                                           if args.p2p else "NCCL send/recv") if slab else None),
-                       "schedule": (("one launch per step, boundary ranges signalled to the comm stream"
-                                     if (args.one_launch or (slab and not args.p2p)) else
+                       "schedule": (("one launch per step storing its boundary planes into the neighbours' "
+                                     "halos (peer stores), stream-ordered counters" if (slab and args.p2p) else
+                                     "one launch per step, boundary ranges signalled to the comm stream"
+                                     if (args.one_launch or slab) else
                                      "split (boundary planes, then interior)") if split else
                                     "single launch per step") + (", CUDA graph replay" if args.graph else ""),
                        "kernel_tuning": tuning, "autotune": tuned},
