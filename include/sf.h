@@ -247,6 +247,14 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   (default 1 = every launch); sf_get_profile* scale the timed sum by
                                   launches / timed launches.  An event pair between two kernels
                                   costs 1-3 % of a step and defeats PDL.                          */
+#define SF_OPT_LOOP2D 14       /* 1 (default): a small 2D grid (configs[0]: 141 x 141; up to ~200 k
+                                  points) runs the whole sf_forward / sf_adjoint time loop (no
+                                  snapshots, no gradient) in ONE launch of a 16-CTA cluster: each
+                                  CTA holds a slab of rows (both levels, c3, beta) in shared
+                                  memory, reads the neighbouring rows through distributed shared
+                                  memory, and cluster barriers order stencil, injection and
+                                  records step by step (launch-bound otherwise).  Bitwise the
+                                  per-step kernels.  0: one launch per step.                     */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 /* Setup-time tuning (the counterpart of the paper's runtime block-size auto-tuning,
  * P:729-731): times `steps` plain stencil steps (no sparse work) of every feasible launch

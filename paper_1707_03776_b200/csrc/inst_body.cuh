@@ -5,6 +5,7 @@
 #include "launch.cuh"
 #include "stencil_generic.cuh"
 #include "stencil_tma.cuh"
+#include "loop2d.cuh"
 
 #ifndef SF_R
 #error "define SF_R"
@@ -152,4 +153,27 @@ int SF_CAT(sf_tma_smem_r, SF_R)(int vy, int damp, int mode)
     if (vy == 1) return smem_vy<1>(damp, mode);
     if (vy == 3) return SF_R >= 5 ? smem_vy<2, 1>(damp, mode) : 0;
     return smem_vy<2>(damp, mode);
+}
+
+// whole 2D time loop of a small grid in one CTA cluster (loop2d.cuh, SF_OPT_LOOP2D)
+cudaError_t SF_CAT(sf_launch_loop2d_r, SF_R)(const Loop2dArgs &a, cudaStream_t st)
+{
+    const size_t smem = loop2d_smem(a.rpc, a.n2, a.beta != nullptr);
+    auto kern = k_loop2d<SF_R>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(SF_LOOP2D_CTAS);
+    cfg.blockDim = dim3(SF_LOOP2D_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = SF_LOOP2D_CTAS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }

@@ -40,6 +40,18 @@ SF_DECL_LAUNCH(7)
 SF_DECL_LAUNCH(8)
 #undef SF_DECL_LAUNCH
 
+struct Loop2dArgs;
+#define SF_DECL_LOOP(R) cudaError_t sf_launch_loop2d_r##R(const Loop2dArgs &a, cudaStream_t st);
+SF_DECL_LOOP(1)
+SF_DECL_LOOP(2)
+SF_DECL_LOOP(3)
+SF_DECL_LOOP(4)
+SF_DECL_LOOP(5)
+SF_DECL_LOOP(6)
+SF_DECL_LOOP(7)
+SF_DECL_LOOP(8)
+#undef SF_DECL_LOOP
+
 #define SF_DECL_SMEM(R) int sf_tma_smem_r##R(int vy, int damp, int mode);
 SF_DECL_SMEM(1)
 SF_DECL_SMEM(2)

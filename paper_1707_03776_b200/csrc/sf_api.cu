@@ -19,6 +19,7 @@
 
 #include "sf_internal.h"
 #include "sparse.cuh"
+#include "loop2d.cuh"
 
 #define SF_VERSION 1
 #ifndef SF_SIDE_MIN_POINTS
@@ -1207,6 +1208,10 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         if (value < 1) return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_PROF_EVERY %d < 1", value);
         h->prof_every = value;
         return SF_OK;
+    case SF_OPT_LOOP2D:
+        h->loop2d = value != 0;
+        drop_graphs(h);
+        return SF_OK;
     case SF_OPT_PDL:
         h->pdl = value != 0;
         drop_graphs(h);
@@ -1647,6 +1652,71 @@ static sf_status join_side(sf_handle *h, cudaStream_t st)
     return SF_OK;
 }
 
+// SF_OPT_LOOP2D: a small 2D grid (both levels in one CTA's shared memory) runs its whole time
+// loop -- stencil, injection, records -- in one launch (loop2d.cuh; bitwise the per-step path)
+static int loop2d_rpc(const sf_handle *h) { return (int)((h->nb[0] + SF_LOOP2D_CTAS - 1) / SF_LOOP2D_CTAS); }
+static bool loop2d_ok(const sf_handle *h)
+{
+    return h->loop2d && h->ndim == 2 && h->nranks == 1 && h->variant != SF_VAR_TMA &&
+           loop2d_smem(loop2d_rpc(h), (int)h->nb[1], h->beta != nullptr) <= SF_LOOP2D_SMEM_MAX &&
+           h->src.ntgt <= SF_LOOP2D_LOC && h->rec.ntgt <= SF_LOOP2D_LOC;
+}
+
+static sf_status launch_loop2d(sf_handle *h, float *A, float *B, const SfSparse &inj, const float *vals,
+                               const SfSparse &itp, float *rec, bool backward, cudaStream_t st)
+{
+    Loop2dArgs a{};
+    a.n0 = (int)h->nb[0];
+    a.n2 = (int)h->nb[1];
+    a.rpc = loop2d_rpc(h);
+    a.nsteps = h->nt - 1;
+    a.backward = backward ? 1 : 0;
+    a.nt = h->nt;
+    a.w = h->w;
+    a.c3 = h->c3;
+    a.beta = h->beta;
+    a.sigx = h->sig[0];
+    a.sigz = h->sig[2];
+    a.hdt = (float)(0.5 * h->dt);
+    a.A = A;
+    a.B = B;
+    a.ntgt = vals ? inj.ntgt : 0;
+    a.tgt = inj.j_tgt;
+    a.rowptr = inj.j_rowptr;
+    a.pt = inj.j_pt;
+    a.coef = inj.j_coef;
+    a.vals = vals;
+    a.nvals = inj.np;
+    a.np = rec ? itp.np : 0;
+    a.K = itp.ik;
+    a.eidx = itp.e_idx;
+    a.ew = itp.e_w;
+    a.rec = rec;
+    ProfScope ps(h, PK_STENCIL, st);
+    cudaError_t e;
+    switch (h->r) {
+    case 1: e = sf_launch_loop2d_r1(a, st); break;
+    case 2: e = sf_launch_loop2d_r2(a, st); break;
+    case 3: e = sf_launch_loop2d_r3(a, st); break;
+    case 4: e = sf_launch_loop2d_r4(a, st); break;
+    case 5: e = sf_launch_loop2d_r5(a, st); break;
+    case 6: e = sf_launch_loop2d_r6(a, st); break;
+    case 7: e = sf_launch_loop2d_r7(a, st); break;
+    default: e = sf_launch_loop2d_r8(a, st); break;
+    }
+    if (e != cudaSuccess) {
+        // (a device without 16-CTA clusters: fall back to one launch per step for good)
+        if (e == cudaErrorInvalidValue || e == cudaErrorNotSupported || e == cudaErrorInvalidConfiguration ||
+            e == cudaErrorLaunchOutOfResources) {
+            cudaGetLastError();
+            h->loop2d = false;
+            return SF_ERR_INVALID_ARG;  // caller retries on the per-step path
+        }
+        return sf_set_error(SF_ERR_CUDA, "loop2d launch: %s", cudaGetErrorString(e));
+    }
+    return SF_OK;
+}
+
 static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, float *u, float *snaps,
                               int save_every, void *stream)
 {
@@ -1658,6 +1728,10 @@ static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, fl
     const int64_t N = h->N;
     float *A = u, *B = u + N;  // A = u^{-1}, B = u^0
     sf_status s;
+    if (!snaps && loop2d_ok(h)) {
+        s = launch_loop2d(h, A, B, h->src, wavelet, h->rec, rec, false, st);
+        if (s != SF_ERR_INVALID_ARG || h->loop2d) return s;
+    }
     h->itp_pending[0] = h->itp_pending[1] = false;
     if (h->nranks > 1) {  // make the halo of u^0 valid for the first stencil / record
         if (h->p2p && (s = sf_comm_p2p_setup(h, A, B, st))) return s;
@@ -1704,6 +1778,10 @@ static sf_status adjoint_body(sf_handle *h, const float *res, float *srca, float
     const float gscale = dograd ? (float)((double)save_every / (h->dt * h->dt)) : 0.f;
     float *A = v, *B = v + N;  // A = v^{nt}, B = v^{nt-1}
     sf_status s;
+    if (!dograd && loop2d_ok(h)) {
+        s = launch_loop2d(h, A, B, h->rec, res, h->src, srca, true, st);
+        if (s != SF_ERR_INVALID_ARG || h->loop2d) return s;
+    }
     if (h->nranks > 1) {
         if (h->p2p && (s = sf_comm_p2p_setup(h, A, B, st))) return s;
         if ((s = post_step_exchange(h, B, st))) return s;

@@ -113,6 +113,7 @@ struct sf_handle {
     bool zsplit = true;               // SF_OPT_ZSPLIT: narrow tiles for a z remainder <= 64
     // one-launch slab schedule (SF_OPT_ONE_LAUNCH): the stencil launch signals its finished
     // boundary ranges on device counters; the comm stream waits on them, then exchanges
+    bool loop2d = true;               // SF_OPT_LOOP2D: small 2D grids run the whole time loop in one CTA
     bool pdl = true;                  // SF_OPT_PDL: programmatic dependent launches (injection, stencil after it)
     bool prev_inject = false;         // the last kernel launched on the step stream was an injection
     int one_launch = 1;               // 1: in NCCL slab mode when applicable; 2: also on one GPU (emulation)

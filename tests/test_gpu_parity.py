@@ -1267,3 +1267,34 @@ def test_wide_layout_bitwise(so):
             assert np.array_equal(a, b)
     ro, uo, _ = oracle_forward(p)
     assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
+
+
+@pytest.mark.parametrize("so,sep", [(4, False), (8, False), (4, True), (16, False)])
+def test_loop2d_bitwise(so, sep):
+    """SF_OPT_LOOP2D (a small 2D grid runs its whole forward / adjoint time loop in one CTA,
+    both levels in shared memory): records, final levels and the adjoint's source records
+    are bitwise those of the per-step kernels, and the forward matches the oracle.  Damping
+    as the beta array or as separable profiles; ragged extents."""
+    p = synth.random_problem(2, (61, 47), so, 80, seed=91, nbl=6, nsrc=2, nrec=9)
+    res = np.random.default_rng(4).standard_normal((p.nt, 9)).astype(np.float32)
+    outs = []
+    for loop in (1, 0):
+        prop = sf().Propagator(dev(p.m), None if sep else dev(p.damp), shape=p.shape, h=p.h,
+                               space_order=p.space_order, nt=p.nt, dt=p.dt,
+                               src_coords=p.src_coords.astype(np.float64),
+                               rec_coords=p.rec_coords.astype(np.float64), sigma=p.sigma if sep else None)
+        prop.set_option(sf().SF_OPT_LOOP2D, loop)
+        prop.set_profiling(True)
+        prop.profile(reset=True)
+        rec, u, _ = prop.forward(dev(p.wavelet))
+        srca, v, _ = prop.adjoint(dev(res))
+        torch.cuda.synchronize()
+        n = prop.profile(reset=True)["stencil_launches"]
+        assert n == (2 if loop else 2 * (p.nt - 1)), n
+        outs.append([x.cpu().numpy() for x in (rec, u, srca, v)])
+        prop.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    if not sep:
+        ro, uo, _ = oracle_forward(p)
+        assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
