@@ -35,7 +35,7 @@ TOL = 1e-4
 
 
 def _want(ci):
-    return _SEL in ("1", "all") or str(ci) in _SEL.split(",")
+    return _SEL == "all" or (_SEL == "1" and ci != "2h") or str(ci) in _SEL.split(",")
 
 
 def rel(a, b):
@@ -111,7 +111,9 @@ def _forward_case(ci):
     assert out["u_last_rel_l2"] <= TOL and out["u_prev_rel_l2"] <= TOL
 
 
-def _gradient_case(ci, shot=0):
+def _gradient_case(ci, shot=0, half=False, tag=None):
+    """half: fp16 snapshots on both sides (SF_OPT_SNAP_HALF / reading C23) and the GPU's
+    checkpointed gradient (sf_gradient_ckpt, segment 40) instead of sf_gradient."""
     p = synth.make_config(ci, shot=shot) if ci == 4 else synth.make_config(ci)
     k = p.save_every
     t0 = time.time()
@@ -121,7 +123,12 @@ def _gradient_case(ci, shot=0):
     pt.close()
     prop = make_prop(p)
     tun = prop.tuning()
-    g, J = prop.gradient(dev(p.wavelet), d_obs_g, save_every=k)
+    if half:
+        import paper_1707_03776_b200 as sf
+        prop.set_option(sf.SF_OPT_SNAP_HALF, 1)
+        g, J = prop.gradient_ckpt(dev(p.wavelet), d_obs_g, save_every=k, segment=10 * k)
+    else:
+        g, J = prop.gradient(dev(p.wavelet), d_obs_g, save_every=k)
     torch.cuda.synchronize()
     gg = g.cpu().numpy()
     dg = d_obs_g.cpu().numpy()
@@ -150,7 +157,7 @@ def _gradient_case(ci, shot=0):
         # oracle: its own d_obs, checkpointed gradient
         d_obs_o = oracle.forward(p, m=p.m_true)["rec"]
         S = ckpt_segment(p.nt, k)
-        go = oracle.gradient(p, d_obs_o, save_every=k, checkpoint=S)
+        go = oracle.gradient(p, d_obs_o, save_every=k, checkpoint=S, snap_dtype="float16" if half else None)
         rres, src = float(np.linalg.norm(go["res"]) / np.linalg.norm(d_obs_o)), "in-process"
         t2 = time.time()
         pre = {}
@@ -159,7 +166,9 @@ def _gradient_case(ci, shot=0):
            "d_obs": trace_stats(dg, d_obs_o), "d_syn_oracle_rel_residual": rres,
            "grad_rel_l2": rel(gg, go["grad"]), "J_gpu": J, "J_oracle": go["J"],
            "J_rel_err": abs(J - go["J"]) / go["J"], "gpu_s": t1 - t0, "oracle_s": t2 - t1, **pre}
-    _dump(ci, out)
+    if half:
+        out["variant"] = "fp16 snapshots (both sides), GPU sf_gradient_ckpt segment %d" % (10 * k)
+    _dump(tag or ci, out)
     assert out["d_obs"]["rel_l2"] <= TOL
     assert out["grad_rel_l2"] <= TOL and out["J_rel_err"] <= TOL
 
@@ -177,6 +186,11 @@ def test_config1_full():
 @pytest.mark.skipif(not _want(2), reason="not selected")
 def test_config2_full_gradient():
     _gradient_case(2)
+
+
+@pytest.mark.skipif(not _want("2h"), reason="not selected")
+def test_config2_full_gradient_fp16_ckpt():
+    _gradient_case(2, half=True, tag="2h")
 
 
 @pytest.mark.skipif(not _want(3), reason="not selected")
