@@ -15,13 +15,17 @@
 
 namespace {
 
-template <int VY, int DM, int MODE, int LZ, bool BIDIR = false, int LAY = 0>
+template <int VY, int DM, int MODE, int LZ, int BIDIR = 0, int LAY = 0>
 cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
-    if constexpr (!BIDIR && LZ == 32 && LAY == 0) {
+    if constexpr (BIDIR == 0 && LZ == 32 && LAY == 0) {
         // the one-launch slab schedule has its own instances (direction and boundary-signal
-        // code compiled out of the plain ones: it cost up to 7 % at r = 8 when only inactive)
-        if (a.bidir) return launch_tma<VY, DM, MODE, LZ, true>(L, a, st);
+        // code compiled out of the plain ones: it cost up to 7 % at r = 8 when only inactive;
+        // the per-plane peer-store test another 12 %: a third instance for SF_OPT_P2P)
+        if (a.bidir) {
+            if (a.mq[1] > a.mq[0] || a.mq[3] > a.mq[2]) return launch_tma<VY, DM, MODE, LZ, 2>(L, a, st);
+            return launch_tma<VY, DM, MODE, LZ, 1>(L, a, st);
+        }
     }
     using C = sftma::Cfg<SF_R, VY, DM, MODE, LZ, LAY>;
     auto kern = sftma::k_tma3d<SF_R, VY, DM, MODE, LZ, BIDIR, LAY>;
@@ -96,9 +100,9 @@ template <int VY, int DM, int LZ, int LAY = 0>
 cudaError_t launch_tma_dm(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     switch (L.mode) {
-    case SF_MODE_PLAIN: return launch_tma<VY, DM, SF_MODE_PLAIN, LZ, false, LAY>(L, a, st);
-    case SF_MODE_SAVE: return launch_tma<VY, DM, SF_MODE_SAVE, LZ, false, LAY>(L, a, st);
-    default: return launch_tma<VY, DM, SF_MODE_GRAD, LZ, false, LAY>(L, a, st);
+    case SF_MODE_PLAIN: return launch_tma<VY, DM, SF_MODE_PLAIN, LZ, 0, LAY>(L, a, st);
+    case SF_MODE_SAVE: return launch_tma<VY, DM, SF_MODE_SAVE, LZ, 0, LAY>(L, a, st);
+    default: return launch_tma<VY, DM, SF_MODE_GRAD, LZ, 0, LAY>(L, a, st);
     }
 }
 

@@ -304,7 +304,10 @@ __device__ __forceinline__ int seg_dir(const SfStepArgs &a, int it, int tiles, i
     return (a.bidir && nchunk > 1 && it / tiles == nchunk - 1 && w1 == (int64_t)(it % tiles + 1) * PT) ? -1 : 1;
 }
 
-template <int R, int VY, int DM, int MODE, int LZ = 32, bool BIDIR = false, int LAY = 0>
+// BIDIR: 0 plain; 1 one-launch slab schedule (downward last chunk, boundary signals); 2 the
+// same + peer stores of the boundary planes (SF_OPT_P2P) -- separate instances, so that
+// neither the plain kernel nor the NCCL form pays for code it does not run
+template <int R, int VY, int DM, int MODE, int LZ = 32, int BIDIR = 0, int LAY = 0>
 __global__ void __launch_bounds__(Cfg<R, VY, DM, MODE, LZ, LAY>::THREADS, 1)
 k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtensorMap tm_old,
         const __grid_constant__ CUtensorMap tm_c3, const __grid_constant__ CUtensorMap tm_beta,
@@ -790,7 +793,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                 }
                             }
                         }
-                        if (BIDIR && ((q >= a.mq[0] && q < a.mq[1]) || (q >= a.mq[2] && q < a.mq[3]))) {
+                        if (BIDIR == 2 && ((q >= a.mq[0] && q < a.mq[1]) || (q >= a.mq[2] && q < a.mq[3]))) {
                             // peer-store halo exchange (SF_OPT_P2P): a boundary plane
                             // is also stored straight into the neighbour's halo of the same level
                             // (peer-mapped buffer at byte offset md from its own address)
