@@ -312,6 +312,8 @@ def run_ours(args):
         # setup-time tuning (sf_autotune; the paper's runtime block-size tuning):
         # outside the timed region, same bits for every choice
         tuned = prop.autotune(steps=10)
+    if args.tblock:
+        prop.set_option(15, 1)  # SF_OPT_TBLOCK: two steps per launch (forward without snapshots)
     wav = dev(p.wavelet)
     u = prop.zeros_state()
     rec = torch.empty((p.nt, p.rec_coords.shape[0]), device="cuda")
@@ -396,13 +398,16 @@ def run_ours(args):
     # wall time per update (every main-stream kernel of the step, gaps included); the tighter
     # one is reported
     sampled_ms = prof["stencil_ms"] / max(prof["stencil_launches"], 1)
-    wall_ms = ms_max / (args.steps * (p.nt - 1) * passes)
+    upl = 2 if args.tblock else 1            # updates per stencil launch
+    wall_ms = ms_max / (args.steps * (p.nt - 1) * passes) * upl
     launch_ms = min(sampled_ms, wall_ms)
     split = args.split or slab
     if split:
         # boundary and interior launches overlap: time the stencil by the wall time per update
         launch_ms = wall_ms
     alg_bytes = bpp * npts_local
+    if args.tblock:
+        alg_bytes = (bpp + 4) * npts_local   # two updates: u^{n-1}, u^n, c3 (, beta) read, two levels written
     if grad_mode:
         # forward: nt-1 launches, (nt-1)//k of them also store a snapshot (+4 B/pt); adjoint:
         # nt-1 launches, (nt-1)//k of them also read the snapshot and update the gradient
@@ -459,6 +464,7 @@ def run_ours(args):
                                      "one launch per step, boundary ranges signalled to the comm stream"
                                      if (args.one_launch or slab) else
                                      "split (boundary planes, then interior)") if split else
+                                    "two steps per launch (temporal blocking)" if args.tblock else
                                     "single launch per step") + (", CUDA graph replay" if args.graph else ""),
                        "kernel_tuning": tuning, "autotune": tuned},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -647,6 +653,9 @@ def main():
     ap.add_argument("--sep", action="store_true",
                     help="damped configs: regenerate beta in-kernel from the separable damping "
                          "profiles (16 B/pt) instead of streaming the hoisted beta array (20 B/pt)")
+    ap.add_argument("--tblock", action="store_true",
+                    help="forward configs: two time steps per launch (SF_OPT_TBLOCK, temporal "
+                         "blocking; r <= 4, one GPU) -- measured slower, A/B only")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-steps-nt", type=int, default=6,
                     help="--impl reference: time samples per timed step of the oracle")

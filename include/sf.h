@@ -255,6 +255,16 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   memory, and cluster barriers order stencil, injection and
                                   records step by step (launch-bound otherwise).  Bitwise the
                                   per-step kernels.  0: one launch per step.                     */
+#define SF_OPT_TBLOCK 15       /* temporal blocking, default 0: 1 runs sf_forward without
+                                  snapshots two time steps per launch (3D, space order <= 8, one
+                                  GPU, no separable profiles, n_z % 4 == 0; SF_ERR_INVALID_ARG
+                                  otherwise): each CTA computes step 1 on its tile grown by r
+                                  rows / 4 columns per side and step 2 on the tile from one read
+                                  of u^{n-1}, u^n, c3, beta (24 B per two updates instead of 40),
+                                  bitwise equal to two single steps.  Allocates a second state
+                                  pair (2 N floats) when set; an odd step count ends with one
+                                  single step.  Measured slower than the single-step kernel on
+                                  B200, hence off by default.              */
 SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
 /* Setup-time tuning (the counterpart of the paper's runtime block-size auto-tuning,
  * P:729-731): times `steps` plain stencil steps (no sparse work) of every feasible launch

@@ -34,7 +34,7 @@ EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint
 
 SF_OPT_L2_PREFETCH, SF_OPT_SPLIT, SF_OPT_FUSE_MAX, SF_OPT_COMM_SMS, SF_OPT_GRAPH, SF_OPT_SNAP_HALF, SF_OPT_P2P, SF_OPT_ZSPLIT = \
     1, 2, 3, 4, 5, 7, 8, 9
-SF_OPT_ONE_LAUNCH, SF_OPT_PDL, SF_OPT_PROF_EVERY, SF_OPT_LOOP2D = 11, 12, 13, 14
+SF_OPT_ONE_LAUNCH, SF_OPT_PDL, SF_OPT_PROF_EVERY, SF_OPT_LOOP2D, SF_OPT_TBLOCK = 11, 12, 13, 14, 15
 
 
 class SfError(RuntimeError):

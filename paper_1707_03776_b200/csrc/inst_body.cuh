@@ -6,6 +6,9 @@
 #include "stencil_generic.cuh"
 #include "stencil_tma.cuh"
 #include "loop2d.cuh"
+#if SF_R <= 4
+#include "stencil_tb2.cuh"
+#endif
 
 #ifndef SF_R
 #error "define SF_R"
@@ -181,3 +184,44 @@ cudaError_t SF_CAT(sf_launch_loop2d_r, SF_R)(const Loop2dArgs &a, cudaStream_t s
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
+
+#if SF_R <= 4
+// two steps per pass (temporal blocking, stencil_tb2.cuh, SF_OPT_TBLOCK): persistent grid of
+// (tile, x-chunk) items; the chunk count minimises rounds x (chunk + 4r)
+cudaError_t SF_CAT(sf_launch_tb2_r, SF_R)(const SfTmaMaps &m, const TbArgs &a0, int ctas, cudaStream_t st)
+{
+    TbArgs a = a0;
+    const bool damp = a.beta != nullptr;
+    const int64_t tiles = (int64_t)((a.n2 + sftb::TZ - 1) / sftb::TZ) * ((a.n1 + sftb::TY - 1) / sftb::TY);
+    if (tiles <= 0 || a.n0 <= 0) return cudaSuccess;
+    double best = 1e300;
+    int chunk = a.n0, nch = 1;
+    for (int c = 1; c <= std::min(a.n0, 64); ++c) {
+        const int ch = (a.n0 + c - 1) / c, ce = (a.n0 + ch - 1) / ch;
+        const int64_t items = tiles * ce, g = std::min<int64_t>(items, ctas);
+        const double t = (double)((items + g - 1) / g) * (double)(ch + 4 * SF_R);
+        if (t < best - 1e-9) {
+            best = t;
+            chunk = ch;
+            nch = ce;
+        }
+    }
+    a.chunk = chunk;
+    a.nchunk = nch;
+    const int64_t g = std::min<int64_t>(tiles * nch, ctas);
+    int smem;
+    cudaError_t e;
+    if (damp) {
+        smem = sftb::TbCfg<SF_R, true>::SMEM;
+        e = cudaFuncSetAttribute(sftb::k_tb2<SF_R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        sftb::k_tb2<SF_R, true><<<(unsigned)g, 256, smem, st>>>(m.cur, m.old, m.c3, m.beta, a);
+    } else {
+        smem = sftb::TbCfg<SF_R, false>::SMEM;
+        e = cudaFuncSetAttribute(sftb::k_tb2<SF_R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        sftb::k_tb2<SF_R, false><<<(unsigned)g, 256, smem, st>>>(m.cur, m.old, m.c3, m.c3, a);
+    }
+    return cudaGetLastError();
+}
+#endif

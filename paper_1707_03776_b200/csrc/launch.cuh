@@ -52,6 +52,28 @@ SF_DECL_LOOP(7)
 SF_DECL_LOOP(8)
 #undef SF_DECL_LOOP
 
+// two steps per pass (temporal blocking, stencil_tb2.cuh), r <= 4
+struct TbArgs {
+    int n0, n1, n2;
+    SfWeights w;
+    const float *c3, *beta;    // step 2's coefficients (beta NULL: no damping array)
+    float *o1, *o2;            // u^{n+1}, u^{n+2}
+    int chunk, nchunk;
+    // fused injection: per tile, entries [beg[tile], beg[tile + 1]) sorted by plane:
+    // plane e_q, position e_p = ey * 128 + ec in the grown tile, CSR row e_t
+    const int *beg, *e_q, *e_p, *e_t;
+    const int *rowptr, *pt;
+    const float *coef;
+    const float *vals1, *vals2;  // source values of step 1 / step 2 (NULL: none)
+};
+
+#define SF_DECL_TB(R) cudaError_t sf_launch_tb2_r##R(const SfTmaMaps &m, const TbArgs &a, int ctas, cudaStream_t st);
+SF_DECL_TB(1)
+SF_DECL_TB(2)
+SF_DECL_TB(3)
+SF_DECL_TB(4)
+#undef SF_DECL_TB
+
 #define SF_DECL_SMEM(R) int sf_tma_smem_r##R(int vy, int damp, int mode);
 SF_DECL_SMEM(1)
 SF_DECL_SMEM(2)

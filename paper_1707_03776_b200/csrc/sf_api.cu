@@ -810,6 +810,11 @@ extern "C" void sf_destroy(sf_handle *h)
     cudaFree(h->dJ);
     free_sparse(h->src);
     free_sparse(h->rec);
+    cudaFree(h->tb_buf);
+    cudaFree(h->tb_beg);
+    cudaFree(h->tb_q);
+    cudaFree(h->tb_p);
+    cudaFree(h->tb_t);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->ev_ready) cudaEventDestroy(h->ev_ready);
     for (int k = 0; k < 2; ++k)
@@ -1160,6 +1165,8 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
     return SF_OK;
 }
 
+static sf_status ensure_tb(sf_handle *h);
+
 extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
 {
     if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
@@ -1227,6 +1234,14 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         return SF_OK;
     case SF_OPT_SNAP_HALF:
         h->snap_half = value != 0;
+        drop_graphs(h);
+        return SF_OK;
+    case SF_OPT_TBLOCK:
+        if (value) {
+            sf_status st = ensure_tb(h);
+            if (st) return st;
+        }
+        h->tblock = value != 0;
         drop_graphs(h);
         return SF_OK;
     case SF_OPT_GRAPH:
@@ -1721,6 +1736,182 @@ static sf_status launch_loop2d(sf_handle *h, float *A, float *B, const SfSparse 
     return SF_OK;
 }
 
+// ------------------------------------------------------------------ two steps per pass (SF_OPT_TBLOCK)
+// stencil_tb2.cuh: tiles of 8 rows x 120 columns, step 1 on the tile grown by r rows and
+// 4 columns per side (8 + 2r rows x 128 columns)
+static const int TB_TY = 8, TB_TZ = 120, TB_MZ = 4;
+
+static bool tb_ok(const sf_handle *h)
+{
+    return h->ndim == 3 && h->r <= 4 && h->nranks == 1 && !h->sep && h->nb[2] % 4 == 0 &&
+           resolve_variant(h) == SF_VAR_TMA;
+}
+
+// the second state pair and the per-tile source lists: entries (plane, ey * 128 + ec, CSR row)
+// for every tile whose grown region holds the target, sorted by (tile, plane)
+static sf_status ensure_tb(sf_handle *h)
+{
+    if (!tb_ok(h))
+        return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_TBLOCK: needs a 3D one-GPU handle, space order <= 8, "
+                                                "no separable profiles, n_z %% 4 == 0, the TMA kernel");
+    if (h->tb_buf) return SF_OK;
+    SF_CUDA_TRY(cudaMalloc((void **)&h->tb_buf, 2 * sizeof(float) * h->N));
+    const int64_t n1 = h->nb[1], n2 = h->nb[2], R = h->r;
+    const int64_t ntz = (n2 + TB_TZ - 1) / TB_TZ, nty = (n1 + TB_TY - 1) / TB_TY, tiles = ntz * nty;
+    struct E {
+        int64_t tile;
+        int q, p, t;
+    };
+    std::vector<E> es;
+    for (size_t t = 0; t < h->src.h_tgt.size(); ++t) {
+        const int64_t g = h->src.h_tgt[t];
+        const int64_t x = g / (n1 * n2), y = (g / n2) % n1, z = g % n2;
+        for (int64_t ty = std::max<int64_t>(0, (y - R) / TB_TY - 1); ty < nty && ty * TB_TY - R <= y; ++ty)
+            for (int64_t tz = std::max<int64_t>(0, (z - TB_MZ) / TB_TZ - 1); tz < ntz && tz * TB_TZ - TB_MZ <= z; ++tz) {
+                const int64_t ey = y - (ty * TB_TY - R), ec = z - (tz * TB_TZ - TB_MZ);
+                if (ey < 0 || ey >= TB_TY + 2 * R || ec < 0 || ec >= 128) continue;
+                es.push_back({ty * ntz + tz, (int)x, (int)(ey * 128 + ec), (int)t});
+            }
+    }
+    std::sort(es.begin(), es.end(), [](const E &a, const E &b) {
+        return std::tie(a.tile, a.q, a.p) < std::tie(b.tile, b.q, b.p);
+    });
+    std::vector<int> beg(tiles + 1, 0), q, p, tt;
+    for (const E &e : es) beg[e.tile + 1]++;
+    for (int64_t i = 0; i < tiles; ++i) beg[i + 1] += beg[i];
+    for (const E &e : es) {
+        q.push_back(e.q);
+        p.push_back(e.p);
+        tt.push_back(e.t);
+    }
+    sf_status s;
+    if ((s = upload(&h->tb_beg, beg))) return s;
+    if (!es.empty()) {
+        if ((s = upload(&h->tb_q, q))) return s;
+        if ((s = upload(&h->tb_p, p))) return s;
+        if ((s = upload(&h->tb_t, tt))) return s;
+    }
+    return SF_OK;
+}
+
+// one two-step launch: (u^{n-1} = X, u^n = Y) -> (u^{n+1} = Z, u^{n+2} = W); source rows
+// v1 (step n) and v2 (step n + 1), or NULL
+static sf_status launch_tb(sf_handle *h, const float *X, const float *Y, float *Z, float *W, const float *v1,
+                           const float *v2, cudaStream_t st)
+{
+    const int R = h->r, EY = TB_TY + 2 * R;
+    SfTmaMaps m;
+    memset(&m, 0, sizeof m);
+    const int64_t d3[3] = {h->nb[2], h->nb[1], h->nb[0]};
+    const uint32_t bu[3] = {128 + 2 * TB_MZ, (uint32_t)(EY + 2 * R), 1};
+    const uint32_t bc[3] = {128, (uint32_t)EY, 1};
+    sf_status s;
+    if ((s = make_map(&m.cur, Y, 3, d3, bu))) return s;
+    if ((s = make_map(&m.old, X, 3, d3, bc))) return s;
+    if ((s = make_map(&m.c3, h->c3, 3, d3, bc))) return s;
+    if (h->beta && (s = make_map(&m.beta, h->beta, 3, d3, bc))) return s;
+    TbArgs a{};
+    a.n0 = (int)h->nb[0];
+    a.n1 = (int)h->nb[1];
+    a.n2 = (int)h->nb[2];
+    a.w = h->w;
+    a.c3 = h->c3;
+    a.beta = h->beta;
+    a.o1 = Z;
+    a.o2 = W;
+    if (h->src.ntgt > 0 && (v1 || v2)) {
+        a.beg = h->tb_beg;
+        a.e_q = h->tb_q;
+        a.e_p = h->tb_p;
+        a.e_t = h->tb_t;
+        a.rowptr = h->src.j_rowptr;
+        a.pt = h->src.j_pt;
+        a.coef = h->src.j_coef;
+        a.vals1 = v1;
+        a.vals2 = v2;
+    }
+    cudaError_t e;
+    {
+        ProfScope ps(h, PK_STENCIL, st);
+        switch (R) {
+        case 1: e = sf_launch_tb2_r1(m, a, resolve_ctas(h), st); break;
+        case 2: e = sf_launch_tb2_r2(m, a, resolve_ctas(h), st); break;
+        case 3: e = sf_launch_tb2_r3(m, a, resolve_ctas(h), st); break;
+        default: e = sf_launch_tb2_r4(m, a, resolve_ctas(h), st); break;
+        }
+    }
+    if (e != cudaSuccess) return sf_set_error(SF_ERR_CUDA, "two-step launch: %s", cudaGetErrorString(e));
+    h->n_tb++;
+    return SF_OK;
+}
+
+// records of the levels a launch wrote (side stream, overlapping the next launch); the
+// launch that overwrites that buffer pair waits for them (ev_itp[pair])
+static sf_status tb_records(sf_handle *h, const float *l1, float *r1, const float *l2, float *r2, int pair,
+                            cudaStream_t st)
+{
+    if (h->rec.np == 0 || !r1) return SF_OK;
+    SF_CUDA_TRY(cudaEventRecord(h->ev_ready, st));
+    SF_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_ready, 0));
+    sf_status s;
+    if ((s = launch_interp(h, h->rec, l1, r1, h->side))) return s;
+    if (l2 && (s = launch_interp(h, h->rec, l2, r2, h->side))) return s;
+    SF_CUDA_TRY(cudaEventRecord(h->ev_itp[pair], h->side));
+    h->itp_pending[pair] = true;
+    return SF_OK;
+}
+
+static sf_status tb_wait(sf_handle *h, int pair, cudaStream_t st)
+{
+    if (!h->itp_pending[pair]) return SF_OK;
+    SF_CUDA_TRY(cudaStreamWaitEvent(st, h->ev_itp[pair], 0));
+    h->itp_pending[pair] = false;
+    return SF_OK;
+}
+
+// sf_forward without snapshots, two steps per launch: the state pair alternates between the
+// caller's u (pair 0) and tb_buf (pair 1); an odd step count ends with one single step, and
+// the final (u^{nt-2}, u^{nt-1}) is moved back into u
+static sf_status forward_tb(sf_handle *h, const float *wavelet, float *rec, float *u, cudaStream_t st)
+{
+    const int64_t N = h->N;
+    float *PR[2][2] = {{u, u + N}, {h->tb_buf, h->tb_buf + N}};
+    const int np = h->src.np, nr = h->rec.np;
+    sf_status s;
+    h->itp_pending[0] = h->itp_pending[1] = false;
+    int pp = 0;  // pair holding (u^{n-1}, u^n)
+    if ((s = tb_records(h, PR[0][1], rec, nullptr, nullptr, 0, st))) return s;
+    int n = 0;
+    for (; n + 2 <= h->nt - 1; n += 2) {
+        const int o = pp ^ 1;
+        if ((s = tb_wait(h, o, st))) return s;
+        const float *v1 = wavelet ? wavelet + (int64_t)n * np : nullptr;
+        const float *v2 = wavelet ? wavelet + (int64_t)(n + 1) * np : nullptr;
+        if ((s = launch_tb(h, PR[pp][0], PR[pp][1], PR[o][0], PR[o][1], v1, v2, st))) return s;
+        if ((s = tb_records(h, PR[o][0], rec ? rec + (int64_t)(n + 1) * nr : nullptr, PR[o][1],
+                            rec ? rec + (int64_t)(n + 2) * nr : nullptr, o, st)))
+            return s;
+        pp = o;
+    }
+    float *prev = PR[pp][0], *last = PR[pp][1];
+    if (n < h->nt - 1) {  // one single step in place: u^{n+1} over u^{n-1}
+        if ((s = tb_wait(h, pp, st))) return s;
+        const float *wrow = wavelet ? wavelet + (int64_t)n * np : nullptr;
+        float *rrow = rec ? rec + (int64_t)(n + 1) * nr : nullptr;
+        StepBufs b{PR[pp][1], PR[pp][0], nullptr, nullptr, 0, 0, nullptr, 0.f, &h->src, wrow, &h->rec, rrow};
+        if ((s = do_step(h, b, SF_MODE_PLAIN, nullptr, nullptr, st))) return s;
+        if ((s = tb_records(h, PR[pp][0], rrow, nullptr, nullptr, pp, st))) return s;
+        prev = PR[pp][1];
+        last = PR[pp][0];
+    }
+    if ((s = join_side(h, st))) return s;
+    if (prev == u && last == u + N) return SF_OK;
+    if (prev == u + N && last == u) return swap_halves(h, u, u + N, st);
+    SF_CUDA_TRY(cudaMemcpyAsync(u, prev, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
+    SF_CUDA_TRY(cudaMemcpyAsync(u + N, last, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
+    return SF_OK;
+}
+
 static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, float *u, float *snaps,
                               int save_every, void *stream)
 {
@@ -1736,6 +1927,7 @@ static sf_status forward_body(sf_handle *h, const float *wavelet, float *rec, fl
         s = launch_loop2d(h, A, B, h->src, wavelet, h->rec, rec, false, st);
         if (s != SF_ERR_INVALID_ARG || h->loop2d) return s;
     }
+    if (!snaps && h->tblock && tb_ok(h)) return forward_tb(h, wavelet, rec, u, st);
     h->itp_pending[0] = h->itp_pending[1] = false;
     if (h->nranks > 1) {  // make the halo of u^0 valid for the first stencil / record
         if (h->p2p && (s = sf_comm_p2p_setup(h, A, B, st))) return s;

@@ -129,6 +129,12 @@ struct sf_handle {
     float *p2p_nbr[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [left/right][A/B] of the neighbours
     uint32_t *p2p_nflag[2] = {nullptr, nullptr};             // the neighbours' counters this rank writes
     std::vector<std::pair<std::string, void *>> ipc_open;    // opened IPC handles (NCCL mode), closed at destroy
+    // two steps per pass (SF_OPT_TBLOCK, stencil_tb2.cuh): the second buffer pair the
+    // forward rotates through, and the per-tile source lists of the two-step kernel
+    bool tblock = false;
+    float *tb_buf = nullptr;          // [2][N]
+    int *tb_beg = nullptr, *tb_q = nullptr, *tb_p = nullptr, *tb_t = nullptr;
+    long long n_tb = 0;               // two-step launches so far
 };
 
 // error reporting (thread-local message)

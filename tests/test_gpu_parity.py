@@ -1298,3 +1298,47 @@ def test_loop2d_bitwise(so, sep):
     if not sep:
         ro, uo, _ = oracle_forward(p)
         assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
+
+
+@pytest.mark.parametrize("so,damp,shape,nt", [
+    (8, True, (30, 21, 252), 41),    # 3 z tiles (the last 12 columns), 3 y tiles (ragged), odd step count
+    (8, False, (25, 17, 132), 40),   # no damping array, even step count (ends with one single step)
+    (6, True, (22, 33, 256), 27),
+    (4, True, (19, 26, 248), 31),
+    (2, True, (14, 9, 124), 20),
+    (8, True, (12, 10, 120), 3),     # one two-step launch
+    (8, True, (12, 10, 120), 2),     # one single step only
+])
+def test_tblock_bitwise(so, damp, shape, nt):
+    """SF_OPT_TBLOCK (two time steps per launch, stencil_tb2.cuh): records and final levels
+    bitwise those of the single-step path, sources in many tiles (random wavelets, sources
+    on the grown tiles' halos), and the forward matches the oracle."""
+    p = synth.random_problem(3, shape, so, nt, seed=so + nt, nbl=2 if damp else 0, nsrc=12, nrec=9,
+                             damp=damp, random_wavelet=True)
+    outs = []
+    for tb in (1, 0):
+        prop = make_prop(p)
+        if tb:
+            prop.set_option(sf().SF_OPT_TBLOCK, 1)
+        prop.set_profiling(True)
+        prop.profile(reset=True)
+        rec, u, _ = prop.forward(dev(p.wavelet))
+        torch.cuda.synchronize()
+        n = prop.profile(reset=True)["stencil_launches"]
+        if tb:
+            assert n == (nt - 1) // 2 + (nt - 1) % 2, n
+        outs.append([x.cpu().numpy() for x in (rec, u)])
+        prop.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    ro, uo, _ = oracle_forward(p)
+    assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
+
+
+def test_tblock_rejects_unsupported():
+    """SF_OPT_TBLOCK needs space order <= 8, 3D, n_z % 4 == 0: an error, not a fallback."""
+    p = synth.random_problem(3, (12, 10, 64), 10, 5, seed=1, nbl=2)
+    prop = make_prop(p)
+    with pytest.raises(sf().SfError):
+        prop.set_option(sf().SF_OPT_TBLOCK, 1)
+    prop.close()
