@@ -2272,8 +2272,11 @@ struct HostCache {
     cudaEvent_t evh = nullptr;    // uploads done (orders sf_create's legacy-stream work)
 };
 // one cache per device: its buffers, stream and events belong to the device that was
-// current when they were created (cudaMalloc is synchronous, so a buffer is usable on any
-// stream of its device as soon as ensure() returns)
+// current when they were created.  The buffers come from the plain (cudaMalloc) /
+// (cudaFree), not from the stream-ordered pool the macros above route to: cudaMalloc is
+// synchronous, so a buffer is usable on any stream of its device (the caller's stream may
+// be non-blocking) as soon as ensure() returns, and cudaFree waits for the device, so a
+// buffer still read by earlier work on another stream is never released under it
 constexpr int SF_HC_DEVICES = 64;
 HostCache g_hcs[SF_HC_DEVICES];
 
@@ -2281,10 +2284,10 @@ sf_status ensure(float **p, size_t *cap, size_t n)
 {
     if (n == 0) return SF_OK;
     if (*cap >= n) return SF_OK;
-    cudaFree(*p);
+    if (*p) SF_CUDA_TRY((cudaFree)(*p));
     *p = nullptr;
     *cap = 0;
-    SF_CUDA_TRY(cudaMalloc(p, n * sizeof(float)));
+    SF_CUDA_TRY((cudaMalloc)((void **)p, n * sizeof(float)));
     *cap = n;
     return SF_OK;
 }
