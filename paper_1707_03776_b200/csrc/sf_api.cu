@@ -1791,6 +1791,9 @@ static sf_status ensure_tb(sf_handle *h)
         if ((s = upload(&h->tb_p, p))) return s;
         if ((s = upload(&h->tb_t, tt))) return s;
     }
+    // the pool allocations are ordered on the legacy stream: complete them before the
+    // caller's (possibly non-blocking) stream uses the buffers
+    SF_CUDA_TRY(cudaStreamSynchronize(cudaStreamLegacy));
     return SF_OK;
 }
 
