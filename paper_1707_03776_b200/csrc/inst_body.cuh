@@ -66,7 +66,7 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
         }
     }
     const int64_t g = std::min(tiles * nch, slots);
-    dim3 block(32, C::NW + 1);  // NW consumer warps + 1 TMA producer warp
+    dim3 block(32, C::THREADS / 32);  // NW consumer warps + the TMA producer warp(s)
     // programmatic dependent launch (SF_OPT_PDL): the CTAs' prologue (barrier init, tensor-map
     // prefetch) overlaps the previous kernel's tail; they wait (griddepcontrol.wait) before
     // their first global access
@@ -141,8 +141,9 @@ int smem_vy(int damp, int mode)
 cudaError_t SF_CAT(sf_launch_step_r, SF_R)(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
 {
     if (L.variant == SF_VAR_TMA) {
-        if (L.lz == 8) return launch_tma_vy<2, 8>(L, a, st);
+        if (L.lz == 8) return L.vy == 4 ? launch_tma_vy<2, 8, 2>(L, a, st) : launch_tma_vy<2, 8>(L, a, st);
         if (L.vy == 1) return launch_tma_vy<1, 32>(L, a, st);
+        if (L.vy == 4) return launch_tma_vy<2, 32, 2>(L, a, st);  // 8 consumer warps (Geo LAY = 2)
 #if SF_R >= 5
         if (L.vy == 3) return launch_tma_vy<2, 32, 1>(L, a, st);  // wide layout (Geo LAY = 1)
 #endif
@@ -159,6 +160,7 @@ int SF_CAT(sf_tma_smem_r, SF_R)(int vy, int damp, int mode)
 {
     if (vy == 1) return smem_vy<1>(damp, mode);
     if (vy == 3) return SF_R >= 5 ? smem_vy<2, 1>(damp, mode) : 0;
+    if (vy == 4) return smem_vy<2, 2>(damp, mode);
     return smem_vy<2>(damp, mode);
 }
 

@@ -196,20 +196,24 @@ static int resolve_vy(const sf_handle *h)
 {
     if (h->vy == 1) return 1;
     if (h->vy == 3 && h->r >= 5) return 3;  // the wide layout exists for r >= 5 only
+    if (h->vy == 4) return 4;
     return 2;
 }
 
 // TMA kernel tile geometry (stencil_tma.cuh Geo): VY rows per thread (tuning `vy`, auto
 // 2), 7 consumer warps -> BY = 7 VY tile rows; 4 z per lane -> 128-column tiles.
 // vy = 3: the wide layout (Geo LAY = 1, r >= 5): 11 consumer warps x 2 rows, 2 z per lane ->
-// 22 x 64 tiles.
-static int tile_nw(int vy) { return vy == 3 ? 11 : 7; }
-static int tile_rows(int vy) { return vy == 3 ? 2 : vy; }  // rows per thread
+// 22 x 64 tiles.  vy = 4: the warp-specialised layout (Geo LAY = 2): 8 consumer warps x 2 rows
+// x 4 z per lane -> 16 x 128 tiles, a producer warpgroup handing its registers over.
+static int tile_nw(int vy) { return vy == 3 ? 11 : vy == 4 ? 8 : 7; }
+static int tile_rows(int vy) { return vy >= 3 ? 2 : vy; }  // rows per thread
 static int tile_vz(const sf_handle *, int vy) { return vy == 3 ? 2 : 4; }
 static int tile_tz(const sf_handle *h, int vy) { return 32 * tile_vz(h, vy); }
 static int tile_by(int vy) { return tile_nw(vy) * tile_rows(vy); }
-// narrow tiles of the z remainder (Geo<R, 2, 8>): 8 lanes x 4 z, 4 lane rows x 2 rows x 7 warps
-static const int NARROW_TZ = 32, NARROW_BY = 56;
+// narrow tiles of the z remainder (Geo<R, 2, 8, LAY>): 8 lanes x 4 z, 4 lane rows x 2 rows x
+// 7 warps (8 with the warp-specialised layout)
+static const int NARROW_TZ = 32;
+static int narrow_by(int vy) { return 4 * 2 * (vy == 4 ? 8 : 7); }
 
 // persistent CTAs of the TMA kernel (0 = one per SM)
 static int resolve_ctas(const sf_handle *h) { return h->ctas > 0 ? h->ctas : h->sms; }
@@ -449,7 +453,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     // 256 vs 296 us); at r <= 4 it runs at the HBM roofline and the extra launch costs
     // (400^3 so8: 233 vs 225 us).
     int64_t zrem = 0;
-    if (L.variant == SF_VAR_TMA && h->ndim == 3 && h->zsplit && L.vy == 2 && h->r >= 5) {
+    if (L.variant == SF_VAR_TMA && h->ndim == 3 && h->zsplit && (L.vy == 2 || L.vy == 4) && h->r >= 5) {
         const int64_t rem = a.n2 % tile_tz(h, 2);
         if (rem > 0 && rem <= 64 && a.n2 > tile_tz(h, 2)) zrem = rem;
     }
@@ -477,7 +481,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     if (L.variant == SF_VAR_TMA) {
         sf_status s;
         if ((s = build_maps(maps, tile_tz(h, L.vy), tile_by(L.vy)))) return s;
-        if (zrem && (s = build_maps(nmaps, NARROW_TZ, NARROW_BY))) return s;
+        if (zrem && (s = build_maps(nmaps, NARROW_TZ, narrow_by(L.vy)))) return s;
     }
     L.maps = &maps;
     // fuse only small point sets (a few shots' sources): large sets (receiver grids) would
@@ -504,7 +508,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     //  next step: no in-kernel interpolation)
 
     if (b.bidir) {
-        if (L.variant != SF_VAR_TMA || zrem || L.vy == 3)
+        if (L.variant != SF_VAR_TMA || zrem || L.vy != 2)
             return sf_set_error(SF_ERR_INVALID_ARG, "one-launch schedule needs the TMA kernel (7-warp layout) without a z split");
         a.bidir = 1;
         a.sig = b.nosig ? nullptr : h->sigc;
@@ -1084,7 +1088,7 @@ extern "C" sf_status sf_create_slab(const sf_desc *d, void *comm, int rank, int 
 extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas)
 {
     if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
-    if (variant < 0 || variant > 2 || vy < 0 || vy > 3 || ctas < 0)
+    if (variant < 0 || variant > 2 || vy < 0 || vy > 4 || ctas < 0)
         return sf_set_error(SF_ERR_INVALID_ARG, "bad tuning (%d, %d, %d)", variant, vy, ctas);
     if (variant == SF_VAR_TMA && !tma_ok(h))
         return sf_set_error(SF_ERR_INVALID_ARG, "TMA variant needs 3D and n2 %% 4 == 0");
@@ -1112,6 +1116,7 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
         if (h->r >= 5) cands.push_back({SF_VAR_TMA, 2, 0});  // narrow remainder tiles off
         cands.push_back({SF_VAR_TMA, 1, 1});
         if (h->r >= 5 && h->ndim == 3) cands.push_back({SF_VAR_TMA, 3, 1});  // wide layout
+        cands.push_back({SF_VAR_TMA, 4, 1});  // warp-specialised 8-consumer-warp layout
     }
     cands.push_back({SF_VAR_GENERIC, 0, 1});
     const Cand keep{h->variant, h->vy, h->zsplit ? 1 : 0};

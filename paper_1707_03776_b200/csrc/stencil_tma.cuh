@@ -41,6 +41,12 @@
 #ifndef SF_DC_MIN_HI
 #define SF_DC_MIN_HI 2
 #endif
+#ifndef SF_WS_PREG
+#define SF_WS_PREG 24
+#endif
+#ifndef SF_WS_CREG
+#define SF_WS_CREG 240
+#endif
 #ifndef SF_MBAR_SUSPEND_NS
 #define SF_MBAR_SUSPEND_NS 0x100000
 #endif
@@ -162,10 +168,15 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *tm)
 // thread halve the register queue (2r+1 planes x points) so that 12 warps (3 per SM sub-
 // partition) fit the register file: more warps to hide the FP latency that bounds the
 // 7-warp layout at high order.  Tiles 22 x 64.
+// LAY = 2 ("ws", tuning vy = 4): 8 consumer warps (2 per SM sub-partition, 16 x 128 tiles) and
+// a producer WARPGROUP that hands its registers to the consumers (setmaxnreg): the launch
+// holds 12 warps at 168 registers; the producer warpgroup shrinks to SF_WS_PREG (one warp
+// issues the TMA loads, three exit), the consumers grow to SF_WS_CREG.  The 7-warp layout
+// leaves the producer's sub-partition with one consumer warp: the eighth fills it.
 template <int R, int VY, int LZ = 32, int LAY = 0>
 struct Geo {
     static constexpr int VZ = LAY == 1 ? 2 : 4;
-    static constexpr int NW = LAY == 1 ? 11 : 7;        // consumer warps
+    static constexpr int NW = LAY == 1 ? 11 : LAY == 2 ? 8 : 7;  // consumer warps
     static constexpr int LY = 32 / LZ;                  // lane rows per warp
     static constexpr int BY = NW * LY * VY;             // rows per tile
     static constexpr int TZ = LZ * VZ;                  // columns per tile
@@ -198,7 +209,9 @@ struct Cfg {
     static constexpr int DC_FIT = (BUDGET - DU * UST) / CST;
     static constexpr int DC = DC_FIT >= 4 ? 4 : DC_FIT;
     static constexpr int SMEM = DU * UST + DC * CST + 128;  // + alignment slack
-    static constexpr int THREADS = 32 * (NW + 1);       // NW consumer warps + 1 TMA producer warp
+    // NW consumer warps + 1 TMA producer warp (LAY = 2: + a producer warpgroup of 4)
+    static constexpr int PWARPS = LAY == 2 ? 4 : 1;
+    static constexpr int THREADS = 32 * (NW + PWARPS);
     static_assert(DC >= 1, "coefficient ring does not fit shared memory");
     static_assert(DU >= R + 2, "u ring does not fit shared memory");
 };
@@ -358,9 +371,15 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     __syncthreads();
     sf_pdl_wait();  // (PDL) the prologue above overlapped the previous kernel's tail
 
-    if (wy == NW) {
+    if (LAY == 2) {
+        // register hand-over between the warpgroups (12 warps x 168 at launch): producer
+        // warpgroup 24 x 128, consumers 240 x 256 threads = 64 512 <= 65 536
+        if (wy >= NW) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(SF_WS_PREG));
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(SF_WS_CREG));
+    }
+    if (wy >= NW) {
         // ------------------------------------------------ producer warp (TMA issue)
-        if (lane == 0) {
+        if (wy == NW && lane == 0) {
             prefetch_tmap(&tm_cur);
             prefetch_tmap(&tm_old);
             prefetch_tmap(&tm_c3);

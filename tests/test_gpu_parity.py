@@ -1269,6 +1269,39 @@ def test_wide_layout_bitwise(so):
     assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
 
 
+@pytest.mark.parametrize("so,shape", [(2, (23, 45, 132)), (4, (37, 45, 200)), (8, (37, 45, 132)),
+                                      (8, (29, 33, 256)), (12, (37, 45, 132)), (12, (31, 40, 200)),
+                                      (16, (37, 45, 132)), (16, (30, 17, 128))])
+def test_ws_layout_bitwise(so, shape):
+    """The warp-specialised TMA layout (tuning vy = 4: 8 consumer warps x 2 rows x 4 z, 16 x 128
+    tiles, a producer warpgroup handing its registers to the consumers with setmaxnreg):
+    forward records / final levels / snapshots (SAVE), the gradient (GRAD) and the adjoint's
+    source records are bitwise those of the default layout and of the generic kernel, and
+    match the oracle.  Ragged tiles in y; n2 = 132 puts a 4-column remainder on the narrow
+    64 x 32 tiles at r >= 5; n2 = 200 / 256 keep the fused source lists of the forward."""
+    p = synth.random_problem(3, shape, so, 40, seed=97 + so, nbl=5, nsrc=2, nrec=9)
+    p.m_true = (p.m * 0.93).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    res = np.random.default_rng(so).standard_normal((p.nt, 9)).astype(np.float32)
+    outs = []
+    for variant, vy in ((2, 4), (2, 2), (1, 0)):
+        prop = make_prop(p)
+        prop.set_tuning(variant, vy, 0)
+        assert prop.tuning()["vy"] == (vy if variant == 2 else 0)
+        rec, u, snaps = prop.forward(dev(p.wavelet), save_every=3)
+        g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+        srca, v, _ = prop.adjoint(dev(res))
+        torch.cuda.synchronize()
+        outs.append((rec.cpu().numpy(), u.cpu().numpy(), snaps.cpu().numpy(), g.cpu().numpy(), J,
+                     srca.cpu().numpy(), v.cpu().numpy()))
+        prop.close()
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+    ro, uo, _ = oracle_forward(p)
+    assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
+
+
 @pytest.mark.parametrize("so,sep", [(4, False), (8, False), (4, True), (16, False)])
 def test_loop2d_bitwise(so, sep):
     """SF_OPT_LOOP2D (a small 2D grid runs its whole forward / adjoint time loop in one CTA,
