@@ -174,7 +174,9 @@ SF_API sf_status sf_get_profile_detail(sf_handle *h, double *ms_by_kind, long lo
 /* Tuning: kernel variant (0 auto, 1 generic thread-per-point, 2 TMA 2.5D streaming),
  * TMA layout `vy` (0 auto = 2: 2 rows x 4 z per thread, 7 consumer warps, 14 x 128 tiles;
  * 1: one row per thread, 7-row tiles; 3, space order >= 10: 2 rows x 2 z per thread, 11
- * consumer warps, 22 x 64 tiles -- otherwise read as 2) and the number of
+ * consumer warps, 22 x 64 tiles -- otherwise read as 2; 4: warp-specialised, 8 consumer warps
+ * x 2 rows x 4 z, 16 x 128 tiles, a producer warpgroup handing its registers to the
+ * consumers) for every step mode (clears the GRAD-mode layout sf_autotune sets), and the number of
  * persistent TMA CTAs `ctas` (0 auto = one per SM; the (tile, plane) work is split into
  * `ctas` equal runs; every setting gives the same bits).  SF_ERR_INVALID_ARG for other
  * values. */
@@ -255,6 +257,15 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   memory, and cluster barriers order stencil, injection and
                                   records step by step (launch-bound otherwise).  Bitwise the
                                   per-step kernels.  0: one launch per step.                     */
+#define SF_OPT_BALANCE 16      /* TMA kernel work split: 2 (default) auto, 1 balanced, 0 chunked.
+                                  Chunked: (tile, x-chunk) items dealt round-robin to the
+                                  persistent CTAs (y/z-neighbouring tiles in step: their shared
+                                  halo rows hit in L2), the chunk count minimising rounds x
+                                  (chunk + 2r).  Balanced: CTA b streams the contiguous planes
+                                  [b T / G, (b + 1) T / G) of all T (tile, plane) units (equal
+                                  shares whatever the tile count; neighbours drift apart, halo
+                                  rows re-read from HBM).  Auto: balanced for space order >= 10
+                                  when the chunked split wastes more than 3 %.  Same bits.       */
 #define SF_OPT_TBLOCK 15       /* temporal blocking, default 0: 1 runs sf_forward without
                                   snapshots two time steps per launch (3D, space order <= 8, one
                                   GPU, no separable profiles, n_z % 4 == 0; SF_ERR_INVALID_ARG
@@ -272,6 +283,9 @@ SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
  * tiles (space order >= 10), the thread-per-point kernel -- on the caller's scratch state u
  * ([2][Nloc] device floats, overwritten), keeps the fastest in the handle and returns it in
  * chosen[3] = {variant, vy, zsplit} (may be NULL) and its time per step in *ms (may be NULL).
+ * With the TMA kernel it then times the 7- and 8-warp layouts (vy 2, 4) in GRAD mode (the
+ * gradient's adjoint: snapshot and gradient planes streamed beside the stencil; scratch
+ * values) and keeps the faster for GRAD-mode steps (sf_get_grad_tuning).
  * Every configuration computes the same bits.  Synchronises `stream`. */
 SF_API sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen, float *ms, void *stream);
 /* Test hook of the one-launch schedule on one GPU (SF_OPT_ONE_LAUNCH 2): after each step's
@@ -282,6 +296,9 @@ SF_API sf_status sf_debug_probe(sf_handle *h, float *dst, long long *one_launch_
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */
 SF_API sf_status sf_get_tuning(const sf_handle *h, int *variant, int *vy, int *ctas);
+/* The TMA layout (vy) of GRAD-mode steps (0 with the generic kernel); SF_ERR_INVALID_ARG on
+ * NULL arguments. */
+SF_API sf_status sf_get_grad_tuning(const sf_handle *h, int *vy);
 
 /* ---- multi-GPU (slab decomposition along axis 0; one process per GPU, NCCL) ---- */
 

@@ -11,7 +11,7 @@ This package never imports ``oracle`` (the fp64 CPU reference used by the tests)
 """
 from ._lib import EXPORTS, LIB_PATH, SfError, build, lib  # noqa: F401
 from ._lib import (SF_OPT_COMM_SMS, SF_OPT_FUSE_MAX, SF_OPT_GRAPH, SF_OPT_L2_PREFETCH,  # noqa: F401
-                   SF_OPT_ONE_LAUNCH, SF_OPT_P2P, SF_OPT_PDL, SF_OPT_PROF_EVERY, SF_OPT_LOOP2D, SF_OPT_TBLOCK, SF_OPT_SNAP_HALF, SF_OPT_SPLIT, SF_OPT_ZSPLIT)
+                   SF_OPT_ONE_LAUNCH, SF_OPT_P2P, SF_OPT_PDL, SF_OPT_PROF_EVERY, SF_OPT_LOOP2D, SF_OPT_TBLOCK, SF_OPT_BALANCE, SF_OPT_SNAP_HALF, SF_OPT_SPLIT, SF_OPT_ZSPLIT)
 from .api import (Propagator, allreduce_gradient, fd_weights, forward_host,  # noqa: F401
                   nccl_comm_destroy, nccl_comm_info, nccl_check, nccl_comm_init, nccl_unique_id, slab_halo_plan, slab_plan,
                   local_group_create, local_group_destroy, sparse_owner, convection2d, laplace2d)

@@ -25,7 +25,7 @@ STATUS = {0: "SF_OK", 1: "SF_ERR_INVALID_ARG", 2: "SF_ERR_SHAPE", 3: "SF_ERR_ORD
 EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint", "sf_residual",
            "sf_gradient_workspace_bytes", "sf_gradient", "sf_gradient_ckpt_workspace_bytes",
            "sf_gradient_ckpt", "sf_forward_host", "sf_forward_once", "sf_set_profiling",
-           "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
+           "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_get_grad_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_nccl_comm_info",
            "sf_nccl_check", "sf_create_slab",
            "sf_allreduce_gradient", "sf_local_group_create", "sf_local_group_destroy",
@@ -34,7 +34,8 @@ EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint
 
 SF_OPT_L2_PREFETCH, SF_OPT_SPLIT, SF_OPT_FUSE_MAX, SF_OPT_COMM_SMS, SF_OPT_GRAPH, SF_OPT_SNAP_HALF, SF_OPT_P2P, SF_OPT_ZSPLIT = \
     1, 2, 3, 4, 5, 7, 8, 9
-SF_OPT_ONE_LAUNCH, SF_OPT_PDL, SF_OPT_PROF_EVERY, SF_OPT_LOOP2D, SF_OPT_TBLOCK = 11, 12, 13, 14, 15
+SF_OPT_ONE_LAUNCH, SF_OPT_PDL, SF_OPT_PROF_EVERY, SF_OPT_LOOP2D, SF_OPT_TBLOCK, SF_OPT_BALANCE = \
+    11, 12, 13, 14, 15, 16
 
 
 class SfError(RuntimeError):
@@ -89,6 +90,7 @@ def lib():
             "sf_set_tuning": [P, I, I, I],
             "sf_set_option": [P, I, I],
             "sf_get_tuning": [P, P, P, P],
+            "sf_get_grad_tuning": [P, P],
             "sf_slab_plan": [I64, I, I, I, P, P],
             "sf_slab_halo_plan": [I64, I, I, I, P],
             "sf_sparse_owner": [I64, I, I, D, D, P],

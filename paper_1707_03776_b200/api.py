@@ -212,7 +212,12 @@ class Propagator:
     def tuning(self):
         v, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         check(lib().sf_get_tuning(self._h, ctypes.byref(v), ctypes.byref(b), ctypes.byref(c)))
-        return {"variant": v.value, "vy": b.value, "ctas": c.value}
+        out = {"variant": v.value, "vy": b.value, "ctas": c.value}
+        g = ctypes.c_int()
+        if hasattr(lib(), "sf_get_grad_tuning"):  # (A/B builds of older revisions lack it)
+            check(lib().sf_get_grad_tuning(self._h, ctypes.byref(g)))
+            out["vy_grad"] = g.value
+        return out
 
     @_ondev
     def set_profiling(self, on: bool = True):
@@ -221,7 +226,8 @@ class Propagator:
     @_ondev
     def autotune(self, steps: int = 8, stream=None) -> dict:
         """sf_autotune: time every feasible launch configuration on a scratch state and keep
-        the fastest (same bits either way).  Returns {variant, vy, zsplit, ms_per_step}."""
+        the fastest (same bits either way; GRAD-mode steps get their own layout, tuning()
+        reports it as vy_grad).  Returns {variant, vy, zsplit, ms_per_step}."""
         u = torch.zeros((2,) + self.local_shape, device=self.device)
         ch = (ctypes.c_int * 3)()
         ms = ctypes.c_float()

@@ -192,11 +192,14 @@ static int resolve_variant(const sf_handle *h)
     return SF_VAR_GENERIC;
 }
 
-static int resolve_vy(const sf_handle *h)
+// TMA layout of a step of `mode`: GRAD-mode steps may use their own (sf_autotune times them
+// separately: the 8-warp layout is faster for the plain step at high order, slower in GRAD)
+static int resolve_vy(const sf_handle *h, int mode)
 {
-    if (h->vy == 1) return 1;
-    if (h->vy == 3 && h->r >= 5) return 3;  // the wide layout exists for r >= 5 only
-    if (h->vy == 4) return 4;
+    const int vy = (mode == SF_MODE_GRAD && h->vy_grad) ? h->vy_grad : h->vy;
+    if (vy == 1) return 1;
+    if (vy == 3 && h->r >= 5) return 3;  // the wide layout exists for r >= 5 only
+    if (vy == 4) return 4;
     return 2;
 }
 
@@ -424,7 +427,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     SfLaunch L{};
     L.ndim = h->ndim;
     L.variant = b.force_generic ? SF_VAR_GENERIC : resolve_variant(h);
-    L.vy = resolve_vy(h);
+    L.vy = resolve_vy(h, mode);
     if (b.mq) {
         for (int k = 0; k < 4; ++k) a.mq[k] = b.mq[k];
         a.md[0] = b.md[0];
@@ -441,6 +444,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     L.mode = mode;
     L.snap_slot = b.snap_slot;
     L.lz = 32;
+    L.balance = h->balance;
     // PDL only after a standalone injection kernel: stencil -> stencil gains nothing measurable
     // (a persistent launch cannot co-reside with the previous one), and plain launches keep
     // the sampled event timing of the stencil exact
@@ -949,8 +953,8 @@ static sf_status create_common(const sf_desc *d, sf_handle *h)
     // allocation): fused-injection lists for the default tile shape, split-schedule lists in
     // slab mode.  (A later sf_set_tuning to another tile shape rebuilds the lists once.)
     if (resolve_variant(h) == SF_VAR_TMA) {
-        if (h->src.ntgt > 0 && h->src.ntgt <= h->fuse_max && (s = ensure_inj_tiles(h, h->src, resolve_vy(h)))) return s;
-        if (h->rec.ntgt > 0 && h->rec.ntgt <= h->fuse_max && (s = ensure_inj_tiles(h, h->rec, resolve_vy(h)))) return s;
+        if (h->src.ntgt > 0 && h->src.ntgt <= h->fuse_max && (s = ensure_inj_tiles(h, h->src, resolve_vy(h, SF_MODE_PLAIN)))) return s;
+        if (h->rec.ntgt > 0 && h->rec.ntgt <= h->fuse_max && (s = ensure_inj_tiles(h, h->rec, resolve_vy(h, SF_MODE_PLAIN)))) return s;
     }
     if (h->split) {
         if (h->src.ntgt > 0 && (s = ensure_split_lists(h, h->src))) return s;
@@ -1094,6 +1098,7 @@ extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas)
         return sf_set_error(SF_ERR_INVALID_ARG, "TMA variant needs 3D and n2 %% 4 == 0");
     h->variant = variant;
     h->vy = vy;
+    h->vy_grad = 0;
     h->ctas = ctas;
     drop_graphs(h);
     return SF_OK;
@@ -1152,13 +1157,48 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
             bi = (int)c;
         }
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    h->prof = keep_prof;
     const Cand pick = (s || bi < 0) ? keep : cands[bi];
     h->variant = pick.variant;
     h->vy = pick.vy;
     h->zsplit = pick.zsplit != 0;
+    h->vy_grad = 0;
+    // GRAD-mode steps (the gradient's adjoint: snapshot and gradient planes streamed beside
+    // the stencil) get their own layout: time the TMA layouts with the winner's z split in GRAD
+    // mode on the same scratch state (snapshot = the current level, gradient = the output
+    // buffer: the values are scratch, only the time counts)
+    float best_g = 1e30f;
+    if (!s && pick.variant == SF_VAR_TMA && h->ndim == 3) {
+        for (int vg : {2, 4}) {
+            h->vy = vg;
+            for (int it = -2; it < steps && !s; ++it) {
+                if (it == 0) SF_CUDA_TRY(cudaEventRecord(e0, st));
+                StepBufs b{};
+                b.cur = (it & 1) ? A : B;
+                b.out = (it & 1) ? B : A;
+                b.snaps = b.cur;
+                b.nsnap = 1;
+                b.snap_slot = 0;
+                b.grad = b.out;
+                b.gscale = 0.0f;
+                bool fused = false;
+                s = launch_step(h, b, SF_MODE_GRAD, st, &fused);
+            }
+            if (s) break;
+            SF_CUDA_TRY(cudaEventRecord(e1, st));
+            SF_CUDA_TRY(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            SF_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+            ms /= (float)steps;
+            if (ms < best_g) {
+                best_g = ms;
+                h->vy_grad = vg;
+            }
+        }
+        h->vy = pick.vy;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h->prof = keep_prof;
     drop_graphs(h);
     if (s) return s;
     if (chosen) {
@@ -1241,6 +1281,11 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         h->snap_half = value != 0;
         drop_graphs(h);
         return SF_OK;
+    case SF_OPT_BALANCE:
+        if (value < 0 || value > 2) return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_BALANCE %d", value);
+        h->balance = value;
+        drop_graphs(h);
+        return SF_OK;
     case SF_OPT_TBLOCK:
         if (value) {
             sf_status st = ensure_tb(h);
@@ -1263,11 +1308,18 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
     }
 }
 
+extern "C" sf_status sf_get_grad_tuning(const sf_handle *h, int *vy)
+{
+    if (!h || !vy) return sf_set_error(SF_ERR_INVALID_ARG, "handle or vy is NULL");
+    *vy = resolve_variant(h) == SF_VAR_TMA ? resolve_vy(h, SF_MODE_GRAD) : 0;
+    return SF_OK;
+}
+
 extern "C" sf_status sf_get_tuning(const sf_handle *h, int *variant, int *vy, int *ctas)
 {
     if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
     const int v = resolve_variant(h);
-    const int b = resolve_vy(h);
+    const int b = resolve_vy(h, SF_MODE_PLAIN);
     if (variant) *variant = v;
     if (vy) *vy = v == SF_VAR_TMA ? b : 0;
     if (ctas) *ctas = v == SF_VAR_TMA ? resolve_ctas(h) : 0;

@@ -9,10 +9,15 @@
 //   X  = sum_{k=1..r} w_k * ( (x_-k + x_+k) - 2 u )
 //   Lap = P + X,  w_k = fp32(w_k^exact / h^2)
 // so that a constant field is annihilated exactly (4u and 2u are exact) and the fp32
-// weights never need to sum to zero.  (A single chain over the three axes with one
-// -fl(6u) term costs 7 instead of 8 FP operations per radius and is also exact on constants,
-// but fl(6u) adds a rounding error per point that the exact 4u / 2u avoid: measured twice the
-// fp32 error, configs[2] gradient 1.9e-4 vs 3.8e-5 -- DESIGN.md section 7.)  Update (the
+// weights never need to sum to zero.  3D, r >= 5, outside the gradient's GRAD mode: the
+// MERGED form (sf_merged3 below) -- one chain over the three axes per radius,
+//   L  = sum_{k=1..r} w_k * fma(-6, u, ((y_-k + y_+k) + (z_-k + z_+k)) + (x_-k + x_+k))
+// 7 instead of 8 FP operations per radius (the kernel is FP-issue bound at high order:
+// configs[4] -7 %), still exact on a constant field: the FMA forms 6u exactly inside.  (An
+// earlier chain that subtracted a separately rounded fl(6u) doubled the fp32 error --
+// configs[2] gradient 1.9e-4 vs 3.8e-5; the gradient's in-kernel
+// S = out - 2u + old is the most sensitive use of L, so GRAD mode keeps the per-axis form.)
+// Update (the
 // paper's solve(), with a
 // centred u.dt, reading C1), beta/c3 hoisted per point at setup:
 //   out = u + beta (u - old) + c3 * Lap
@@ -53,6 +58,22 @@ __device__ __forceinline__ float sf_inplane3(float ym, float yp, float zm, float
 __device__ __forceinline__ float sf_inplane2(float zm, float zp, float u)
 {
     return __fmaf_rn(-2.0f, u, __fadd_rn(zm, zp));
+}
+
+// Merged form (SF_MERGED): t_k = (((y-k + y+k) + (z-k + z+k)) + (x-k + x+k)) - 6u, one FMA with
+// the exact product 6u (no separately rounded fl(6u)), L = sum_k w_k t_k: 7 instead of 8 FP
+// operations per radius, still exact on a constant field.
+#ifndef SF_MERGED
+#define SF_MERGED 1
+#endif
+__host__ __device__ constexpr bool sf_merged_form(int r, int mode)
+{
+    return SF_MERGED && r >= 5 && mode != SF_MODE_GRAD;
+}
+__device__ __forceinline__ float sf_merged3(float ym, float yp, float zm, float zp, float xm, float xp, float u)
+{
+    float s = __fadd_rn(__fadd_rn(__fadd_rn(ym, yp), __fadd_rn(zm, zp)), __fadd_rn(xm, xp));
+    return __fmaf_rn(-6.0f, u, s);
 }
 
 // x term at radius k: (xm + xp) - 2u

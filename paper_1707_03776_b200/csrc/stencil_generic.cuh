@@ -22,7 +22,20 @@ k_generic3d(SfStepArgs a)
     const float *__restrict__ c = a.cur;
     const float u = __ldg(c + idx);
     float lap;
-    {
+    if constexpr (sf_merged_form(R, MODE)) {
+        float L = 0.0f;
+#pragma unroll
+        for (int k = 1; k <= R; ++k) {
+            const float ym = (y - k >= 0) ? __ldg(c + idx - k * sy) : 0.0f;
+            const float yp = (y + k < a.n1) ? __ldg(c + idx + k * sy) : 0.0f;
+            const float zm = (z - k >= 0) ? __ldg(c + idx - k) : 0.0f;
+            const float zp = (z + k < a.n2) ? __ldg(c + idx + k) : 0.0f;
+            const float xm = (x - k >= 0) ? __ldg(c + idx - k * sx) : 0.0f;
+            const float xp = (x + k < a.n0b) ? __ldg(c + idx + k * sx) : 0.0f;
+            L = __fmaf_rn(a.w.w[k], sf_merged3(ym, yp, zm, zp, xm, xp, u), L);
+        }
+        lap = L;
+    } else {
         float P = 0.0f, X = 0.0f;
 #pragma unroll
         for (int k = 1; k <= R; ++k) {

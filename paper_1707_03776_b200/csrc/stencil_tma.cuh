@@ -331,6 +331,9 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     constexpr bool DAMP = C::DAMP;
     constexpr int VZ = C::VZ, NJ = VZ / 2, NW = C::NW, BY = C::BY, TZ = C::TZ, HZ = C::HZ;
     constexpr int Q = C::Q, W = C::W, DU = C::DU, DC = C::DC;
+    // merged Laplacian form (sf_merged3: one chain over the three axes per radius, 7 instead
+    // of 8 FP operations) for r >= 5 outside the gradient (stencil_common.cuh)
+    constexpr bool MRG = sf_merged_form(R, MODE);
     const int PD = a.l2_prefetch;  // planes of L2 prefetch beyond the smem ring (0 = off)
     // slot release by the consumers: one arrive per warp (lane 0, after __syncwarp).  Per-
     // thread arrives (tried for r >= 5, 1.6 % faster on configs[3]) produced rare wrong values
@@ -351,8 +354,22 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     // narrow remainder tiles); neighbours beyond that range are still read (real halo)
     const int ntz = (int)((a.n2t - a.zbase + TZ - 1) / TZ);
     const int tiles = ntz * (int)((a.n1 + BY - 1) / BY);
-    const int items = tiles * nchunk;
+    // nchunk == 0: balanced contiguous split -- CTA b walks the planes [b T / G, (b + 1) T / G)
+    // of the tile-major sequence of all T = tiles x PT (tile, plane) units (one "item" per CTA,
+    // cut into segments at tile boundaries): every CTA gets the same number of planes whatever
+    // the tile count, at the price of neighbouring tiles drifting apart in x (their shared halo
+    // rows then come from HBM twice); otherwise items = (tile, x-chunk) dealt round-robin.
+    const bool bal = nchunk == 0;
+    const int64_t TT = (int64_t)tiles * PT;
+    const int items = bal ? (int)gridDim.x : tiles * nchunk;
     if ((int)blockIdx.x >= items) return;  // uniform over the CTA
+    auto item_w0 = [&](int it) -> int64_t {
+        return bal ? TT * it / gridDim.x : (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk;
+    };
+    auto item_w1 = [&](int it) -> int64_t {
+        return bal ? TT * (it + 1) / gridDim.x : min((int64_t)(it % tiles) * PT + (int64_t)(it / tiles + 1) * chunk,
+                                                      (int64_t)(it % tiles + 1) * PT);
+    };
 
     if (wy == 0 && lane == 0) {
 #pragma unroll 1
@@ -389,8 +406,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
             uint32_t uph = 0, cph = 0;
             int64_t gu = 0, gc = 0;  // ring uses so far
             for (int it = blockIdx.x; it < items; it += gridDim.x)
-            for (int64_t w = (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk,
-                         w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
+            for (int64_t w = item_w0(it), w1 = item_w1(it); w < w1;) {
                 const Seg sg = next_seg(w, w1, P1, PT, a);
                 // (BIDIR instances only: the one-launch slab schedule; elsewhere dir == 1 folds)
                 const int dir = BIDIR ? seg_dir(a, it, tiles, nchunk, w1, PT) : 1;
@@ -471,14 +487,13 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
     for (int k = 1; k <= R; ++k) Wk[k] = pk2(a.w.w[k], a.w.w[k]);
     Wk[0] = 0ull;
-    const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f);
+    const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f), M6 = pk2(-6.f, -6.f);
     const f2_t NG = pk2(-a.gscale, -a.gscale), ONE2 = pk2(1.f, 1.f);
     const f2_t HDT2 = pk2(a.hdt, a.hdt);
     constexpr int QINF = 0x7fffffff;
 
     for (int it = blockIdx.x; it < items; it += gridDim.x)
-    for (int64_t w = (int64_t)(it % tiles) * PT + (int64_t)(it / tiles) * chunk,
-                 w1 = min(w + chunk, (int64_t)(it % tiles + 1) * PT); w < w1;) {
+    for (int64_t w = item_w0(it), w1 = item_w1(it); w < w1;) {
         const Seg sg = next_seg(w, w1, P1, PT, a);
         const int dir = BIDIR ? seg_dir(a, it, tiles, nchunk, w1, PT) : 1;
         w += sg.qb - sg.qa;
@@ -559,8 +574,9 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                     // ---- (1) in-plane partial of output plane q = p - R: its u tile is
                     // resident (arrived R planes ago), so this overlaps the wait for plane p
                     f2_t Pin[VY][NJ], Uq[VY][NJ];
-                    if (outp) {
-                        const float *uq = ubase + uo * UF;
+                    // in-plane terms of output plane q from its u tile; xs(j, jp, k) adds the x pair
+                    // (merged form) or nothing (per-axis form: the x term is a separate chain)
+                    auto inplane = [&](const float *uq, auto xs) {
                         // y rows rown - R .. rown + VY - 1 + R (own rows included)
                         f2_t Y[VY + 2 * R][NJ];
 #pragma unroll
@@ -607,7 +623,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                             for (int jp = 0; jp < NJ; ++jp) {
                                 const f2_t u = Uq[j][jp];
-                                // radius ascending (== sf_inplane3 per lane)
+                                // radius ascending (== sf_inplane3 / sf_merged3 per lane)
                                 f2_t P = 0ull;
 #pragma unroll
                                 for (int k = 1; k <= R; ++k) {
@@ -618,17 +634,24 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                                         zs = pk2(__fadd_rn(F(em), F(ep)), __fadd_rn(F(em + 1), F(ep + 1)));
                                     else
                                         zs = add2(PZ(em), PZ(ep));
-                                    P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
+                                    if constexpr (MRG)
+                                        P = fma2(Wk[k], fma2(M6, u, add2(add2(ys, zs), xs(j, jp, k))), P);
+                                    else
+                                        P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
                                 }
                                 Pin[j][jp] = P;
                             }
                         }
-                    }
+                    };
+                    // ---- (1) in-plane partial of output plane q = p - R: its u tile is
+                    // resident (arrived R planes ago), so this overlaps the wait for plane p
+                    // (merged form: inside the slot code below, after the wait)
+                    if (!MRG && outp) inplane(ubase + uo * UF, [](int, int, int) { return 0ull; });
                     // ---- (2) plane p of u^n into queue slot sl; x term of plane q (slot sl - R)
                     mbar_wait(ufull + 8 * us, uph);
                     const float *ut = ubase + us * UF;
                     f2_t X[VY][NJ];
-                    auto slot = [&](auto ic) {
+                                        auto slot = [&](auto ic) {
                         constexpr int S = decltype(ic)::value;
                         constexpr int SQ = (S - R + Q) % Q;
 #pragma unroll
@@ -636,7 +659,12 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
                             SF_CHK(ut + own_off + j * W, ut, ut + W * C::H);
                             ldp<VZ>(ut + own_off + j * W, V[S][j]);
                         }
-                        if (outp) {
+                        if (MRG && outp) {
+                            // merged form: one chain over the three axes per radius
+                            inplane(ubase + uo * UF, [&](int j, int jp, int k) {
+                                return add2(V[(SQ - k + Q) % Q][j][jp], V[(SQ + k) % Q][j][jp]);
+                            });
+                        } else if (outp) {
 #pragma unroll
                             for (int j = 0; j < VY; ++j)
 #pragma unroll
@@ -719,7 +747,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
 #pragma unroll
                             for (int jp = 0; jp < NJ; ++jp) {
                                 const f2_t u = Uq[j][jp];
-                                const f2_t lap = add2(Pin[j][jp], X[j][jp]);
+                                const f2_t lap = MRG ? Pin[j][jp] : add2(Pin[j][jp], X[j][jp]);
                                 // out = u + beta (u - old) + c3 lap   (== sf_update per lane)
                                 const f2_t d = fma2(M1, ov[j][jp], u);
                                 res2[j][jp] = fma2(cv[j][jp], lap, fma2(bv[j][jp], d, u));

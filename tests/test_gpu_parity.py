@@ -1229,17 +1229,26 @@ def test_pdl_launches_bitwise():
 def test_autotune_picks_a_configuration_same_bits(shape, so):
     """sf_autotune (setup-time tuning): times every feasible launch configuration
     on a scratch state, keeps the fastest; the forward after it is bitwise the forward with
-    the default tuning (every configuration computes the same bits)."""
+    the default tuning (every configuration computes the same bits); so is the gradient,
+    whose GRAD-mode steps run the layout autotune picked for them (vy_grad)."""
     p = synth.random_problem(3, shape, so, 30, seed=71, nbl=4, nsrc=2, nrec=9)
+    d_obs = (np.random.default_rng(3).standard_normal((p.nt, 9)) * 1e-3).astype(np.float32)
     ref = gpu_forward(p)
     prop = make_prop(p)
+    g0, J0 = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
+    g0 = g0.cpu().numpy()
     t = prop.autotune(steps=4)
     assert t["variant"] in (1, 2) and t["ms_per_step"] > 0
     tun = prop.tuning()
     assert tun["variant"] == t["variant"]
+    assert tun["vy_grad"] in ((2, 4) if t["variant"] == 2 else (0,))
     rec, u, _ = prop.forward(dev(p.wavelet))
+    g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
     torch.cuda.synchronize()
     assert np.array_equal(rec.cpu().numpy(), ref[0]) and np.array_equal(u.cpu().numpy(), ref[1])
+    assert np.array_equal(g.cpu().numpy(), g0) and J == J0
+    prop.set_tuning(2, 4, 0)  # explicit layouts apply to every mode
+    assert prop.tuning()["vy_grad"] == 4
     prop.close()
 
 
@@ -1298,6 +1307,37 @@ def test_ws_layout_bitwise(so, shape):
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
             assert np.array_equal(a, b)
+    ro, uo, _ = oracle_forward(p)
+    assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
+
+
+@pytest.mark.parametrize("so,shape,vy,ctas", [(4, (37, 45, 200), 2, 0), (8, (29, 33, 256), 4, 5),
+                                              (12, (37, 45, 132), 4, 0), (12, (31, 40, 200), 2, 7),
+                                              (16, (30, 17, 128), 4, 3), (16, (41, 45, 132), 2, 0)])
+def test_balanced_split_bitwise(so, shape, vy, ctas):
+    """SF_OPT_BALANCE = 1 (each persistent CTA streams an equal contiguous run of the tile-major
+    (tile, plane) sequence, cut at tile boundaries) gives the bits of the chunked split (0):
+    forward records / levels / snapshots with fused sources, the gradient and the adjoint;
+    CTA counts that put segment starts mid-tile (ctas 3, 5, 7), narrow remainder tiles
+    (n2 = 132, r >= 5); and it matches the oracle."""
+    p = synth.random_problem(3, shape, so, 36, seed=131 + so, nbl=5, nsrc=2, nrec=9)
+    p.m_true = (p.m * 0.93).astype(np.float32)
+    d_obs = oracle.forward(p, m=p.m_true)["rec"].astype(np.float32)
+    res = np.random.default_rng(so).standard_normal((p.nt, 9)).astype(np.float32)
+    outs = []
+    for bal in (1, 0):
+        prop = make_prop(p)
+        prop.set_tuning(2, vy, ctas)
+        prop.set_option(sf().SF_OPT_BALANCE, bal)
+        rec, u, snaps = prop.forward(dev(p.wavelet), save_every=3)
+        g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=3)
+        srca, v, _ = prop.adjoint(dev(res))
+        torch.cuda.synchronize()
+        outs.append((rec.cpu().numpy(), u.cpu().numpy(), snaps.cpu().numpy(), g.cpu().numpy(), J,
+                     srca.cpu().numpy(), v.cpu().numpy()))
+        prop.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
     ro, uo, _ = oracle_forward(p)
     assert rel(outs[0][0], ro) <= TOL and rel(outs[0][1][1], uo[1]) <= TOL
 
