@@ -257,15 +257,15 @@ SF_API sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas);
                                   memory, and cluster barriers order stencil, injection and
                                   records step by step (launch-bound otherwise).  Bitwise the
                                   per-step kernels.  0: one launch per step.                     */
-#define SF_OPT_BALANCE 16      /* TMA kernel work split: 2 (default) auto, 1 balanced, 0 chunked.
+#define SF_OPT_BALANCE 16      /* TMA kernel work split: 0 (default) chunked, 1 balanced.
                                   Chunked: (tile, x-chunk) items dealt round-robin to the
                                   persistent CTAs (y/z-neighbouring tiles in step: their shared
                                   halo rows hit in L2), the chunk count minimising rounds x
                                   (chunk + 2r).  Balanced: CTA b streams the contiguous planes
                                   [b T / G, (b + 1) T / G) of all T (tile, plane) units (equal
                                   shares whatever the tile count; neighbours drift apart, halo
-                                  rows re-read from HBM).  Auto: balanced for space order >= 10
-                                  when the chunked split wastes more than 3 %.  Same bits.       */
+                                  rows re-read from HBM).  Sets the split of every step mode;
+                                  sf_autotune chooses per mode.  Same bits.                      */
 #define SF_OPT_TBLOCK 15       /* temporal blocking, default 0: 1 runs sf_forward without
                                   snapshots two time steps per launch (3D, space order <= 8, one
                                   GPU, no separable profiles, n_z % 4 == 0; SF_ERR_INVALID_ARG
@@ -283,9 +283,11 @@ SF_API sf_status sf_set_option(sf_handle *h, int option, int value);
  * tiles (space order >= 10), the thread-per-point kernel -- on the caller's scratch state u
  * ([2][Nloc] device floats, overwritten), keeps the fastest in the handle and returns it in
  * chosen[3] = {variant, vy, zsplit} (may be NULL) and its time per step in *ms (may be NULL).
- * With the TMA kernel it then times the 7- and 8-warp layouts (vy 2, 4) in GRAD mode (the
- * gradient's adjoint: snapshot and gradient planes streamed beside the stencil; scratch
- * values) and keeps the faster for GRAD-mode steps (sf_get_grad_tuning).
+ * At space order >= 10 every TMA candidate is timed with both work splits (SF_OPT_BALANCE).
+ * With the TMA kernel it then times the 7- and 8-warp layouts (vy 2, 4; x both splits at
+ * space order >= 10) in GRAD mode (the gradient's adjoint: snapshot and gradient planes
+ * streamed beside the stencil; scratch values) and keeps the fastest for GRAD-mode steps
+ * (sf_get_tuning_modes).
  * Every configuration computes the same bits.  Synchronises `stream`. */
 SF_API sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen, float *ms, void *stream);
 /* Test hook of the one-launch schedule on one GPU (SF_OPT_ONE_LAUNCH 2): after each step's
@@ -296,9 +298,11 @@ SF_API sf_status sf_debug_probe(sf_handle *h, float *dst, long long *one_launch_
 
 /* Which variant / vy / ctas the next launch will use (after auto selection). */
 SF_API sf_status sf_get_tuning(const sf_handle *h, int *variant, int *vy, int *ctas);
-/* The TMA layout (vy) of GRAD-mode steps (0 with the generic kernel); SF_ERR_INVALID_ARG on
- * NULL arguments. */
-SF_API sf_status sf_get_grad_tuning(const sf_handle *h, int *vy);
+/* Per-mode tuning of the TMA kernel (each pointer may be NULL; 0s with the generic kernel):
+ * the layout (vy) of GRAD-mode steps and the work split (SF_OPT_BALANCE: 0 chunked, 1
+ * balanced) of the plain / SAVE steps and of the GRAD-mode steps, as sf_autotune left them.
+ * SF_ERR_INVALID_ARG on a NULL handle. */
+SF_API sf_status sf_get_tuning_modes(const sf_handle *h, int *vy_grad, int *balance, int *balance_grad);
 
 /* ---- multi-GPU (slab decomposition along axis 0; one process per GPU, NCCL) ---- */
 

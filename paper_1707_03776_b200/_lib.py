@@ -25,7 +25,7 @@ STATUS = {0: "SF_OK", 1: "SF_ERR_INVALID_ARG", 2: "SF_ERR_SHAPE", 3: "SF_ERR_ORD
 EXPORTS = ["sf_fd_weights", "sf_create", "sf_destroy", "sf_forward", "sf_adjoint", "sf_residual",
            "sf_gradient_workspace_bytes", "sf_gradient", "sf_gradient_ckpt_workspace_bytes",
            "sf_gradient_ckpt", "sf_forward_host", "sf_forward_once", "sf_set_profiling",
-           "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_get_grad_tuning", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
+           "sf_get_profile", "sf_get_profile_detail", "sf_set_tuning", "sf_set_option", "sf_get_tuning", "sf_get_tuning_modes", "sf_slab_plan", "sf_slab_halo_plan", "sf_sparse_owner",
            "sf_nccl_unique_id", "sf_nccl_comm_init", "sf_nccl_comm_destroy", "sf_nccl_comm_info",
            "sf_nccl_check", "sf_create_slab",
            "sf_allreduce_gradient", "sf_local_group_create", "sf_local_group_destroy",
@@ -90,7 +90,7 @@ def lib():
             "sf_set_tuning": [P, I, I, I],
             "sf_set_option": [P, I, I],
             "sf_get_tuning": [P, P, P, P],
-            "sf_get_grad_tuning": [P, P],
+            "sf_get_tuning_modes": [P, P, P, P],
             "sf_slab_plan": [I64, I, I, I, P, P],
             "sf_slab_halo_plan": [I64, I, I, I, P],
             "sf_sparse_owner": [I64, I, I, D, D, P],

@@ -213,10 +213,10 @@ class Propagator:
         v, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         check(lib().sf_get_tuning(self._h, ctypes.byref(v), ctypes.byref(b), ctypes.byref(c)))
         out = {"variant": v.value, "vy": b.value, "ctas": c.value}
-        g = ctypes.c_int()
-        if hasattr(lib(), "sf_get_grad_tuning"):  # (A/B builds of older revisions lack it)
-            check(lib().sf_get_grad_tuning(self._h, ctypes.byref(g)))
-            out["vy_grad"] = g.value
+        g, b0, b1 = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        if hasattr(lib(), "sf_get_tuning_modes"):  # (A/B builds of older revisions lack it)
+            check(lib().sf_get_tuning_modes(self._h, ctypes.byref(g), ctypes.byref(b0), ctypes.byref(b1)))
+            out.update(vy_grad=g.value, balance=b0.value, balance_grad=b1.value)
         return out
 
     @_ondev

@@ -66,17 +66,13 @@ cudaError_t launch_tma(const SfLaunch &L, const SfStepArgs &a, cudaStream_t st)
         }
     }
     int64_t g = std::min(tiles * nch, slots);
-    // balanced contiguous split (SF_OPT_BALANCE; kernel nchunk = 0): every CTA streams the
-    // same number of planes, at most ~2 segments (2 warm-ups) each.  Auto: r >= 5 only (FP-
-    // bound there: the halo rows its drifting neighbours re-read from HBM are affordable;
-    // at r <= 4 the kernel is HBM-bound) and when the chunked split wastes > 3 %.
-    if (!a.bidir && L.balance != 0 && slots >= 1) {
-        const int64_t gb = std::min<int64_t>(slots, tiles * PT);
-        const double tb = (double)((tiles * PT + gb - 1) / gb) + 2.0 * (2 * SF_R);
-        if (L.balance == 1 || (SF_R >= 5 && tb < 0.97 * best)) {
-            g = gb;
-            nch = 0;
-        }
+    // balanced contiguous split (SF_OPT_BALANCE / sf_autotune; kernel nchunk = 0): every CTA
+    // streams the same number of planes, at most ~2 segments (2 warm-ups) each -- faster where
+    // the tile count packs badly into the chunked rounds (configs[4], 8-warp layout: -4 %),
+    // much slower where the neighbours' re-read halo rows cost HBM time (configs[1], [3])
+    if (!a.bidir && L.balance == 1) {
+        g = std::min<int64_t>(slots, tiles * PT);
+        nch = 0;
     }
     dim3 block(32, C::THREADS / 32);  // NW consumer warps + the TMA producer warp(s)
     // programmatic dependent launch (SF_OPT_PDL): the CTAs' prologue (barrier init, tensor-map

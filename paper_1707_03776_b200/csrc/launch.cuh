@@ -22,7 +22,7 @@ struct SfLaunch {
     int snap_slot;    // GRAD: snapshot slot for the 4D snapshot tensor map
     int lz;           // TMA lane layout: 32 (128-column tiles) or 8 (narrow 32-column tiles)
     int pdl;          // launch with programmatic stream serialisation (SF_OPT_PDL)
-    int balance;      // TMA work split: 0 (tile, x-chunk) items, 1 balanced contiguous, 2 auto (SF_OPT_BALANCE)
+    int balance;      // TMA work split: 0 (tile, x-chunk) items, 1 balanced contiguous (SF_OPT_BALANCE)
     const SfTmaMaps *maps;
 };
 

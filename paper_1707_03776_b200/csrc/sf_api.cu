@@ -444,7 +444,7 @@ static sf_status launch_step(sf_handle *h, const StepBufs &b, int mode, cudaStre
     L.mode = mode;
     L.snap_slot = b.snap_slot;
     L.lz = 32;
-    L.balance = h->balance;
+    L.balance = (mode == SF_MODE_GRAD && h->balance_grad >= 0) ? h->balance_grad : h->balance;
     // PDL only after a standalone injection kernel: stencil -> stencil gains nothing measurable
     // (a persistent launch cannot co-reside with the previous one), and plain launches keep
     // the sampled event timing of the stencil exact
@@ -1099,6 +1099,7 @@ extern "C" sf_status sf_set_tuning(sf_handle *h, int variant, int vy, int ctas)
     h->variant = variant;
     h->vy = vy;
     h->vy_grad = 0;
+    h->balance_grad = -1;
     h->ctas = ctas;
     drop_graphs(h);
     return SF_OK;
@@ -1113,18 +1114,22 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
     if (!h || !u || steps < 1) return sf_set_error(SF_ERR_INVALID_ARG, "autotune: NULL handle/state or steps < 1");
     cudaStream_t st = S(stream);
     struct Cand {
-        int variant, vy, zsplit;
+        int variant, vy, zsplit, bal;
     };
     std::vector<Cand> cands;
     if (tma_ok(h)) {
-        cands.push_back({SF_VAR_TMA, 2, 1});
-        if (h->r >= 5) cands.push_back({SF_VAR_TMA, 2, 0});  // narrow remainder tiles off
-        cands.push_back({SF_VAR_TMA, 1, 1});
-        if (h->r >= 5 && h->ndim == 3) cands.push_back({SF_VAR_TMA, 3, 1});  // wide layout
-        cands.push_back({SF_VAR_TMA, 4, 1});  // warp-specialised 8-consumer-warp layout
+        // the balanced work split only where the kernel is FP-bound (r >= 5): at r <= 4 its
+        // re-read halo rows cost HBM time (configs[1]: 0.150 vs 0.121 ms)
+        for (int bal = 0; bal <= (h->r >= 5 ? 1 : 0); ++bal) {
+            cands.push_back({SF_VAR_TMA, 2, 1, bal});
+            if (h->r >= 5) cands.push_back({SF_VAR_TMA, 2, 0, bal});  // narrow remainder tiles off
+            cands.push_back({SF_VAR_TMA, 1, 1, bal});
+            if (h->r >= 5 && h->ndim == 3) cands.push_back({SF_VAR_TMA, 3, 1, bal});  // wide layout
+            cands.push_back({SF_VAR_TMA, 4, 1, bal});  // warp-specialised 8-consumer-warp layout
+        }
     }
-    cands.push_back({SF_VAR_GENERIC, 0, 1});
-    const Cand keep{h->variant, h->vy, h->zsplit ? 1 : 0};
+    cands.push_back({SF_VAR_GENERIC, 0, 1, 0});
+    const Cand keep{h->variant, h->vy, h->zsplit ? 1 : 0, h->balance};
     const bool keep_prof = h->prof;
     h->prof = false;
     cudaEvent_t e0, e1;
@@ -1138,6 +1143,8 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
         h->variant = cands[c].variant;
         h->vy = cands[c].vy;
         h->zsplit = cands[c].zsplit != 0;
+        h->balance = cands[c].bal;
+        h->balance_grad = -1;
         for (int it = -2; it < steps && !s; ++it) {  // two untimed warm-up steps
             if (it == 0) SF_CUDA_TRY(cudaEventRecord(e0, st));
             StepBufs b{};
@@ -1161,15 +1168,19 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
     h->variant = pick.variant;
     h->vy = pick.vy;
     h->zsplit = pick.zsplit != 0;
+    h->balance = pick.bal;
     h->vy_grad = 0;
+    h->balance_grad = -1;
     // GRAD-mode steps (the gradient's adjoint: snapshot and gradient planes streamed beside
     // the stencil) get their own layout: time the TMA layouts with the winner's z split in GRAD
     // mode on the same scratch state (snapshot = the current level, gradient = the output
     // buffer: the values are scratch, only the time counts)
     float best_g = 1e30f;
     if (!s && pick.variant == SF_VAR_TMA && h->ndim == 3) {
-        for (int vg : {2, 4}) {
+        for (int cg = 0; cg < (h->r >= 5 ? 4 : 2); ++cg) {
+            const int vg = (cg & 1) ? 4 : 2, bg = cg >> 1;
             h->vy = vg;
+            h->balance = bg;
             for (int it = -2; it < steps && !s; ++it) {
                 if (it == 0) SF_CUDA_TRY(cudaEventRecord(e0, st));
                 StepBufs b{};
@@ -1192,9 +1203,11 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
             if (ms < best_g) {
                 best_g = ms;
                 h->vy_grad = vg;
+                h->balance_grad = bg;
             }
         }
         h->vy = pick.vy;
+        h->balance = pick.bal;
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -1282,8 +1295,9 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
         drop_graphs(h);
         return SF_OK;
     case SF_OPT_BALANCE:
-        if (value < 0 || value > 2) return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_BALANCE %d", value);
+        if (value < 0 || value > 1) return sf_set_error(SF_ERR_INVALID_ARG, "SF_OPT_BALANCE %d", value);
         h->balance = value;
+        h->balance_grad = -1;
         drop_graphs(h);
         return SF_OK;
     case SF_OPT_TBLOCK:
@@ -1308,10 +1322,13 @@ extern "C" sf_status sf_set_option(sf_handle *h, int option, int value)
     }
 }
 
-extern "C" sf_status sf_get_grad_tuning(const sf_handle *h, int *vy)
+extern "C" sf_status sf_get_tuning_modes(const sf_handle *h, int *vy_grad, int *balance, int *balance_grad)
 {
-    if (!h || !vy) return sf_set_error(SF_ERR_INVALID_ARG, "handle or vy is NULL");
-    *vy = resolve_variant(h) == SF_VAR_TMA ? resolve_vy(h, SF_MODE_GRAD) : 0;
+    if (!h) return sf_set_error(SF_ERR_INVALID_ARG, "handle is NULL");
+    const bool tma = resolve_variant(h) == SF_VAR_TMA;
+    if (vy_grad) *vy_grad = tma ? resolve_vy(h, SF_MODE_GRAD) : 0;
+    if (balance) *balance = tma ? h->balance : 0;
+    if (balance_grad) *balance_grad = tma ? (h->balance_grad >= 0 ? h->balance_grad : h->balance) : 0;
     return SF_OK;
 }
 

@@ -77,7 +77,8 @@ struct sf_handle {
     // tuning
     int variant = SF_VAR_AUTO, vy = 0, ctas = 0;
     int vy_grad = 0;                // TMA layout of GRAD-mode steps (0: as vy; set by sf_autotune)
-    int balance = 2;                // TMA work split (SF_OPT_BALANCE): 0 chunked, 1 balanced, 2 auto
+    int balance = 0;                // TMA work split (SF_OPT_BALANCE): 0 chunked, 1 balanced
+    int balance_grad = -1;          // ... of GRAD-mode steps (-1: as balance; set by sf_autotune)
     int l2_prefetch = 0;            // TMA L2 prefetch distance (planes, 0 = off); env SF_L2_PREFETCH
     // slab decomposition
     int rank = 0, nranks = 1;

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--grad", action="store_true", help="time the adjoint with fused gradient")
     ap.add_argument("--sep", action="store_true", help="separable damping profiles (16 B/pt)")
     ap.add_argument("--prefetch", default="0", help="comma list of L2 prefetch distances (planes)")
+    ap.add_argument("--balance", default="0", help="comma list of SF_OPT_BALANCE values (0 chunked, 1 balanced)")
     ap.add_argument("--random-init", action="store_true",
                     help="start from a random (incompressible) wavefield instead of zeros")
     args = ap.parse_args()
@@ -44,12 +45,14 @@ def main():
         k = p.save_every or 4
         _, _, snaps = prop.forward(wav, save_every=k)
         res = torch.randn((p.nt, p.rec_coords.shape[0]), device="cuda")
-    for vy, ch, pf in itertools.product([int(x) for x in args.vy.split(",")],
-                                        [int(x) for x in args.ctas.split(",")],
-                                        [int(x) for x in args.prefetch.split(",")]):
+    for vy, ch, pf, bal in itertools.product([int(x) for x in args.vy.split(",")],
+                                             [int(x) for x in args.ctas.split(",")],
+                                             [int(x) for x in args.prefetch.split(",")],
+                                             [int(x) for x in args.balance.split(",")]):
         try:
             prop.set_tuning(2, vy, ch)
             prop.set_option(1, pf)
+            prop.set_option(sf.SF_OPT_BALANCE, bal)
         except sf.SfError:
             continue
         t = prop.tuning()
@@ -69,7 +72,7 @@ def main():
         ms = pr["stencil_ms"] / pr["stencil_launches"]
         extra = (4 + 12 / k) if args.grad else 0
         gbs = (bpp + extra) * N / (ms * 1e-3) / 1e9
-        row = {"vy": t["vy"], "ctas": t["ctas"], "req_ctas": ch, "prefetch": pf, "launch_ms": round(ms, 5),
+        row = {"vy": t["vy"], "ctas": t["ctas"], "req_ctas": ch, "prefetch": pf, "balance": bal, "launch_ms": round(ms, 5),
                "interp_us": round(pr["interp_ms"] * 1e3 / max(pr["interp_launches"], 1), 2),
                "GBps": round(gbs, 1), "GPts": round(N / (ms * 1e-3) / 1e9, 2)}
         print(json.dumps(row), flush=True)

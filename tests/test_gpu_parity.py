@@ -1242,6 +1242,7 @@ def test_autotune_picks_a_configuration_same_bits(shape, so):
     tun = prop.tuning()
     assert tun["variant"] == t["variant"]
     assert tun["vy_grad"] in ((2, 4) if t["variant"] == 2 else (0,))
+    assert tun["balance"] in (0, 1) and tun["balance_grad"] in (0, 1)
     rec, u, _ = prop.forward(dev(p.wavelet))
     g, J = prop.gradient(dev(p.wavelet), dev(d_obs), save_every=2)
     torch.cuda.synchronize()
