@@ -17,9 +17,20 @@ timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/e
 CMD="python bench.py --steps 1 --warmup 3 --nt 40 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/ev/plain_bench.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -s 150 -c 150 --csv --log-file gpurun_out/ev/launches.csv $CMD > gpurun_out/ev/ncu_launch.log 2>&1
+# the layout / work split sf_autotune picks in bench.py for each config (the "kernel_tuning" of
+# its bench line): configs[1] 7-warp chunked, [3] 8-warp chunked, [4] 8-warp balanced
+declare -A TUNE=([1]="--vy 2 --balance 0" [3]="--vy 4 --balance 0" [4]="--vy 4 --balance 1")
+# points x algorithmic bytes per point of the captured launch (configs[4]: its 128-column launch)
+declare -A PTS=([1]="37933056 20" [3]="268435456 16" [4]="61440000 16")
+mkdir -p /tmp/ev
 for c in 1 3 4; do
-CMD2="python scripts/tune.py --config $c --nt 8 --random-init --vy 2 --ctas 0"
+CMD2="python scripts/tune.py --config $c --nt 8 --random-init ${TUNE[$c]} --ctas 0"
 $CMD2 > gpurun_out/ev/plain_tune_c$c.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_tma3d -s 4 -c 1 -o gpurun_out/ev/prof_${R}_c$c $CMD2 > gpurun_out/ev/ncu_full_c$c.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_tma3d -s 4 -c 1 -o /tmp/ev/prof_${R}_c$c $CMD2 > gpurun_out/ev/ncu_full_c$c.log 2>&1
 tail -1 gpurun_out/ev/ncu_full_c$c.log
+# summaries on the box (the reports themselves exceed the 64 MiB merge-back)
+set -- ${PTS[$c]}
+python scripts/ncu_summary.py full /tmp/ev/prof_${R}_c$c.ncu-rep gpurun_out/ev/${R}_stencil_ncu_c$c.json --points $1 --bytes-per-point $2
+python scripts/ncu_quick.py /tmp/ev/prof_${R}_c$c.ncu-rep > gpurun_out/ev/${R}_stencil_ncu_c${c}_quick.txt 2>&1
 done
+python scripts/ncu_summary.py launches gpurun_out/ev/launches.csv gpurun_out/ev/${R}_bench_launches.json
