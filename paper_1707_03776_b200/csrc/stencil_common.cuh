@@ -9,11 +9,12 @@
 //   X  = sum_{k=1..r} w_k * ( (x_-k + x_+k) - 2 u )
 //   Lap = P + X,  w_k = fp32(w_k^exact / h^2)
 // so that a constant field is annihilated exactly (4u and 2u are exact) and the fp32
-// weights never need to sum to zero.  3D, r >= 5, outside the gradient's GRAD mode: the
-// MERGED form (sf_merged3 below) -- one chain over the three axes per radius,
+// weights never need to sum to zero.  3D, outside the gradient's GRAD mode: the MERGED form
+// (sf_merged3 below) -- one chain over the three axes per radius,
 //   L  = sum_{k=1..r} w_k * fma(-6, u, ((y_-k + y_+k) + (z_-k + z_+k)) + (x_-k + x_+k))
 // 7 instead of 8 FP operations per radius (the kernel is FP-issue bound at high order:
-// configs[4] -7 %), still exact on a constant field: the FMA forms 6u exactly inside.  (An
+// configs[4] -7 %; at r = 4 under the power cap +1 %), still exact on a constant field: the
+// FMA forms 6u exactly inside.  (An
 // earlier chain that subtracted a separately rounded fl(6u) doubled the fp32 error --
 // configs[2] gradient 1.9e-4 vs 3.8e-5; the gradient's in-kernel
 // S = out - 2u + old is the most sensitive use of L, so GRAD mode keeps the per-axis form.)
@@ -66,9 +67,15 @@ __device__ __forceinline__ float sf_inplane2(float zm, float zp, float u)
 #ifndef SF_MERGED
 #define SF_MERGED 1
 #endif
+#ifndef SF_MERGED_GRAD
+#define SF_MERGED_GRAD 0
+#endif
+#ifndef SF_MERGED_RMIN
+#define SF_MERGED_RMIN 1
+#endif
 __host__ __device__ constexpr bool sf_merged_form(int r, int mode)
 {
-    return SF_MERGED && r >= 5 && mode != SF_MODE_GRAD;
+    return SF_MERGED && r >= SF_MERGED_RMIN && (SF_MERGED_GRAD || mode != SF_MODE_GRAD);
 }
 __device__ __forceinline__ float sf_merged3(float ym, float yp, float zm, float zp, float xm, float xp, float u)
 {

@@ -105,6 +105,8 @@ k_tb2(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtens
     for (int k = 1; k <= R; ++k) Wk[k] = pk2(a.w.w[k], a.w.w[k]);
     Wk[0] = 0ull;
     const f2_t M4 = pk2(-4.f, -4.f), M2 = pk2(-2.f, -2.f), M1 = pk2(-1.f, -1.f), ONE2 = pk2(1.f, 1.f);
+    const f2_t M6 = pk2(-6.f, -6.f);
+    constexpr bool MRG = sf_merged_form(R, SF_MODE_PLAIN);  // as the single-step forward
     const int64_t plane = (int64_t)a.n1 * a.n2;
     const uint32_t ub = smem_u32(uring), cb = smem_u32(cring);
     f2_t V[Q][2][2];   // own u^n values (rows eA, eB; 2 pairs) at the last Q planes
@@ -220,13 +222,18 @@ k_tb2(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtens
                                 f2_t zs;
                                 if (k & 1) zs = pk2(__fadd_rn(F(em), F(ep)), __fadd_rn(F(em + 1), F(ep + 1)));
                                 else zs = add2(PZ(em), PZ(ep));
-                                P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
+                                if constexpr (MRG)  // merged form (== sf_merged3 per lane)
+                                    P = fma2(Wk[k], fma2(M6, u, add2(add2(ys, zs), add2(V[(SQ - k + Q) % Q][j][jp], V[(SQ + k) % Q][j][jp]))), P);
+                                else
+                                    P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
                             }
                             f2_t X = 0ull;
+                            if constexpr (!MRG) {
 #pragma unroll
-                            for (int k = 1; k <= R; ++k)
-                                X = fma2(Wk[k], sf_xterm_x2(V[(SQ - k + Q) % Q][j][jp], V[(SQ + k) % Q][j][jp], u, M2), X);
-                            const f2_t lap = add2(P, X);
+                                for (int k = 1; k <= R; ++k)
+                                    X = fma2(Wk[k], sf_xterm_x2(V[(SQ - k + Q) % Q][j][jp], V[(SQ + k) % Q][j][jp], u, M2), X);
+                            }
+                            const f2_t lap = MRG ? P : add2(P, X);
                             const f2_t d = fma2(M1, ov[jp], u);
                             res[j][jp] = fma2(cv[jp], lap, fma2(bv[jp], d, u));
                         }
@@ -302,12 +309,17 @@ k_tb2(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUtens
                             f2_t zs;
                             if (k & 1) zs = pk2(__fadd_rn(F(em), F(ep)), __fadd_rn(F(em + 1), F(ep + 1)));
                             else zs = add2(PZ(em), PZ(ep));
-                            P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
+                            if constexpr (MRG)
+                                P = fma2(Wk[k], fma2(M6, u, add2(add2(ys, zs), add2(XM[k][jp], XP[k][jp]))), P);
+                            else
+                                P = fma2(Wk[k], fma2(M4, u, add2(ys, zs)), P);
                         }
                         f2_t X = 0ull;
+                        if constexpr (!MRG) {
 #pragma unroll
-                        for (int k = 1; k <= R; ++k) X = fma2(Wk[k], sf_xterm_x2(XM[k][jp], XP[k][jp], u, M2), X);
-                        const f2_t lap = add2(P, X);
+                            for (int k = 1; k <= R; ++k) X = fma2(Wk[k], sf_xterm_x2(XM[k][jp], XP[k][jp], u, M2), X);
+                        }
+                        const f2_t lap = MRG ? P : add2(P, X);
                         const f2_t d = fma2(M1, V[SO][0][jp], u);
                         const f2_t bb = DAMP ? bev[jp] : ONE2;
                         res[jp] = fma2(c3v[jp], lap, fma2(bb, d, u));
