@@ -9,12 +9,13 @@
 //   X  = sum_{k=1..r} w_k * ( (x_-k + x_+k) - 2 u )
 //   Lap = P + X,  w_k = fp32(w_k^exact / h^2)
 // so that a constant field is annihilated exactly (4u and 2u are exact) and the fp32
-// weights never need to sum to zero.  3D, outside the gradient's GRAD mode: the MERGED form
-// (sf_merged3 below) -- one chain over the three axes per radius,
+// weights never need to sum to zero.  3D, r >= 5, outside the gradient's GRAD mode: the
+// MERGED form (sf_merged3 below) -- one chain over the three axes per radius,
 //   L  = sum_{k=1..r} w_k * fma(-6, u, ((y_-k + y_+k) + (z_-k + z_+k)) + (x_-k + x_+k))
 // 7 instead of 8 FP operations per radius (the kernel is FP-issue bound at high order:
-// configs[4] -7 %; at r = 4 under the power cap +1 %), still exact on a constant field: the
-// FMA forms 6u exactly inside.  (An
+// configs[4] -7 %), still exact on a constant field: the FMA forms 6u exactly inside.  (At
+// r = 4 it gained 1 % under the power cap but doubled the configs[2] full-size gradient error,
+// 3.8e-5 -> 7.0e-5: SF_MERGED_RMIN stays 5.)  (An
 // earlier chain that subtracted a separately rounded fl(6u) doubled the fp32 error --
 // configs[2] gradient 1.9e-4 vs 3.8e-5; the gradient's in-kernel
 // S = out - 2u + old is the most sensitive use of L, so GRAD mode keeps the per-axis form.)
@@ -71,7 +72,7 @@ __device__ __forceinline__ float sf_inplane2(float zm, float zp, float u)
 #define SF_MERGED_GRAD 0
 #endif
 #ifndef SF_MERGED_RMIN
-#define SF_MERGED_RMIN 1
+#define SF_MERGED_RMIN 5
 #endif
 __host__ __device__ constexpr bool sf_merged_form(int r, int mode)
 {

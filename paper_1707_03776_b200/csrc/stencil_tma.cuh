@@ -332,7 +332,7 @@ k_tma3d(const __grid_constant__ CUtensorMap tm_cur, const __grid_constant__ CUte
     constexpr int VZ = C::VZ, NJ = VZ / 2, NW = C::NW, BY = C::BY, TZ = C::TZ, HZ = C::HZ;
     constexpr int Q = C::Q, W = C::W, DU = C::DU, DC = C::DC;
     // merged Laplacian form (sf_merged3: one chain over the three axes per radius, 7 instead
-    // of 8 FP operations) outside the gradient's GRAD mode (stencil_common.cuh)
+    // of 8 FP operations) at r >= 5 outside the gradient's GRAD mode (stencil_common.cuh)
     constexpr bool MRG = sf_merged_form(R, MODE);
     const int PD = a.l2_prefetch;  // planes of L2 prefetch beyond the smem ring (0 = off)
     // slot release by the consumers: one arrive per warp (lane 0, after __syncwarp).  Per-
