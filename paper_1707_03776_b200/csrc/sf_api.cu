@@ -1173,9 +1173,24 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
     h->balance_grad = -1;
     // GRAD-mode steps (the gradient's adjoint: snapshot and gradient planes streamed beside
     // the stencil) get their own layout: time the TMA layouts with the winner's z split in GRAD
-    // mode on the same scratch state (snapshot = the current level, gradient = the output
-    // buffer: the values are scratch, only the time counts)
+    // mode on the same scratch state, with a snapshot and a gradient buffer of their own
+    // (zeroed scratch: only the time counts).  Aliasing them to the state's two levels, as
+    // an earlier form did, hid their 12 B/pt of HBM traffic in L2 and could pick a layout
+    // whose traffic is 1.4x the algorithmic bytes in the real adjoint (configs[4], ncu:
+    // profiles/r02_step_traffic_c4.json); the aliased form stays as the fallback when the
+    // scratch allocation fails.
     float best_g = 1e30f;
+    float *gsc = nullptr;
+    if (!s && pick.variant == SF_VAR_TMA && h->ndim == 3) {
+        if (cudaMalloc(&gsc, 2 * (size_t)h->N * sizeof(float)) != cudaSuccess) {
+            cudaGetLastError();
+            gsc = nullptr;
+        } else if (cudaMemsetAsync(gsc, 0, 2 * (size_t)h->N * sizeof(float), st) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(gsc);
+            gsc = nullptr;
+        }
+    }
     if (!s && pick.variant == SF_VAR_TMA && h->ndim == 3) {
         for (int cg = 0; cg < (h->r >= 5 ? 4 : 2); ++cg) {
             const int vg = (cg & 1) ? 4 : 2, bg = cg >> 1;
@@ -1186,10 +1201,10 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
                 StepBufs b{};
                 b.cur = (it & 1) ? A : B;
                 b.out = (it & 1) ? B : A;
-                b.snaps = b.cur;
+                b.snaps = gsc ? gsc : b.cur;
                 b.nsnap = 1;
                 b.snap_slot = 0;
-                b.grad = b.out;
+                b.grad = gsc ? gsc + h->N : b.out;
                 b.gscale = 0.0f;
                 bool fused = false;
                 s = launch_step(h, b, SF_MODE_GRAD, st, &fused);
@@ -1209,6 +1224,7 @@ extern "C" sf_status sf_autotune(sf_handle *h, float *u, int steps, int *chosen,
         h->vy = pick.vy;
         h->balance = pick.bal;
     }
+    if (gsc) cudaFree(gsc);  // (synchronises the device: setup time)
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     h->prof = keep_prof;
