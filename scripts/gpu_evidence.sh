@@ -34,3 +34,13 @@ python scripts/ncu_summary.py full /tmp/ev/prof_${R}_c$c.ncu-rep gpurun_out/ev/$
 python scripts/ncu_quick.py /tmp/ev/prof_${R}_c$c.ncu-rep > gpurun_out/ev/${R}_stencil_ncu_c${c}_quick.txt 2>&1
 done
 python scripts/ncu_summary.py launches gpurun_out/ev/launches.csv gpurun_out/ev/${R}_bench_launches.json
+# gradient configs: DRAM traffic of every stencil launch of one timed step (NVTX range sf_timed:
+# the setup-time tuning runs unprofiled), weighted per mode to the full config's average update
+for c in 2 4; do
+CMD3="python bench.py --config $c --nt 41 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
+$CMD3 > gpurun_out/ev/plain_step_c$c.log 2>&1 && \
+ncu --nvtx --nvtx-include "sf_timed/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+    --clock-control none -k regex:k_tma3d --csv --log-file gpurun_out/ev/${R}_step_traffic_c$c.csv $CMD3 > gpurun_out/ev/ncu_step_c$c.log 2>&1
+L=1; [ $c = 4 ] && L=2
+python scripts/ncu_step_traffic.py gpurun_out/ev/${R}_step_traffic_c$c.csv gpurun_out/ev/${R}_step_traffic_c$c.json --config $c --nt-run 41 --launches-per-update $L
+done
